@@ -1,0 +1,145 @@
+/*
+ * bcss_sttsm.h — C ABI of the B200-native BCSS change of basis ("sttsm").
+ *
+ * Computes C = [A; X, ..., X] = A x_0 X x_1 X ... x_{m-1} X for a symmetric
+ * order-m tensor A (dimension n) held in Blocked Compact Symmetric Storage,
+ * with the algorithm-by-blocks that reuses partially-symmetric temporaries.
+ * This is the drop-in for the reference hot path
+ *   blocksym.sttsm_bcss(a, x, b_c, counter, reuse, temp_hook)
+ *   (/root/reference/pkg/src/blocksym/change_of_basis.py:239-284).
+ *
+ * Buffer contract (identical to the reference's .bcss payload,
+ * /root/reference/pkg/src/blocksym/io.py:50-55):
+ *   A_packed : simplex_count(n/b_a, m) canonical blocks in hypertriangle
+ *              (lexicographic, nondecreasing-index) order, each b_a^m doubles
+ *              in dimensional (Fortran) order.
+ *   X        : p x n doubles, row-major (numpy C-order; the reference slices
+ *              x[jb*b_c:(jb+1)*b_c, ib*b_a:(ib+1)*b_a], change_of_basis.py:229).
+ *   C_packed : simplex_count(p/b_c, m) blocks of b_c^m doubles, same order.
+ *
+ * No torch or CUDA types appear in the signatures: streams are passed as
+ * void* (a cudaStream_t), device buffers as plain pointers.  Functions return
+ * BCSS_OK (0) or a status code; bcss_last_error() holds the message of the
+ * last failure on the calling thread.  Nothing throws across the ABI.
+ */
+#ifndef BCSS_STTSM_H
+#define BCSS_STTSM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The Python host layer maps them onto the reference's
+ * exception types (/root/reference/pkg/src/blocksym/errors.py:4-25). */
+enum bcss_status {
+  BCSS_OK = 0,
+  BCSS_ERR_PARAMETER = 1,          /* ParameterError (e.g. m < 2, change_of_basis.py:56-57) */
+  BCSS_ERR_SHAPE = 2,              /* ShapeError (dims / X shape, change_of_basis.py:58-62) */
+  BCSS_ERR_BLOCK_DIVISIBILITY = 3, /* BlockDivisibilityError (change_of_basis.py:264-265) */
+  BCSS_ERR_RANGE = 4,              /* RangeError (index outside the grid, storage.py:131-133) */
+  BCSS_ERR_CUDA = 5,               /* CUDA runtime failure (device, launch, memory) */
+  BCSS_ERR_NOMEM = 6,              /* workspace does not fit */
+  BCSS_ERR_STATE = 7               /* API misuse (null plan, missing workspace, ...) */
+};
+
+typedef struct bcss_plan bcss_plan; /* opaque */
+
+/* Message of the last failure on this thread ("" if none). */
+const char* bcss_last_error(void);
+/* ABI version of this library (major*100 + minor). */
+int bcss_abi_version(void);
+
+/* ---- combinatorics and cost model (host only, no GPU needed) ------------- */
+
+/* C(extent+m-1, m): number of nondecreasing m-tuples over 0..extent-1.
+ * Replaces simplex_count (indexing.py:64-68). Returns -1 on bad arguments. */
+int64_t bcss_simplex_count(int64_t extent, int m);
+
+/* Lexicographic rank of the nondecreasing tuple idx[0..m-1] among
+ * hypertriangle_iter(extent, m) (indexing.py:57-61); this is the block's
+ * position in a packed payload. */
+int bcss_hypertriangle_rank(const int64_t* idx, int m, int64_t extent, int64_t* out_rank);
+
+/* Inverse of bcss_hypertriangle_rank: the rank-th nondecreasing tuple. */
+int bcss_hypertriangle_unrank(int64_t rank, int m, int64_t extent, int64_t* out_idx);
+
+/* Exact flop count of the blocked algorithm, bcss_costs(...).flops
+ * (costs.py:83-112): 2*nbar*b_c*b_a^m * sum_d C(pbar+d,d+1)*blocks(d)*(b_c/b_a)^d.
+ * reuse=0 selects the plain algorithm-by-blocks count. */
+int bcss_blocked_flops(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int reuse,
+                       uint64_t* out_flops);
+
+/* ---- plans ---------------------------------------------------------------- */
+
+/* Validate the problem (change_of_basis.py:54-63, 259-266) and build the
+ * level/work-list plan.  reuse=1 is the reference default (canonical blocks of
+ * every temporary only); reuse=0 materializes every temporary block
+ * (_DenseBlockTable, change_of_basis.py:157-167). */
+int bcss_plan_create(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int reuse,
+                     bcss_plan** out_plan);
+int bcss_plan_destroy(bcss_plan* plan);
+
+/* Restrict the plan to a subset of the top-level output block rows
+ * ("units": values of jb_{m-1}, the outermost loop of descend,
+ * change_of_basis.py:269-283).  Only the C blocks whose largest block index
+ * lies in the subset are written.  Used to shard C across GPUs. */
+int bcss_plan_set_units(bcss_plan* plan, const int32_t* units, int n_units);
+
+/* Upper bound on workspace bytes; the plan processes the units in waves so
+ * that live temporaries fit.  0 = no limit. */
+int bcss_plan_set_workspace_limit(bcss_plan* plan, size_t bytes);
+
+/* Keep every temporary of every level resident (for temp_hook replays). */
+int bcss_plan_set_keep_temps(bcss_plan* plan, int keep);
+
+/* Device workspace the plan needs (temporaries + tables) for its settings. */
+int bcss_plan_workspace_bytes(bcss_plan* plan, size_t* out_bytes);
+
+/* Caller-provided device workspace (>= bcss_plan_workspace_bytes).  Without
+ * it the plan allocates its own with cudaMalloc on first run. */
+int bcss_plan_set_workspace(bcss_plan* plan, void* dev_ptr, size_t bytes);
+
+/* Plan statistics: waves, kernel launches per run, exact flops of the
+ * assigned units, and number of C blocks written. */
+int bcss_plan_stats(bcss_plan* plan, int64_t* waves, int64_t* launches, uint64_t* flops,
+                    int64_t* c_blocks);
+
+/* ---- execution ------------------------------------------------------------ */
+
+/* Device-resident run: A_packed, X, C_packed are device pointers; the work is
+ * enqueued on `stream` (cudaStream_t, NULL = legacy default) and returns
+ * without synchronizing. */
+int bcss_sttsm_run(bcss_plan* plan, const double* A_packed, const double* X, double* C_packed,
+                   void* stream);
+
+/* Host-buffer run (the reference's call shape): copies A and X to the device,
+ * runs, copies C back and synchronizes.  Pinned host memory gives full
+ * PCIe bandwidth; pageable memory works too. */
+int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X,
+                        double* C_packed);
+
+/* Device pointer and element count of the temporary T(k) produced for the
+ * call whose suffix is (jb_k, ..., jb_{m-1}) (nondecreasing, m-k entries),
+ * valid after a run with keep_temps=1.  Blocks are canonical keys in
+ * hypertriangle order (reuse=1) or all keys in product order (reuse=0), each
+ * b_a^k * b_c^(m-k) doubles in the reference's block layout
+ * (a_0..a_{k-1}, c_k..c_{m-1}), Fortran order (change_of_basis.py:231-235). */
+int bcss_plan_temp(bcss_plan* plan, int k, const int32_t* suffix, const double** out_ptr,
+                   int64_t* out_elems);
+
+/* Copy that temporary to host memory (elems must equal the temporary's size);
+ * synchronizes the device. */
+int bcss_plan_temp_copy(bcss_plan* plan, int k, const int32_t* suffix, double* host_out,
+                        int64_t elems);
+
+/* Number of user kernels the last run launched. */
+int bcss_plan_last_launches(bcss_plan* plan, int64_t* out_launches);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* BCSS_STTSM_H */

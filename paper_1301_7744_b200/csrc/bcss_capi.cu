@@ -1,0 +1,654 @@
+// C ABI of the B200-native BCSS sttsm (declared in include/bcss_sttsm.h).
+//
+// Host side: problem validation (change_of_basis.py:54-63, 259-266), the
+// level/work-list plan that replaces the reference's depth-first `descend`
+// (change_of_basis.py:269-283) by breadth-first levels over "waves" of
+// top-level units, workspace management and kernel launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/bcss_sttsm.h"
+#include "combinatorics.hpp"
+#include "sttsm_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(BCSS_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));        \
+  } while (0)
+
+bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+int ilog2(int64_t v) { int r = 0; while ((int64_t(1) << r) < v) ++r; return r; }
+int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; return r; }
+
+// ---- kernel configurations ----------------------------------------------------
+using FastK = bcss::LevelKernel<128, 128, 32, 2, 4, 3, true>;
+using GenK = bcss::LevelKernel<32, 64, 16, 2, 2, 2, false>;
+
+template <class K>
+__global__ void __launch_bounds__(K::NT, 1) level_kernel(const bcss::LevelArgs a) { K::run(a); }
+
+struct KernelCfg {
+  int BM, BN, NT;
+  size_t smem;
+  void (*fn)(bcss::LevelArgs);
+};
+const KernelCfg kCfgs[] = {
+    {128, 128, FastK::NT, FastK::SMEM_BYTES, level_kernel<FastK>},
+    {32, 64, GenK::NT, GenK::SMEM_BYTES, level_kernel<GenK>},
+};
+enum { CFG_FAST = 0, CFG_GENERIC = 1 };
+
+}  // namespace
+
+// ---- plan ----------------------------------------------------------------------
+struct LevelHost {
+  int k = 0, cfg = 0;
+  int64_t keys_out = 0, keys_in = 0, blk_out = 0, blk_in = 0, rest = 0, bAk = 0;
+  int n_tiles = 0;
+  int64_t n_calls = 0;
+  std::vector<int4> parents;
+  std::vector<long long> item_off;
+  std::vector<int> child_call;
+  std::vector<int32_t> suffixes;  // n_calls x (m-k)
+  size_t off_parents = 0, off_items = 0, off_child = 0;  // into the device table buffer
+};
+
+struct WaveHost {
+  std::vector<int> units;
+  std::vector<LevelHost> levels;  // levels[i] has k = m-1-i
+};
+
+struct bcss_plan {
+  int m = 0;
+  int64_t n = 0, p = 0, bA = 0, bC = 0, nbar = 0, pbar = 0;
+  bool reuse = true;
+  std::vector<int> units;
+  bool units_set = false;
+  size_t ws_limit = 0;
+  bool keep_temps = false;
+
+  bool built = false;
+  std::vector<WaveHost> waves;
+  std::vector<std::vector<int2>> nbr;  // per k
+  std::vector<size_t> nbr_off;         // per k, into the table buffer
+  std::vector<size_t> region_bytes;    // ping-pong (2) or per level (m) when keep_temps
+  size_t ws_bytes = 0;
+  uint64_t flops = 0;
+  int64_t c_blocks = 0;
+
+  int device = -1;
+  void* d_tables = nullptr;
+  size_t tables_bytes = 0;
+  void* d_ws = nullptr;
+  size_t ws_capacity = 0;
+  bool own_ws = false;
+  double *hA = nullptr, *hX = nullptr, *hC = nullptr;  // device buffers for run_host
+  size_t hA_bytes = 0, hX_bytes = 0, hC_bytes = 0;
+  cudaStream_t host_stream = nullptr;
+  int64_t last_launches = 0;
+};
+
+namespace {
+
+int64_t keys_at(const bcss_plan& P, int k) {
+  if (k == 0) return 1;
+  if (k == P.m) return bcss::simplex_count(P.nbar, P.m);  // A is always BCSS
+  return P.reuse ? bcss::simplex_count(P.nbar, k) : ipow(P.nbar, k);
+}
+int64_t blk_at(const bcss_plan& P, int k) { return ipow(P.bA, k) * ipow(P.bC, P.m - k); }
+
+// Neighbour table of level k: for every output key K and every ib, the rank of
+// the stored block of T(k+1) that holds the logical block (K, ib) and the
+// redirection (stored position of each logical mode).  Reuse: K sorted,
+// stored = sorted(K u {ib}) with the canonicalize mapping (insertion).
+// No reuse: K runs over all k-tuples; T(k+1) below the top is itself a dense
+// block table (identity mapping), the top level redirects through A's BCSS.
+void build_nbr(bcss_plan& P, int k, std::vector<int2>& out) {
+  const int64_t nkeys = keys_at(P, k);
+  out.assign((size_t)(nkeys * P.nbar), int2{0, 0});
+  std::vector<int32_t> key(k), idx(k + 1), canon(k + 1), map(k + 1);
+  std::vector<int64_t> canon64(k + 1);
+  for (int64_t kr = 0; kr < nkeys; ++kr) {
+    if (k > 0) {
+      if (P.reuse) {
+        std::vector<int64_t> tmp(k);
+        bcss::hypertriangle_unrank(kr, k, P.nbar, tmp.data());
+        for (int d = 0; d < k; ++d) key[d] = (int32_t)tmp[d];
+      } else {
+        int64_t r = kr;
+        for (int d = k - 1; d >= 0; --d) { key[d] = (int32_t)(r % P.nbar); r /= P.nbar; }
+      }
+    }
+    for (int64_t ib = 0; ib < P.nbar; ++ib) {
+      for (int d = 0; d < k; ++d) idx[d] = key[d];
+      idx[k] = (int32_t)ib;
+      int64_t rank;
+      int pos;
+      if (P.reuse || k + 1 == P.m) {
+        bcss::canonical_mapping(idx.data(), k + 1, canon.data(), map.data());
+        for (int d = 0; d <= k; ++d) canon64[d] = canon[d];
+        rank = bcss::hypertriangle_rank(canon64.data(), k + 1, P.nbar);
+        pos = map[k];
+      } else {
+        rank = kr * P.nbar + ib;
+        for (int d = 0; d <= k; ++d) map[d] = d;
+        pos = k;
+      }
+      int code = pos;
+      for (int d = 0; d <= k; ++d) code |= map[d] << (4 + 3 * d);
+      out[(size_t)(kr * P.nbar + ib)] = int2{(int)rank, code};
+    }
+  }
+}
+
+// Calls (suffixes) of level k generated by the units in `units`:
+// number of nondecreasing (m-1-k)-tuples over [0, u] per unit u.
+int64_t calls_for(const bcss_plan& P, const std::vector<int>& units, int k) {
+  int64_t c = 0;
+  for (int u : units) c += (P.m - 1 - k == 0) ? 1 : bcss::simplex_count(u + 1, P.m - 1 - k);
+  return c;
+}
+
+std::vector<size_t> level_bytes(const bcss_plan& P, const std::vector<int>& units) {
+  std::vector<size_t> b(P.m, 0);
+  for (int k = 1; k < P.m; ++k)
+    b[k] = (size_t)calls_for(P, units, k) * keys_at(P, k) * blk_at(P, k) * sizeof(double);
+  return b;
+}
+
+size_t peak_for(const bcss_plan& P, const std::vector<int>& units) {
+  const auto b = level_bytes(P, units);
+  if (P.keep_temps) { size_t s = 0; for (auto v : b) s += v; return s; }
+  size_t r[2] = {0, 0};
+  for (int k = 1; k < P.m; ++k) r[(P.m - 1 - k) % 2] = std::max(r[(P.m - 1 - k) % 2], b[k]);
+  return r[0] + r[1];
+}
+
+void build_wave_levels(bcss_plan& P, WaveHost& W) {
+  const bool fast = P.reuse && is_pow2(P.bA) && P.bA >= 2 && is_pow2(P.bC);
+  W.levels.clear();
+  std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls
+  int64_t prev_calls = 0;
+  for (int k = P.m - 1; k >= 0; --k) {
+    LevelHost L;
+    L.k = k;
+    L.cfg = fast ? CFG_FAST : CFG_GENERIC;
+    L.keys_out = keys_at(P, k);
+    L.keys_in = keys_at(P, k + 1);
+    L.blk_out = blk_at(P, k);
+    L.blk_in = blk_at(P, k + 1);
+    L.bAk = ipow(P.bA, k);
+    L.rest = L.bAk * ipow(P.bC, P.m - 1 - k);
+    const KernelCfg& C = kCfgs[L.cfg];
+    L.n_tiles = (int)((L.rest + C.BN - 1) / C.BN);
+    const int sl = P.m - k;  // suffix length of this level's calls
+    long long items = 0;
+    auto add_parent = [&](int in_call, int row0, int rows, int child_off) {
+      L.parents.push_back(int4{in_call, row0, rows, child_off});
+      L.item_off.push_back(items);
+      items += (long long)L.keys_out * L.n_tiles * ((rows + C.BM - 1) / C.BM);
+    };
+    if (k == P.m - 1) {
+      for (size_t i = 0; i < W.units.size(); ++i) {
+        L.suffixes.push_back(W.units[i]);
+        L.child_call.push_back((int)i);
+      }
+      size_t s = 0;
+      while (s < W.units.size()) {
+        size_t e = s + 1;
+        while (e < W.units.size() && W.units[e] == W.units[e - 1] + 1) ++e;
+        add_parent(0, (int)(W.units[s] * P.bC), (int)((e - s) * P.bC), (int)s);
+        s = e;
+      }
+      L.n_calls = (int64_t)W.units.size();
+    } else {
+      int64_t running = 0;
+      std::vector<int64_t> full(P.m);
+      for (int64_t c = 0; c < prev_calls; ++c) {
+        const int32_t* sp = &prev_suffix[(size_t)(c * (sl - 1))];
+        const int J = sp[0];
+        add_parent((int)c, 0, (int)((J + 1) * P.bC), (int)running);
+        for (int jb = 0; jb <= J; ++jb) {
+          L.suffixes.push_back(jb);
+          for (int q = 0; q < sl - 1; ++q) L.suffixes.push_back(sp[q]);
+          if (k == 0) {
+            full[0] = jb;
+            for (int q = 0; q < sl - 1; ++q) full[q + 1] = sp[q];
+            L.child_call.push_back((int)bcss::hypertriangle_rank(full.data(), P.m, P.pbar));
+          } else {
+            L.child_call.push_back((int)running);
+          }
+          ++running;
+        }
+      }
+      L.n_calls = running;
+    }
+    L.item_off.push_back(items);
+    prev_suffix = L.suffixes;
+    prev_calls = L.n_calls;
+    W.levels.push_back(std::move(L));
+  }
+}
+
+int build_plan(bcss_plan& P) {
+  if (P.built) return BCSS_OK;
+  try {
+    std::vector<int> units = P.units;
+    if (!P.units_set)
+      for (int u = 0; u < P.pbar; ++u) units.push_back(u);
+    std::sort(units.begin(), units.end());
+    units.erase(std::unique(units.begin(), units.end()), units.end());
+    // waves: greedy groups of units whose live temporaries fit the limit
+    P.waves.clear();
+    std::vector<int> cur;
+    for (int u : units) {
+      std::vector<int> trial = cur;
+      trial.push_back(u);
+      if (!cur.empty() && !P.keep_temps && P.ws_limit > 0 && peak_for(P, trial) > P.ws_limit) {
+        P.waves.push_back(WaveHost{cur, {}});
+        cur = {u};
+      } else {
+        cur = trial;
+      }
+    }
+    if (!cur.empty()) P.waves.push_back(WaveHost{cur, {}});
+    if (!P.keep_temps && P.ws_limit > 0) {
+      for (auto& W : P.waves)
+        if (peak_for(P, W.units) > P.ws_limit)
+          return fail(BCSS_ERR_NOMEM, "one top-level unit needs %zu workspace bytes > limit %zu",
+                      peak_for(P, W.units), P.ws_limit);
+    }
+    // region sizes
+    if (P.keep_temps) {
+      P.region_bytes.assign(P.m, 0);
+      for (auto& W : P.waves) {
+        auto b = level_bytes(P, W.units);
+        for (int k = 1; k < P.m; ++k) P.region_bytes[k] = std::max(P.region_bytes[k], b[k]);
+      }
+    } else {
+      P.region_bytes.assign(2, 0);
+      for (auto& W : P.waves) {
+        auto b = level_bytes(P, W.units);
+        for (int k = 1; k < P.m; ++k) {
+          size_t& r = P.region_bytes[(P.m - 1 - k) % 2];
+          r = std::max(r, b[k]);
+        }
+      }
+    }
+    P.ws_bytes = 0;
+    for (auto& r : P.region_bytes) { r = (r + 255) / 256 * 256; P.ws_bytes += r; }
+    // tables
+    P.nbr.assign(P.m, {});
+    P.nbr_off.assign(P.m, 0);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+    for (int k = 0; k < P.m; ++k) {
+      build_nbr(P, k, P.nbr[k]);
+      P.nbr_off[k] = take(P.nbr[k].size() * sizeof(int2));
+    }
+    P.flops = 0;
+    P.c_blocks = 0;
+    for (auto& W : P.waves) {
+      build_wave_levels(P, W);
+      for (auto& L : W.levels) {
+        L.off_parents = take(L.parents.size() * sizeof(int4));
+        L.off_items = take(L.item_off.size() * sizeof(long long));
+        L.off_child = take(L.child_call.size() * sizeof(int));
+        P.flops += (uint64_t)2 * L.n_calls * P.bC * P.n * L.keys_out * L.rest;
+        if (L.k == 0) P.c_blocks += L.n_calls;
+      }
+    }
+    P.tables_bytes = off;
+    P.built = true;
+    return BCSS_OK;
+  } catch (const std::exception& e) {
+    return fail(BCSS_ERR_PARAMETER, "plan construction failed: %s", e.what());
+  }
+}
+
+int upload_tables(bcss_plan& P) {
+  int dev;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (P.d_tables && P.device == dev) return BCSS_OK;
+  if (P.d_tables) { cudaFree(P.d_tables); P.d_tables = nullptr; }
+  std::vector<char> host(P.tables_bytes, 0);
+  for (int k = 0; k < P.m; ++k)
+    if (!P.nbr[k].empty()) memcpy(&host[P.nbr_off[k]], P.nbr[k].data(), P.nbr[k].size() * sizeof(int2));
+  for (auto& W : P.waves)
+    for (auto& L : W.levels) {
+      memcpy(&host[L.off_parents], L.parents.data(), L.parents.size() * sizeof(int4));
+      memcpy(&host[L.off_items], L.item_off.data(), L.item_off.size() * sizeof(long long));
+      memcpy(&host[L.off_child], L.child_call.data(), L.child_call.size() * sizeof(int));
+    }
+  CUDA_TRY(cudaMalloc(&P.d_tables, std::max<size_t>(P.tables_bytes, 256)));
+  CUDA_TRY(cudaMemcpy(P.d_tables, host.data(), P.tables_bytes, cudaMemcpyHostToDevice));
+  P.device = dev;
+  static bool attr_done[64] = {false};
+  if (dev < 64 && !attr_done[dev]) {
+    for (const auto& C : kCfgs)
+      CUDA_TRY(cudaFuncSetAttribute(C.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
+    attr_done[dev] = true;
+  }
+  return BCSS_OK;
+}
+
+int ensure_workspace(bcss_plan& P) {
+  if (P.ws_bytes == 0) return BCSS_OK;
+  if (P.d_ws && P.ws_capacity >= P.ws_bytes) return BCSS_OK;
+  if (P.d_ws && !P.own_ws)
+    return fail(BCSS_ERR_STATE, "caller workspace of %zu bytes < required %zu", P.ws_capacity, P.ws_bytes);
+  if (P.d_ws) cudaFree(P.d_ws);
+  P.d_ws = nullptr;
+  cudaError_t e = cudaMalloc(&P.d_ws, P.ws_bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BCSS_ERR_NOMEM, "cudaMalloc of %zu workspace bytes failed: %s", P.ws_bytes, cudaGetErrorString(e));
+  }
+  P.ws_capacity = P.ws_bytes;
+  P.own_ws = true;
+  return BCSS_OK;
+}
+
+double* region_for(bcss_plan& P, int k) {
+  char* base = static_cast<char*>(P.d_ws);
+  if (P.keep_temps) {
+    size_t off = 0;
+    for (int q = 0; q < k; ++q) off += P.region_bytes[q];
+    return reinterpret_cast<double*>(base + off);
+  }
+  return reinterpret_cast<double*>(base + ((P.m - 1 - k) % 2 == 0 ? 0 : P.region_bytes[0]));
+}
+
+int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c) {
+  if (m < 2) return fail(BCSS_ERR_PARAMETER, "change of basis is defined for order >= 2");
+  if (m > 8) return fail(BCSS_ERR_PARAMETER, "order %d > 8 is not supported", m);
+  if (n < 1 || p < 1 || b_a < 1 || b_c < 1)
+    return fail(BCSS_ERR_PARAMETER, "dimensions and block dimensions must be positive");
+  if (n % b_a != 0) return fail(BCSS_ERR_BLOCK_DIVISIBILITY, "block dimension %lld does not divide %lld", (long long)b_a, (long long)n);
+  if (p % b_c != 0) return fail(BCSS_ERR_BLOCK_DIVISIBILITY, "output block dimension %lld does not divide %lld", (long long)b_c, (long long)p);
+  // int32 limits of the device tables and per-block offsets
+  const double blk = std::pow((double)std::max(b_a, b_c), m);
+  if (blk >= 2147483647.0) return fail(BCSS_ERR_PARAMETER, "block of %g elements exceeds the int32 block offset range", blk);
+  if (n > (1 << 30) || p > (1 << 30)) return fail(BCSS_ERR_PARAMETER, "dimension too large");
+  return BCSS_OK;
+}
+
+}  // namespace
+
+// ---- C ABI -----------------------------------------------------------------------
+extern "C" {
+
+const char* bcss_last_error(void) { return g_last_error.c_str(); }
+int bcss_abi_version(void) { return 100; }
+
+int64_t bcss_simplex_count(int64_t extent, int m) {
+  if (extent < 1 || m < 1) return -1;
+  try { return bcss::simplex_count(extent, m); } catch (...) { return -1; }
+}
+
+int bcss_hypertriangle_rank(const int64_t* idx, int m, int64_t extent, int64_t* out_rank) {
+  if (!idx || !out_rank || m < 1 || extent < 1) return fail(BCSS_ERR_PARAMETER, "bad arguments");
+  for (int t = 0; t < m; ++t) {
+    if (idx[t] < 0 || idx[t] >= extent)
+      return fail(BCSS_ERR_RANGE, "index %lld outside grid %lld", (long long)idx[t], (long long)extent);
+    if (t > 0 && idx[t] < idx[t - 1]) return fail(BCSS_ERR_SHAPE, "index is not nondecreasing");
+  }
+  try { *out_rank = bcss::hypertriangle_rank(idx, m, extent); } catch (const std::exception& e) {
+    return fail(BCSS_ERR_PARAMETER, "%s", e.what());
+  }
+  return BCSS_OK;
+}
+
+int bcss_hypertriangle_unrank(int64_t rank, int m, int64_t extent, int64_t* out_idx) {
+  if (!out_idx || m < 1 || extent < 1) return fail(BCSS_ERR_PARAMETER, "bad arguments");
+  try {
+    if (rank < 0 || rank >= bcss::simplex_count(extent, m)) return fail(BCSS_ERR_RANGE, "rank out of range");
+    bcss::hypertriangle_unrank(rank, m, extent, out_idx);
+  } catch (const std::exception& e) {
+    return fail(BCSS_ERR_PARAMETER, "%s", e.what());
+  }
+  return BCSS_OK;
+}
+
+int bcss_blocked_flops(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int reuse, uint64_t* out_flops) {
+  if (!out_flops) return fail(BCSS_ERR_PARAMETER, "null output");
+  if (m < 2) return fail(BCSS_ERR_PARAMETER, "cost model is defined for order >= 2");
+  if (n < 1 || p < 1 || b_a < 1 || b_c < 1) return fail(BCSS_ERR_PARAMETER, "dimensions must be positive");
+  if (n % b_a || p % b_c) return fail(BCSS_ERR_PARAMETER, "block dimensions must divide the dimensions");
+  try { *out_flops = bcss::blocked_flops(m, n, p, b_a, b_c, reuse != 0); } catch (const std::exception& e) {
+    return fail(BCSS_ERR_PARAMETER, "%s", e.what());
+  }
+  return BCSS_OK;
+}
+
+int bcss_plan_create(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int reuse, bcss_plan** out_plan) {
+  if (!out_plan) return fail(BCSS_ERR_PARAMETER, "null plan output");
+  *out_plan = nullptr;
+  int st = validate_problem(m, n, p, b_a, b_c);
+  if (st) return st;
+  bcss_plan* P = new (std::nothrow) bcss_plan();
+  if (!P) return fail(BCSS_ERR_NOMEM, "out of host memory");
+  P->m = m; P->n = n; P->p = p; P->bA = b_a; P->bC = b_c;
+  P->nbar = n / b_a; P->pbar = p / b_c; P->reuse = reuse != 0;
+  *out_plan = P;
+  return BCSS_OK;
+}
+
+int bcss_plan_destroy(bcss_plan* P) {
+  if (!P) return BCSS_OK;
+  if (P->d_tables) cudaFree(P->d_tables);
+  if (P->d_ws && P->own_ws) cudaFree(P->d_ws);
+  if (P->hA) cudaFree(P->hA);
+  if (P->hX) cudaFree(P->hX);
+  if (P->hC) cudaFree(P->hC);
+  if (P->host_stream) cudaStreamDestroy(P->host_stream);
+  delete P;
+  return BCSS_OK;
+}
+
+static void invalidate(bcss_plan* P) {
+  P->built = false;
+  if (P->d_tables) { cudaFree(P->d_tables); P->d_tables = nullptr; }
+}
+
+int bcss_plan_set_units(bcss_plan* P, const int32_t* units, int n_units) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (n_units < 0 || (n_units > 0 && !units)) return fail(BCSS_ERR_PARAMETER, "bad unit list");
+  for (int i = 0; i < n_units; ++i)
+    if (units[i] < 0 || units[i] >= P->pbar) return fail(BCSS_ERR_RANGE, "unit %d outside 0..%lld", units[i], (long long)P->pbar - 1);
+  P->units.assign(units, units + n_units);
+  P->units_set = true;
+  invalidate(P);
+  return BCSS_OK;
+}
+
+int bcss_plan_set_workspace_limit(bcss_plan* P, size_t bytes) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  P->ws_limit = bytes;
+  invalidate(P);
+  return BCSS_OK;
+}
+
+int bcss_plan_set_keep_temps(bcss_plan* P, int keep) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  P->keep_temps = keep != 0;
+  invalidate(P);
+  return BCSS_OK;
+}
+
+int bcss_plan_workspace_bytes(bcss_plan* P, size_t* out_bytes) {
+  if (!P || !out_bytes) return fail(BCSS_ERR_STATE, "null argument");
+  int st = build_plan(*P);
+  if (st) return st;
+  *out_bytes = P->ws_bytes;
+  return BCSS_OK;
+}
+
+int bcss_plan_set_workspace(bcss_plan* P, void* dev_ptr, size_t bytes) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (P->d_ws && P->own_ws) cudaFree(P->d_ws);
+  P->d_ws = dev_ptr;
+  P->ws_capacity = dev_ptr ? bytes : 0;
+  P->own_ws = false;
+  return BCSS_OK;
+}
+
+int bcss_plan_stats(bcss_plan* P, int64_t* waves, int64_t* launches, uint64_t* flops, int64_t* c_blocks) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  int st = build_plan(*P);
+  if (st) return st;
+  int64_t nl = 0;
+  for (auto& W : P->waves)
+    for (auto& L : W.levels) nl += L.item_off.back() > 0 ? 1 : 0;
+  if (waves) *waves = (int64_t)P->waves.size();
+  if (launches) *launches = nl;
+  if (flops) *flops = P->flops;
+  if (c_blocks) *c_blocks = P->c_blocks;
+  return BCSS_OK;
+}
+
+int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X, double* C, void* stream) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (!A || !X || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
+  int st = build_plan(*P);
+  if (st) return st;
+  if ((st = upload_tables(*P))) return st;
+  if ((st = ensure_workspace(*P))) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int dev, sms;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  char* tbl = static_cast<char*>(P->d_tables);
+  int64_t launches = 0;
+  for (auto& W : P->waves) {
+    for (auto& L : W.levels) {
+      const long long total = L.item_off.back();
+      if (total == 0) continue;
+      const KernelCfg& K = kCfgs[L.cfg];
+      bcss::LevelArgs a;
+      memset(&a, 0, sizeof(a));
+      a.X = X;
+      a.Tin = (L.k == P->m - 1) ? A : region_for(*P, L.k + 1);
+      a.Tout = (L.k == 0) ? C : region_for(*P, L.k);
+      a.parents = reinterpret_cast<const int4*>(tbl + L.off_parents);
+      a.item_off = reinterpret_cast<const long long*>(tbl + L.off_items);
+      a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
+      a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
+      a.total_items = total;
+      a.keys_in = L.keys_in; a.keys_out = L.keys_out;
+      a.blk_in = L.blk_in; a.blk_out = L.blk_out;
+      a.n_parents = (int)L.parents.size();
+      a.n = (int)P->n; a.ldx = (int)P->n; a.p_rows = (int)P->p;
+      a.nbar = (int)P->nbar; a.bA = (int)P->bA; a.bC = (int)P->bC;
+      a.lbA = is_pow2(P->bA) ? ilog2(P->bA) : -1;
+      a.k = L.k;
+      a.rest = (int)L.rest; a.bAk = (int)L.bAk;
+      a.n_tiles = L.n_tiles;
+      for (int i = 0; i < 10; ++i) a.pw[i] = (long long)std::min<double>(std::pow((double)P->bA, i), 9.0e18);
+      int occ = 1;
+      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
+      const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
+      K.fn<<<(unsigned)grid, K.NT, K.smem, s>>>(a);
+      CUDA_TRY(cudaGetLastError());
+      ++launches;
+    }
+  }
+  P->last_launches = launches;
+  return BCSS_OK;
+}
+
+int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* C) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (!A || !X || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
+  const size_t a_bytes = (size_t)bcss::simplex_count(P->nbar, P->m) * ipow(P->bA, P->m) * sizeof(double);
+  const size_t x_bytes = (size_t)(P->p * P->n) * sizeof(double);
+  const size_t c_bytes = (size_t)bcss::simplex_count(P->pbar, P->m) * ipow(P->bC, P->m) * sizeof(double);
+  auto grow = [&](double*& ptr, size_t& cap, size_t need) -> int {
+    if (cap >= need) return BCSS_OK;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr; cap = 0;
+    CUDA_TRY(cudaMalloc(&ptr, need));
+    cap = need;
+    return BCSS_OK;
+  };
+  int st;
+  if ((st = grow(P->hA, P->hA_bytes, a_bytes))) return st;
+  if ((st = grow(P->hX, P->hX_bytes, x_bytes))) return st;
+  if ((st = grow(P->hC, P->hC_bytes, c_bytes))) return st;
+  if (!P->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->host_stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaMemcpyAsync(P->hA, A, a_bytes, cudaMemcpyHostToDevice, P->host_stream));
+  CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->host_stream));
+  if (P->units_set) CUDA_TRY(cudaMemsetAsync(P->hC, 0, c_bytes, P->host_stream));
+  if ((st = bcss_sttsm_run(P, P->hA, P->hX, P->hC, P->host_stream))) return st;
+  CUDA_TRY(cudaMemcpyAsync(C, P->hC, c_bytes, cudaMemcpyDeviceToHost, P->host_stream));
+  CUDA_TRY(cudaStreamSynchronize(P->host_stream));
+  return BCSS_OK;
+}
+
+int bcss_plan_temp(bcss_plan* P, int k, const int32_t* suffix, const double** out_ptr, int64_t* out_elems) {
+  if (!P || !suffix || !out_ptr || !out_elems) return fail(BCSS_ERR_STATE, "null argument");
+  if (!P->keep_temps || !P->built || !P->d_ws) return fail(BCSS_ERR_STATE, "temporaries were not kept");
+  if (k < 1 || k >= P->m) return fail(BCSS_ERR_RANGE, "level %d outside 1..%d", k, P->m - 1);
+  const int sl = P->m - k;
+  int64_t base_calls = 0;
+  for (auto& W : P->waves) {
+    const LevelHost& L = W.levels[P->m - 1 - k];
+    for (int64_t c = 0; c < L.n_calls; ++c) {
+      if (std::equal(suffix, suffix + sl, &L.suffixes[(size_t)(c * sl)])) {
+        const int64_t elems = L.keys_out * L.blk_out;
+        *out_ptr = region_for(*P, k) + (base_calls + c) * elems;
+        *out_elems = elems;
+        if (P->waves.size() != 1) return fail(BCSS_ERR_STATE, "temporaries span several waves");
+        return BCSS_OK;
+      }
+    }
+  }
+  return fail(BCSS_ERR_RANGE, "no call with that suffix at level %d", k);
+}
+
+int bcss_plan_temp_copy(bcss_plan* P, int k, const int32_t* suffix, double* host_out, int64_t elems) {
+  if (!host_out) return fail(BCSS_ERR_PARAMETER, "null output");
+  const double* ptr = nullptr;
+  int64_t have = 0;
+  int st = bcss_plan_temp(P, k, suffix, &ptr, &have);
+  if (st) return st;
+  if (have != elems) return fail(BCSS_ERR_SHAPE, "temporary has %lld elements, buffer %lld", (long long)have, (long long)elems);
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(host_out, ptr, (size_t)elems * sizeof(double), cudaMemcpyDeviceToHost));
+  return BCSS_OK;
+}
+
+int bcss_plan_last_launches(bcss_plan* P, int64_t* out) {
+  if (!P || !out) return fail(BCSS_ERR_STATE, "null argument");
+  *out = P->last_launches;
+  return BCSS_OK;
+}
+
+}  // extern "C"

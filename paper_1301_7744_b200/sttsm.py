@@ -1,0 +1,272 @@
+"""Drop-in ``sttsm_bcss`` on the B200 FP64 tensor-core path.
+
+``sttsm_bcss(a, x, b_c, counter=None, reuse=True, temp_hook=None)`` has the
+reference's signature and behaviour (/root/reference/pkg/src/blocksym/
+change_of_basis.py:239-284): same argument checks and exceptions, same
+result object, flop count reported to ``counter``, ``temp_hook(k, temp)``
+called with every finished temporary in the reference's depth-first order.
+The computation runs in ``_bcss_sttsm.so`` (hand-written sm_100a CUDA); there
+is no CPU fallback.
+
+``SttsmPlan`` is the plan-level API over the C ABI (include/bcss_sttsm.h) for
+device-resident buffers (torch CUDA tensors or raw pointers), used by the
+benchmark, the multi-GPU layer and anyone who keeps A resident in HBM.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Callable
+
+import numpy as np
+
+from . import _native
+from .costs import bcss_flops, bcss_memops
+from .counters import OpCounter
+from .errors import BlockDivisibilityError, ParameterError, ShapeError
+from .indexing import simplex_count
+from .storage import BcssTensor, PartialSymTensor, packed_payload
+
+TempHook = Callable[[int, object], None]
+
+
+class SttsmPlan:
+    """A validated problem plus its level/work-list tables and workspace.
+
+    ``units`` restricts the run to the C blocks whose largest block index is
+    in ``units`` (top-level subtrees of the reference's ``descend``);
+    ``workspace_limit`` (bytes) splits the units into waves so temporaries
+    fit; ``keep_temps`` keeps every temporary resident for ``temp``.
+    """
+
+    def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, reuse: bool = True,
+                 units=None, workspace_limit: int = 0, keep_temps: bool = False):
+        lib = _native.lib()
+        self.m, self.n, self.p, self.b_a, self.b_c, self.reuse = m, n, p, b_a, b_c, bool(reuse)
+        h = ctypes.c_void_p()
+        _native.check(lib.bcss_plan_create(m, n, p, b_a, b_c, int(reuse), ctypes.byref(h)))
+        self._h = h
+        self._ws = None  # torch-owned workspace, when one was attached
+        if units is not None:
+            arr = (ctypes.c_int32 * len(units))(*[int(u) for u in units])
+            _native.check(lib.bcss_plan_set_units(h, arr, len(units)))
+        if workspace_limit:
+            _native.check(lib.bcss_plan_set_workspace_limit(h, int(workspace_limit)))
+        if keep_temps:
+            _native.check(lib.bcss_plan_set_keep_temps(h, 1))
+        self.units = None if units is None else sorted(set(int(u) for u in units))
+        self.a_elems = simplex_count(n // b_a, m) * b_a**m
+        self.c_elems = simplex_count(p // b_c, m) * b_c**m
+
+    # ---- lifecycle ------------------------------------------------------------
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            _native.lib().bcss_plan_destroy(self._h)
+            self._h = None
+        self._ws = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- introspection --------------------------------------------------------
+    @property
+    def workspace_bytes(self) -> int:
+        out = ctypes.c_size_t()
+        _native.check(_native.lib().bcss_plan_workspace_bytes(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    def stats(self) -> dict:
+        w, l, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        f = ctypes.c_uint64()
+        _native.check(_native.lib().bcss_plan_stats(self._h, ctypes.byref(w), ctypes.byref(l),
+                                                    ctypes.byref(f), ctypes.byref(c)))
+        return {"waves": w.value, "launches": l.value, "flops": int(f.value), "c_blocks": c.value}
+
+    @property
+    def last_launches(self) -> int:
+        out = ctypes.c_int64()
+        _native.check(_native.lib().bcss_plan_last_launches(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    # ---- execution ------------------------------------------------------------
+    def attach_torch_workspace(self, device=None) -> None:
+        """Allocate the workspace from torch's caching allocator (so torch and
+        the plan share one memory pool) and hand it to the plan."""
+        import torch
+
+        nbytes = self.workspace_bytes
+        if nbytes == 0:
+            return
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+        _native.check(_native.lib().bcss_plan_set_workspace(
+            self._h, ctypes.c_void_p(self._ws.data_ptr()), self._ws.numel()))
+
+    def run_ptr(self, a_ptr: int, x_ptr: int, c_ptr: int, stream: int = 0) -> None:
+        """Enqueue on raw device pointers (no synchronization)."""
+        _native.check(_native.lib().bcss_sttsm_run(
+            self._h, ctypes.c_void_p(a_ptr), ctypes.c_void_p(x_ptr), ctypes.c_void_p(c_ptr),
+            ctypes.c_void_p(stream)))
+
+    def run(self, a, x, c, stream=None) -> None:
+        """Enqueue on torch CUDA tensors (A packed, X p x n row-major, C packed)
+        on ``stream`` (default: torch's current stream).  Asynchronous."""
+        import torch
+
+        for name, t, numel in (("A", a, self.a_elems), ("X", x, self.p * self.n),
+                               ("C", c, self.c_elems)):
+            if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+                raise ShapeError(f"{name} must be a contiguous float64 CUDA tensor")
+            if t.numel() != numel:
+                raise ShapeError(f"{name} has {t.numel()} elements, expected {numel}")
+        if self._ws is None:
+            self.attach_torch_workspace(a.device)
+        s = stream if stream is not None else torch.cuda.current_stream(a.device)
+        self.run_ptr(a.data_ptr(), x.data_ptr(), c.data_ptr(), s.cuda_stream)
+
+    def run_host(self, a: np.ndarray, x: np.ndarray, c: np.ndarray) -> None:
+        """Host buffers in, host buffer out (copies + run + sync in the library)."""
+        for name, t, numel in (("A", a, self.a_elems), ("X", x, self.p * self.n),
+                               ("C", c, self.c_elems)):
+            if t.dtype != np.float64 or not t.flags.c_contiguous or t.size != numel:
+                raise ShapeError(f"{name} must be a contiguous float64 array of {numel} elements")
+        _native.check(_native.lib().bcss_sttsm_run_host(
+            self._h, ctypes.c_void_p(a.ctypes.data), ctypes.c_void_p(x.ctypes.data),
+            ctypes.c_void_p(c.ctypes.data)))
+
+    def temp(self, k: int, suffix) -> np.ndarray:
+        """Host copy of the kept temporary T(k) of call ``suffix`` (keep_temps)."""
+        nkeys = simplex_count(self.n // self.b_a, k) if self.reuse else (self.n // self.b_a) ** k
+        elems = nkeys * self.b_a**k * self.b_c ** (self.m - k)
+        out = np.empty(elems, dtype=np.float64)
+        arr = (ctypes.c_int32 * len(suffix))(*[int(s) for s in suffix])
+        _native.check(_native.lib().bcss_plan_temp_copy(
+            self._h, k, arr, ctypes.c_void_p(out.ctypes.data), elems))
+        return out
+
+
+class DenseBlockTable:
+    """Temporary with every block materialized (``reuse=False``); mirrors the
+    reference's ``_DenseBlockTable`` (change_of_basis.py:157-167)."""
+
+    def __init__(self, sym_modes: int, grid: int, blocks: dict):
+        self.sym_modes = sym_modes
+        self.grid = grid
+        self.blocks = blocks
+        self._identity = tuple(range(next(iter(blocks.values())).ndim))
+
+    def stored_and_transform(self, sym_idx):
+        return self.blocks[tuple(sym_idx)], self._identity
+
+    def to_dense(self) -> np.ndarray:
+        sample = next(iter(self.blocks.values()))
+        b = sample.shape[0]
+        tail = sample.shape[self.sym_modes:]
+        out = np.empty((self.grid * b,) * self.sym_modes + tail, order="F")
+        tail_sl = tuple(slice(None) for _ in tail)
+        for key, arr in self.blocks.items():
+            out[tuple(slice(i * b, (i + 1) * b) for i in key) + tail_sl] = arr
+        return out
+
+
+def temp_to_dense(temp) -> np.ndarray:
+    """Dense array of a temporary handed to ``temp_hook`` (either flavour);
+    counterpart of the reference's ``temp_to_dense`` (change_of_basis.py:170-182)."""
+    return temp.to_dense()
+
+
+def _check_args(a, x) -> tuple[int, int, int]:
+    """Reference argument checks (change_of_basis.py:54-63, 259-262)."""
+    is_bcss = isinstance(a, BcssTensor) or (
+        hasattr(a, "blocks") and hasattr(a, "b") and hasattr(a, "n")
+        and getattr(a, "tail_dims", ()) == () and not isinstance(a, PartialSymTensor))
+    if not is_bcss:
+        raise ShapeError("sttsm_bcss needs blocked compact symmetric input")
+    m = a.order
+    if m < 2:
+        raise ParameterError("change of basis is defined for order >= 2")
+    n = a.n
+    if x.ndim != 2 or x.shape[1] != n:
+        raise ShapeError(f"matrix shape {x.shape} does not contract dimension {n}")
+    return m, n, x.shape[0]
+
+
+def sttsm_bcss(a, x, b_c: int, counter: OpCounter | None = None, reuse: bool = True,
+               temp_hook: TempHook | None = None) -> BcssTensor:
+    """Blocked change of basis over compact symmetric storage, on the GPU.
+
+    Same contract as the reference ``sttsm_bcss``: returns a fresh
+    ``BcssTensor`` of order m, dimension p, block dimension ``b_c``; inputs
+    are not modified.
+    """
+    x = np.asarray(x, dtype=np.float64)
+    m, n, p = _check_args(a, x)
+    b_a = a.b
+    if b_c < 1 or p % b_c != 0:
+        raise BlockDivisibilityError(f"output block dimension {b_c} does not divide {p}")
+    a_payload = np.ascontiguousarray(packed_payload(a), dtype=np.float64)
+    xc = np.ascontiguousarray(x)
+    c_payload = np.empty(simplex_count(p // b_c, m) * b_c**m, dtype=np.float64)
+    plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, keep_temps=temp_hook is not None)
+    try:
+        plan.run_host(a_payload, xc, c_payload)
+        if temp_hook is not None:
+            _replay_temps(plan, temp_hook)
+    finally:
+        plan.close()
+    if counter is not None:
+        counter.count_flops(bcss_flops(m, n, p, b_a, b_c, reuse))
+        counter.count_memops(bcss_memops(m, n, p, b_a, b_c, reuse))
+    return BcssTensor(m, p, b_c, payload=c_payload)
+
+
+def _replay_temps(plan: SttsmPlan, hook: TempHook) -> None:
+    """Call ``hook(k, temp)`` for every temporary in the reference's order:
+    pre-order over ``descend`` (change_of_basis.py:269-281)."""
+    m, n, b_a, b_c = plan.m, plan.n, plan.b_a, plan.b_c
+    nbar, pbar = n // b_a, plan.p // b_c
+    tail = (b_c,) * (m - 1)
+
+    def make(k: int, suffix: tuple) -> object:
+        flat = plan.temp(k, suffix)
+        tail_k = tail[: m - k]
+        if plan.reuse:
+            return PartialSymTensor(k, n, b_a, tail_k, payload=flat)
+        import itertools
+        shape = (b_a,) * k + tail_k
+        size = int(np.prod(shape))
+        blocks = {key: flat[r * size:(r + 1) * size].reshape(shape, order="F")
+                  for r, key in enumerate(itertools.product(range(nbar), repeat=k))}
+        return DenseBlockTable(k, nbar, blocks)
+
+    def walk(k: int, j_hi: int, suffix: tuple) -> None:
+        if k == 0:
+            return
+        for jb in range(j_hi + 1):
+            s = (jb,) + suffix
+            hook(k, make(k, s))
+            walk(k - 1, jb, s)
+
+    walk(m - 1, pbar - 1, ())
+
+
+def sttsm_bcss_device(a_packed, x, m: int, b_a: int, b_c: int, out=None, reuse: bool = True,
+                      plan: SttsmPlan | None = None, stream=None):
+    """Device-resident entry point on torch CUDA tensors.
+
+    ``a_packed``: packed BCSS payload of A (float64, CUDA); ``x``: p x n
+    float64 CUDA tensor; returns (or fills ``out``) the packed C payload.
+    Asynchronous on ``stream`` (default: current stream).
+    """
+    import torch
+
+    p, n = x.shape
+    if plan is None:
+        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse)
+    if out is None:
+        out = torch.empty(plan.c_elems, dtype=torch.float64, device=x.device)
+    plan.run(a_packed, x, out, stream=stream)
+    return out

@@ -1,0 +1,50 @@
+"""GPU parity against the reference's own outputs (tests/golden, made by
+oracle/gen_golden.py from blocksym.sttsm_bcss): every case runs through the
+drop-in ``sttsm_bcss`` (C ABI -> sm_100a DMMA kernels) and must match the
+reference within relative Frobenius 1e-12 (BASELINE north star) and the
+reference tests' max-rel bar 1e-10 (test_change_of_basis.py:126-136)."""
+
+import glob
+
+import numpy as np
+import pytest
+
+import paper_1301_7744_b200 as bs
+from oracle import bcss_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+CASES = sorted(glob.glob(str(__import__("conftest").GOLDEN / "sttsm_*.npz")))
+
+
+def _load(path):
+    d = np.load(path)
+    m, n, p, b_a, b_c = (int(v) for v in d["dims"])
+    return d, m, n, p, b_a, b_c
+
+
+@pytest.mark.parametrize("path", CASES, ids=lambda s: s.split("/")[-1][6:-4])
+@pytest.mark.parametrize("reuse", [True, False])
+def test_drop_in_matches_reference(path, reuse):
+    d, m, n, p, b_a, b_c = _load(path)
+    a = bs.BcssTensor(m, n, b_a, payload=d["A"])
+    ctr = bs.OpCounter()
+    out = bs.sttsm_bcss(a, d["X"], b_c, ctr, reuse=reuse)
+    want = d["C"] if reuse else d["C_noreuse"]
+    assert out.dims == (p,) * m and out.b == b_c
+    assert orc.rel_frobenius(out.payload, want) <= 1e-12
+    assert orc.max_rel(out.payload, want) <= 1e-10
+    if "C_naive" in d:
+        assert orc.rel_frobenius(out.payload, d["C_naive"]) <= 1e-12
+    assert ctr.flops == int(d["flops"][0 if reuse else 1])
+
+
+def test_temp_hook_replays_reference_temporaries(golden_dir):
+    d = np.load(golden_dir / "temps_m4_n4_b2.npz")
+    a = bs.BcssTensor(4, 4, 2, payload=d["A"])
+    seen = []
+    bs.sttsm_bcss(a, d["X"], 2, temp_hook=lambda k, t: seen.append((k, t)))
+    assert [k for k, _ in seen] == list(d["levels"])
+    for i, (k, t) in enumerate(seen):
+        assert orc.rel_frobenius(t.payload, d[f"T{i}"]) <= 1e-12
+        assert t.dims == (4,) * k + (2,) * (4 - k)
