@@ -138,6 +138,24 @@ int bcss_plan_temp_copy(bcss_plan* plan, int k, const int32_t* suffix, double* h
 /* Number of user kernels the last run launched. */
 int bcss_plan_last_launches(bcss_plan* plan, int64_t* out_launches);
 
+/* Packed-payload ranks of the C blocks this plan writes (its units), in the
+ * order they are produced; n_max bounds the output array.  Used to gather a
+ * sharded C. */
+int bcss_plan_c_block_ranks(bcss_plan* plan, int64_t* out_ranks, int64_t n_max, int64_t* out_n);
+
+/* Per-launch timing: with timing on, every launch of the next runs is
+ * bracketed by CUDA events on the run's stream; bcss_plan_launch_times
+ * returns, for the last run, each launch's level k, exact flops and
+ * device milliseconds (synchronizes the stream). */
+int bcss_plan_set_timing(bcss_plan* plan, int on);
+int bcss_plan_launch_times(bcss_plan* plan, int32_t* out_level, uint64_t* out_flops,
+                           float* out_ms, int64_t n_max, int64_t* out_n);
+
+/* Diagnostic: FP64 tensor-core (DMMA) peak of the current device, measured
+ * with a register-resident mma.sync m8n8k4 f64 loop over all SMs (TFLOP/s).
+ * Used as the roofline denominator; no reference counterpart. */
+int bcss_probe_fp64_peak(double* out_tflops);
+
 #ifdef __cplusplus
 }
 #endif

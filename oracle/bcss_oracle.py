@@ -174,7 +174,7 @@ def sttsm_naive_dense(a: np.ndarray, x: np.ndarray) -> np.ndarray:
 
 
 def sttsm_bcss_packed(a_packed: np.ndarray, x: np.ndarray, m: int, n: int, b_a: int,
-                      b_c: int, keep_temps: bool = False):
+                      b_c: int, keep_temps: bool = False, units=None):
     """Blocked change of basis over packed BCSS storage.
 
     Restates ``sttsm_bcss`` / ``_level_product`` (change_of_basis.py:185-284):
@@ -184,7 +184,9 @@ def sttsm_bcss_packed(a_packed: np.ndarray, x: np.ndarray, m: int, n: int, b_a: 
     contracted.  Temporaries keep the reference block layout
     ``(b_a,)*k + (b_c,)*(m-k)`` (F-order).  Returns the packed C payload
     (blocks in hypertriangle order) and, with ``keep_temps``, a dict
-    ``{(k, suffix): {key: block}}`` of every temporary.
+    ``{(k, suffix): {key: block}}`` of every temporary.  ``units`` restricts
+    the outermost loop to those jb_{m-1} values (a top-level subtree sample);
+    C blocks outside them are left zero.
     """
     x = np.asarray(x, dtype=np.float64)
     p = x.shape[0]
@@ -194,7 +196,7 @@ def sttsm_bcss_packed(a_packed: np.ndarray, x: np.ndarray, m: int, n: int, b_a: 
     top = {key: a_blocks[r].reshape((b_a,) * m, order="F")
            for r, key in enumerate(hypertriangle(nbar, m))}
     c_keys = hypertriangle(pbar, m)
-    c_out = np.empty((len(c_keys), b_c**m))
+    c_out = np.zeros((len(c_keys), b_c**m))
     temps = {}
 
     def level(t_in: dict, k: int, jb: int) -> dict:
@@ -218,6 +220,8 @@ def sttsm_bcss_packed(a_packed: np.ndarray, x: np.ndarray, m: int, n: int, b_a: 
 
     def descend(k: int, t_in: dict, j_hi: int, suffix: tuple) -> None:
         for jb in range(j_hi + 1):
+            if k == m - 1 and units is not None and jb not in units:
+                continue
             produced = level(t_in, k, jb)
             if k == 0:
                 c_out[hypertriangle_rank((jb,) + suffix, pbar)] = \

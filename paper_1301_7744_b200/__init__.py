@@ -21,6 +21,13 @@ from .errors import (
 )
 from .indexing import canonicalize, hypertriangle_iter, hypertriangle_rank, hypertriangle_unrank, simplex_count
 from .storage import BcssTensor, PartialSymTensor, packed_payload
-from .sttsm import DenseBlockTable, SttsmPlan, sttsm_bcss, sttsm_bcss_device, temp_to_dense
+from .sttsm import (
+    DenseBlockTable,
+    SttsmPlan,
+    probe_fp64_peak,
+    sttsm_bcss,
+    sttsm_bcss_device,
+    temp_to_dense,
+)
 
 __version__ = "0.1.0"

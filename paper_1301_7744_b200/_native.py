@@ -55,6 +55,10 @@ SIGNATURES = {
     "bcss_plan_temp": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _P(_vp), _P(_i64)]),
     "bcss_plan_temp_copy": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _vp, _i64]),
     "bcss_plan_last_launches": (_c_int, [_vp, _P(_i64)]),
+    "bcss_plan_c_block_ranks": (_c_int, [_vp, _P(_i64), _i64, _P(_i64)]),
+    "bcss_plan_set_timing": (_c_int, [_vp, _c_int]),
+    "bcss_plan_launch_times": (_c_int, [_vp, _P(ctypes.c_int32), _P(_u64), _P(ctypes.c_float), _i64, _P(_i64)]),
+    "bcss_probe_fp64_peak": (_c_int, [_P(ctypes.c_double)]),
 }
 
 _lib = None

@@ -65,6 +65,22 @@ const KernelCfg kCfgs[] = {
 };
 enum { CFG_FAST = 0, CFG_GENERIC = 1 };
 
+// Register-resident DMMA loop: 16 independent m8n8k4 accumulators per warp.
+__global__ void dmma_peak_kernel(double* sink, int iters) {
+  const double a = 1.0 + threadIdx.x * 1e-9, b = 1.0 - threadIdx.x * 1e-9;
+  double c[16][2];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) bcss::dmma(c[i][0], c[i][1], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += c[i][0] + c[i][1];
+  if (s == 12345.0) sink[threadIdx.x] = s;
+}
+
 }  // namespace
 
 // ---- plan ----------------------------------------------------------------------
@@ -73,6 +89,7 @@ struct LevelHost {
   int64_t keys_out = 0, keys_in = 0, blk_out = 0, blk_in = 0, rest = 0, bAk = 0;
   int n_tiles = 0;
   int64_t n_calls = 0;
+  uint64_t flops = 0;
   std::vector<int4> parents;
   std::vector<long long> item_off;
   std::vector<int> child_call;
@@ -83,6 +100,7 @@ struct LevelHost {
 struct WaveHost {
   std::vector<int> units;
   std::vector<LevelHost> levels;  // levels[i] has k = m-1-i
+  std::vector<size_t> level_off;  // byte offset of T(k)'s region in the workspace
 };
 
 struct bcss_plan {
@@ -98,7 +116,6 @@ struct bcss_plan {
   std::vector<WaveHost> waves;
   std::vector<std::vector<int2>> nbr;  // per k
   std::vector<size_t> nbr_off;         // per k, into the table buffer
-  std::vector<size_t> region_bytes;    // ping-pong (2) or per level (m) when keep_temps
   size_t ws_bytes = 0;
   uint64_t flops = 0;
   int64_t c_blocks = 0;
@@ -113,6 +130,11 @@ struct bcss_plan {
   size_t hA_bytes = 0, hX_bytes = 0, hC_bytes = 0;
   cudaStream_t host_stream = nullptr;
   int64_t last_launches = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> events;  // 2 per launch
+  std::vector<int> launch_level;
+  std::vector<uint64_t> launch_flops;
+  cudaStream_t timed_stream = nullptr;
 };
 
 namespace {
@@ -272,38 +294,38 @@ int build_plan(bcss_plan& P) {
       std::vector<int> trial = cur;
       trial.push_back(u);
       if (!cur.empty() && !P.keep_temps && P.ws_limit > 0 && peak_for(P, trial) > P.ws_limit) {
-        P.waves.push_back(WaveHost{cur, {}});
+        P.waves.push_back(WaveHost{cur, {}, {}});
         cur = {u};
       } else {
         cur = trial;
       }
     }
-    if (!cur.empty()) P.waves.push_back(WaveHost{cur, {}});
+    if (!cur.empty()) P.waves.push_back(WaveHost{cur, {}, {}});
     if (!P.keep_temps && P.ws_limit > 0) {
       for (auto& W : P.waves)
         if (peak_for(P, W.units) > P.ws_limit)
           return fail(BCSS_ERR_NOMEM, "one top-level unit needs %zu workspace bytes > limit %zu",
                       peak_for(P, W.units), P.ws_limit);
     }
-    // region sizes
-    if (P.keep_temps) {
-      P.region_bytes.assign(P.m, 0);
-      for (auto& W : P.waves) {
-        auto b = level_bytes(P, W.units);
-        for (int k = 1; k < P.m; ++k) P.region_bytes[k] = std::max(P.region_bytes[k], b[k]);
-      }
-    } else {
-      P.region_bytes.assign(2, 0);
-      for (auto& W : P.waves) {
-        auto b = level_bytes(P, W.units);
-        for (int k = 1; k < P.m; ++k) {
-          size_t& r = P.region_bytes[(P.m - 1 - k) % 2];
-          r = std::max(r, b[k]);
-        }
-      }
-    }
+    // Workspace layout per wave: keep_temps gives every level its own region;
+    // otherwise levels alternate between two regions (T(k+1) is read while
+    // T(k) is written).  The workspace is the largest wave's footprint.
     P.ws_bytes = 0;
-    for (auto& r : P.region_bytes) { r = (r + 255) / 256 * 256; P.ws_bytes += r; }
+    auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+    for (auto& W : P.waves) {
+      auto b = level_bytes(P, W.units);
+      W.level_off.assign(P.m + 1, 0);
+      size_t end = 0;
+      if (P.keep_temps) {
+        for (int k = 1; k < P.m; ++k) { W.level_off[k] = end; end += al(b[k]); }
+      } else {
+        size_t r[2] = {0, 0};
+        for (int k = 1; k < P.m; ++k) r[(P.m - 1 - k) % 2] = std::max(r[(P.m - 1 - k) % 2], al(b[k]));
+        for (int k = 1; k < P.m; ++k) W.level_off[k] = (P.m - 1 - k) % 2 == 0 ? 0 : r[0];
+        end = r[0] + r[1];
+      }
+      P.ws_bytes = std::max(P.ws_bytes, end);
+    }
     // tables
     P.nbr.assign(P.m, {});
     P.nbr_off.assign(P.m, 0);
@@ -321,7 +343,8 @@ int build_plan(bcss_plan& P) {
         L.off_parents = take(L.parents.size() * sizeof(int4));
         L.off_items = take(L.item_off.size() * sizeof(long long));
         L.off_child = take(L.child_call.size() * sizeof(int));
-        P.flops += (uint64_t)2 * L.n_calls * P.bC * P.n * L.keys_out * L.rest;
+        L.flops = (uint64_t)2 * L.n_calls * P.bC * P.n * L.keys_out * L.rest;
+        P.flops += L.flops;
         if (L.k == 0) P.c_blocks += L.n_calls;
       }
     }
@@ -376,14 +399,8 @@ int ensure_workspace(bcss_plan& P) {
   return BCSS_OK;
 }
 
-double* region_for(bcss_plan& P, int k) {
-  char* base = static_cast<char*>(P.d_ws);
-  if (P.keep_temps) {
-    size_t off = 0;
-    for (int q = 0; q < k; ++q) off += P.region_bytes[q];
-    return reinterpret_cast<double*>(base + off);
-  }
-  return reinterpret_cast<double*>(base + ((P.m - 1 - k) % 2 == 0 ? 0 : P.region_bytes[0]));
+double* region_for(bcss_plan& P, const WaveHost& W, int k) {
+  return reinterpret_cast<double*>(static_cast<char*>(P.d_ws) + W.level_off[k]);
 }
 
 int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c) {
@@ -469,6 +486,7 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->hX) cudaFree(P->hX);
   if (P->hC) cudaFree(P->hC);
   if (P->host_stream) cudaStreamDestroy(P->host_stream);
+  for (auto ev : P->events) cudaEventDestroy(ev);
   delete P;
   return BCSS_OK;
 }
@@ -547,6 +565,11 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X, double* C, vo
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   char* tbl = static_cast<char*>(P->d_tables);
   int64_t launches = 0;
+  if (P->timing) {
+    P->launch_level.clear();
+    P->launch_flops.clear();
+    P->timed_stream = s;
+  }
   for (auto& W : P->waves) {
     for (auto& L : W.levels) {
       const long long total = L.item_off.back();
@@ -555,8 +578,8 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X, double* C, vo
       bcss::LevelArgs a;
       memset(&a, 0, sizeof(a));
       a.X = X;
-      a.Tin = (L.k == P->m - 1) ? A : region_for(*P, L.k + 1);
-      a.Tout = (L.k == 0) ? C : region_for(*P, L.k);
+      a.Tin = (L.k == P->m - 1) ? A : region_for(*P, W, L.k + 1);
+      a.Tout = (L.k == 0) ? C : region_for(*P, W, L.k);
       a.parents = reinterpret_cast<const int4*>(tbl + L.off_parents);
       a.item_off = reinterpret_cast<const long long*>(tbl + L.off_items);
       a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
@@ -575,8 +598,21 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X, double* C, vo
       int occ = 1;
       CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
       const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
+      if (P->timing) {
+        while (P->events.size() < (size_t)(2 * (launches + 1))) {
+          cudaEvent_t ev;
+          CUDA_TRY(cudaEventCreate(&ev));
+          P->events.push_back(ev);
+        }
+        CUDA_TRY(cudaEventRecord(P->events[2 * launches], s));
+      }
       K.fn<<<(unsigned)grid, K.NT, K.smem, s>>>(a);
       CUDA_TRY(cudaGetLastError());
+      if (P->timing) {
+        CUDA_TRY(cudaEventRecord(P->events[2 * launches + 1], s));
+        P->launch_level.push_back(L.k);
+        P->launch_flops.push_back(L.flops);
+      }
       ++launches;
     }
   }
@@ -623,7 +659,7 @@ int bcss_plan_temp(bcss_plan* P, int k, const int32_t* suffix, const double** ou
     for (int64_t c = 0; c < L.n_calls; ++c) {
       if (std::equal(suffix, suffix + sl, &L.suffixes[(size_t)(c * sl)])) {
         const int64_t elems = L.keys_out * L.blk_out;
-        *out_ptr = region_for(*P, k) + (base_calls + c) * elems;
+        *out_ptr = region_for(*P, W, k) + (base_calls + c) * elems;
         *out_elems = elems;
         if (P->waves.size() != 1) return fail(BCSS_ERR_STATE, "temporaries span several waves");
         return BCSS_OK;
@@ -648,6 +684,79 @@ int bcss_plan_temp_copy(bcss_plan* P, int k, const int32_t* suffix, double* host
 int bcss_plan_last_launches(bcss_plan* P, int64_t* out) {
   if (!P || !out) return fail(BCSS_ERR_STATE, "null argument");
   *out = P->last_launches;
+  return BCSS_OK;
+}
+
+int bcss_plan_c_block_ranks(bcss_plan* P, int64_t* out_ranks, int64_t n_max, int64_t* out_n) {
+  if (!P || !out_n) return fail(BCSS_ERR_STATE, "null argument");
+  int st = build_plan(*P);
+  if (st) return st;
+  int64_t cnt = 0;
+  for (auto& W : P->waves)
+    for (auto& L : W.levels)
+      if (L.k == 0)
+        for (int r : L.child_call) {
+          if (out_ranks && cnt < n_max) out_ranks[cnt] = r;
+          ++cnt;
+        }
+  *out_n = cnt;
+  if (out_ranks && cnt > n_max) return fail(BCSS_ERR_RANGE, "output array too small (%lld > %lld)", (long long)cnt, (long long)n_max);
+  return BCSS_OK;
+}
+
+int bcss_plan_set_timing(bcss_plan* P, int on) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  P->timing = on != 0;
+  return BCSS_OK;
+}
+
+int bcss_plan_launch_times(bcss_plan* P, int32_t* out_level, uint64_t* out_flops, float* out_ms, int64_t n_max,
+                           int64_t* out_n) {
+  if (!P || !out_n) return fail(BCSS_ERR_STATE, "null argument");
+  if (!P->timing) return fail(BCSS_ERR_STATE, "timing is off");
+  const int64_t n = (int64_t)P->launch_level.size();
+  *out_n = n;
+  if (n > n_max) return fail(BCSS_ERR_RANGE, "output arrays too small");
+  CUDA_TRY(cudaStreamSynchronize(P->timed_stream));
+  for (int64_t i = 0; i < n; ++i) {
+    float ms = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&ms, P->events[2 * i], P->events[2 * i + 1]));
+    if (out_level) out_level[i] = P->launch_level[i];
+    if (out_flops) out_flops[i] = P->launch_flops[i];
+    if (out_ms) out_ms[i] = ms;
+  }
+  return BCSS_OK;
+}
+
+int bcss_probe_fp64_peak(double* out_tflops) {
+  if (!out_tflops) return fail(BCSS_ERR_PARAMETER, "null output");
+  int dev, sms;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* sink;
+  CUDA_TRY(cudaMalloc(&sink, 1024 * sizeof(double)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int iters = 4000, threads = 256, grid = 2 * sms;
+  dmma_peak_kernel<<<grid, threads>>>(sink, 16);
+  float best = 1e30f;
+  for (int r = 0; r < 3; ++r) {
+    cudaEventRecord(e0);
+    dmma_peak_kernel<<<grid, threads>>>(sink, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    best = std::min(best, ms);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (e != cudaSuccess) return fail(BCSS_ERR_CUDA, "peak probe failed: %s", cudaGetErrorString(e));
+  const double flops = 2.0 * 256.0 * 16.0 * iters * (threads / 32) * (double)grid;
+  *out_tflops = flops / (best * 1e-3) / 1e12;
   return BCSS_OK;
 }
 

