@@ -48,8 +48,9 @@ int ilog2(int64_t v) { int r = 0; while ((int64_t(1) << r) < v) ++r; return r; }
 int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; return r; }
 
 // ---- kernel configurations ----------------------------------------------------
-using FastK = bcss::LevelKernel<128, 128, 32, 2, 4, 3, true>;
-using GenK = bcss::LevelKernel<32, 64, 16, 2, 2, 2, false>;
+using GenK = bcss::GenericLevelKernel<32, 64, 16, 2, 2, 2>;
+template <int BA>
+using Fast128 = bcss::FastLevelKernel<128, 128, 2, 4, 3, BA>;
 
 template <class K>
 __global__ void __launch_bounds__(K::NT, 1) level_kernel(const bcss::LevelArgs a) { K::run(a); }
@@ -60,10 +61,23 @@ struct KernelCfg {
   void (*fn)(bcss::LevelArgs);
 };
 const KernelCfg kCfgs[] = {
-    {128, 128, FastK::NT, FastK::SMEM_BYTES, level_kernel<FastK>},
     {32, 64, GenK::NT, GenK::SMEM_BYTES, level_kernel<GenK>},
+    {128, 128, Fast128<4>::NT, Fast128<4>::SMEM_BYTES, level_kernel<Fast128<4>>},
+    {128, 128, Fast128<8>::NT, Fast128<8>::SMEM_BYTES, level_kernel<Fast128<8>>},
+    {128, 128, Fast128<16>::NT, Fast128<16>::SMEM_BYTES, level_kernel<Fast128<16>>},
+    {128, 128, Fast128<32>::NT, Fast128<32>::SMEM_BYTES, level_kernel<Fast128<32>>},
 };
-enum { CFG_FAST = 0, CFG_GENERIC = 1 };
+enum { CFG_GENERIC = 0 };
+// fast configuration for power-of-two b_a in {4, 8, 16, 32}, else -1
+int fast_cfg(int64_t bA) {
+  switch (bA) {
+    case 4: return 1;
+    case 8: return 2;
+    case 16: return 3;
+    case 32: return 4;
+    default: return -1;
+  }
+}
 
 // Register-resident DMMA loop: 16 independent m8n8k4 accumulators per warp.
 __global__ void dmma_peak_kernel(double* sink, int iters) {
@@ -214,14 +228,14 @@ size_t peak_for(const bcss_plan& P, const std::vector<int>& units) {
 }
 
 void build_wave_levels(bcss_plan& P, WaveHost& W) {
-  const bool fast = P.reuse && is_pow2(P.bA) && P.bA >= 2 && is_pow2(P.bC);
+  const int fcfg = (P.reuse && is_pow2(P.bC)) ? fast_cfg(P.bA) : -1;
   W.levels.clear();
   std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls
   int64_t prev_calls = 0;
   for (int k = P.m - 1; k >= 0; --k) {
     LevelHost L;
     L.k = k;
-    L.cfg = fast ? CFG_FAST : CFG_GENERIC;
+    L.cfg = fcfg >= 0 ? fcfg : CFG_GENERIC;
     L.keys_out = keys_at(P, k);
     L.keys_in = keys_at(P, k + 1);
     L.blk_out = blk_at(P, k);

@@ -97,103 +97,63 @@ __device__ __forceinline__ TileInfo decode_item(const LevelArgs& a, long long it
   return t;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, bool FAST>
-struct LevelKernel {
+// ---------------------------------------------------------------------------
+// Generic kernel: any block sizes (including odd b_a / b_c, b = 1), either
+// reuse mode, any redirection permutation.  Per-element addressing with
+// div/mod and zero-filled bounds; correctness path for small/odd problems.
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+struct GenericLevelKernel {
   static constexpr int NT = WM * WN * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
-  static constexpr int LDA = BK + 4;   // 8 mod 32 banks per row: conflict-free A fragments
-  static constexpr int LDB = BN + 4;   // same for B fragments
+  static constexpr int LDA = BK + 4;
+  static constexpr int LDB = BN + 4;
   static constexpr int A_STAGE = BM * LDA, B_STAGE = BK * LDB;
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
   static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "tile shape");
   static_assert((BM * BK) % NT == 0 && (BK * BN) % NT == 0, "loader balance");
 
-  // ---- operand staging --------------------------------------------------------
   static __device__ __forceinline__ void load_stage(const LevelArgs& a, const TileInfo& t, int kstep,
                                                     double* As, double* Bs) {
     const int tid = threadIdx.x;
     const int k0 = kstep * BK;
-    // A = X[row0 + mt*BM + r, k0 + c]: rows beyond the parent's range are zero.
     const int rbase = t.mt * BM;
-    if (FAST) {
 #pragma unroll
-      for (int it = 0; it < (BM * BK / 2) / NT; ++it) {
-        const int idx = tid + it * NT;
-        const int r = idx / (BK / 2), c = (idx % (BK / 2)) * 2;
-        const bool ok = (rbase + r < t.rows) && (k0 + c < a.n);
-        const double* src = ok ? a.X + (long long)(t.row0 + rbase + r) * a.ldx + k0 + c : a.X;
-        cp_async16(As + r * LDA + c, src, ok);
-      }
-    } else {
-#pragma unroll
-      for (int it = 0; it < (BM * BK) / NT; ++it) {
-        const int idx = tid + it * NT;
-        const int r = idx / BK, c = idx % BK;
-        const bool ok = (rbase + r < t.rows) && (k0 + c < a.n);
-        const double* src = ok ? a.X + (long long)(t.row0 + rbase + r) * a.ldx + k0 + c : a.X;
-        cp_async8(As + r * LDA + c, src, ok);
-      }
+    for (int it = 0; it < (BM * BK) / NT; ++it) {
+      const int idx = tid + it * NT;
+      const int r = idx / BK, c = idx % BK;
+      const bool ok = (rbase + r < t.rows) && (k0 + c < a.n);
+      const double* src = ok ? a.X + (long long)(t.row0 + rbase + r) * a.ldx + k0 + c : a.X;
+      cp_async8(As + r * LDA + c, src, ok);
     }
-    // B = logical T(k+1) block (K, ib) rows e, columns [n0, n0+BN).
     const int n0 = t.nt * BN;
     const int2* nrow = a.nbr + (long long)t.key * a.nbar;
     const double* tin_call = a.Tin + (long long)t.in_call * a.keys_in * a.blk_in;
-    if (FAST) {
-      // Row groups share one ib (one stored block, one contracted position).
-      const int RG = a.bA < BK ? a.bA : BK;
-      const int lgRG = a.bA < BK ? a.lbA : __ffs(BK) - 1;
-      const int kl = a.k * a.lbA;
-#pragma unroll 4
-      for (int it = 0; it < (BK * BN) / NT; ++it) {
-        const int idx = tid + it * NT;
-        const int g = idx >> (lgRG + __ffs(BN) - 1);        // / (RG*BN)
-        const int j = idx & ((RG * BN) - 1);
-        const int i = k0 + (g << lgRG);                     // first reduction row of the group
-        const int ib = i >> a.lbA;
-        const int e0 = i & (a.bA - 1);
-        const int2 nb = __ldg(nrow + (ib < a.nbar ? ib : 0));
-        const int pos = code_p(nb.y);
-        int e, col;
-        if (pos == 0) { e = j & (RG - 1); col = j >> lgRG; }   // stored block is e-contiguous
-        else { col = j & (BN - 1); e = j >> (__ffs(BN) - 1); }  // lo-contiguous
-        const int cg = n0 + col;
-        const bool ok = (i + e < a.n) && (cg < a.rest);
-        const int af = cg & (a.bAk - 1);
-        const int tt = cg >> kl;
-        const int sh = pos * a.lbA;
-        const long long off = (long long)(af & ((1 << sh) - 1)) + ((long long)(e0 + e) << sh) +
-                              ((long long)(af >> sh) << (sh + a.lbA)) + ((long long)tt << (kl + a.lbA));
-        const double* src = ok ? tin_call + (long long)nb.x * a.blk_in + off : a.X;
-        cp_async8(Bs + ((g << lgRG) + e) * LDB + col, src, ok);
-      }
-    } else {
 #pragma unroll 1
-      for (int it = 0; it < (BK * BN) / NT; ++it) {
-        const int idx = tid + it * NT;
-        const int r = idx / BN, col = idx % BN;
-        const int i = k0 + r, cg = n0 + col;
-        const bool ok = (i < a.n) && (cg < a.rest);
-        const double* src = a.X;
-        if (ok) {
-          const int ib = i / a.bA, e = i - ib * a.bA;
-          const int2 nb = __ldg(nrow + ib);
-          int af = cg % a.bAk;
-          const int tt = cg / a.bAk;
-          long long off = (long long)tt * a.pw[a.k + 1] + (long long)e * a.pw[code_map(nb.y, a.k)];
-          for (int d = 0; d < a.k; ++d) {
-            const int dig = af % a.bA;
-            af /= a.bA;
-            off += (long long)dig * a.pw[code_map(nb.y, d)];
-          }
-          src = tin_call + (long long)nb.x * a.blk_in + off;
+    for (int it = 0; it < (BK * BN) / NT; ++it) {
+      const int idx = tid + it * NT;
+      const int r = idx / BN, col = idx % BN;
+      const int i = k0 + r, cg = n0 + col;
+      const bool ok = (i < a.n) && (cg < a.rest);
+      const double* src = a.X;
+      if (ok) {
+        const int ib = i / a.bA, e = i - ib * a.bA;
+        const int2 nb = __ldg(nrow + ib);
+        int af = cg % a.bAk;
+        const int tt = cg / a.bAk;
+        long long off = (long long)tt * a.pw[a.k + 1] + (long long)e * a.pw[code_map(nb.y, a.k)];
+        for (int d = 0; d < a.k; ++d) {
+          const int dig = af % a.bA;
+          af /= a.bA;
+          off += (long long)dig * a.pw[code_map(nb.y, d)];
         }
-        cp_async8(Bs + r * LDB + col, src, ok);
+        src = tin_call + (long long)nb.x * a.blk_in + off;
       }
+      cp_async8(Bs + r * LDB + col, src, ok);
     }
   }
 
-  // ---- DMMA on one staged slice ----------------------------------------------
   static __device__ __forceinline__ void compute_stage(const double* As, const double* Bs,
                                                        double (&acc)[FM][FN][2]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -214,7 +174,6 @@ struct LevelKernel {
     }
   }
 
-  // ---- write-back of the finished tile (inverse fronting folded in) ----------
   static __device__ __forceinline__ void epilogue(const LevelArgs& a, const TileInfo& t,
                                                   double (&acc)[FM][FN][2]) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -232,20 +191,12 @@ struct LevelKernel {
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) {
         const int col = t.nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);
-        if (FAST && a.bAk >= 2) {
-          if (col < a.rest) {
-            const int af = col & (a.bAk - 1);
-            const long long off = af + tstride * (col >> (a.k * a.lbA));
-            *reinterpret_cast<double2*>(base + off) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
-          }
-        } else {
 #pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int cq = col + q;
-            if (cq < a.rest) {
-              const int tt = cq / a.bAk, af = cq - tt * a.bAk;
-              base[af + tstride * tt] = acc[fm][fn][q];
-            }
+        for (int q = 0; q < 2; ++q) {
+          const int cq = col + q;
+          if (cq < a.rest) {
+            const int tt = cq / a.bAk, af = cq - tt * a.bAk;
+            base[af + tstride * tt] = acc[fm][fn][q];
           }
         }
       }
@@ -261,18 +212,15 @@ struct LevelKernel {
     const long long my_items = (a.total_items - 1 - first) / gridDim.x + 1;
     const int ksteps = (a.n + BK - 1) / BK;
     const long long total_steps = my_items * ksteps;
-
     TileInfo ld = decode_item(a, first, BM);
     TileInfo cp = ld;
     int ld_k = 0;
     long long ld_step = 0;
-
     double acc[FM][FN][2];
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
-
     auto advance_load = [&]() {
       ++ld_step;
       if (++ld_k == ksteps) {
@@ -300,6 +248,219 @@ struct LevelKernel {
       cp_async_commit();
       const int slot = (int)(step % STAGES);
       compute_stage(As + slot * A_STAGE, Bs + slot * B_STAGE, acc);
+      if (++cp_k == ksteps) {
+        cp_k = 0;
+        epilogue(a, cp, acc);
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+        if (step + 1 < total_steps) cp = decode_item(a, cp.item + gridDim.x, BM);
+      }
+    }
+    cp_async_wait<0>();
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Fast kernel: power-of-two b_a = BA (compile time) and b_c, reuse=True
+// (insertion redirection).  Per stage (BK = 32 reduction rows) the B tile is
+// G = BK/RG row groups, one stored block S_ib each.  The element (e, col) of
+// the logical block sits at
+//     off = insert_bits(col, at = p*lg(BA), value = e, width = lg(BA))
+// inside S_ib (the contracted digit is spliced into the column index at the
+// insertion position p).  Groups with p == 0 are e-contiguous in HBM and are
+// staged column-major ([col][e], XOR-swizzled quads); the others are
+// column-contiguous and staged row-major ([e][col], padded stride); both with
+// 16-byte cp.async and bank-conflict-free DMMA fragment loads.
+// ---------------------------------------------------------------------------
+template <int BM, int BN, int WM, int WN, int STAGES, int BA>
+struct FastLevelKernel {
+  static constexpr int BK = 32;
+  static constexpr int NT = WM * WN * 32;
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int LBA = (BA == 2) ? 1 : (BA == 4) ? 2 : (BA == 8) ? 3 : (BA == 16) ? 4 : (BA == 32) ? 5 : 6;
+  static constexpr int RG = BA < BK ? BA : BK;  // rows per group (one ib)
+  static constexpr int G = BK / RG;             // groups per stage
+  static constexpr int LDA = BK + 4;
+  static constexpr int LDR = BN + 4;            // row-major group stride ([e][col])
+  static constexpr int GR_SIZE = RG * LDR;      // >= BN*RG, the col-major footprint
+  // col-major swizzle: element (col, e) at col*RG + (e ^ swz(col)); spreads the
+  // four columns a fragment touches over distinct 4-double bank quads.
+  static constexpr int SW_SHIFT = RG >= 16 ? 0 : 1;
+  static constexpr int SW_MASK = RG >= 16 ? 3 : (RG == 8 ? 1 : 0);
+  static __device__ __forceinline__ int swz(int col) { return ((col >> SW_SHIFT) & SW_MASK) << 2; }
+  static constexpr int A_STAGE = BM * LDA, B_STAGE = G * GR_SIZE;
+  static constexpr size_t SMEM_BYTES =
+      (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) + STAGES * G * sizeof(int);
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
+  static_assert((BM * BK / 2) % NT == 0 && (RG * BN / 2) % NT == 0, "loader balance");
+  static_assert((1 << LBA) == BA && RG % 4 == 0, "BA must be a power of two >= 4");
+
+  // ---- operand staging: 16 cp.async.cg per thread per stage ------------------
+  static __device__ __forceinline__ void load_stage(const LevelArgs& a, const TileInfo& t, int kstep,
+                                                    double* As, double* Bs, int* modes) {
+    const int tid = threadIdx.x;
+    const int k0 = kstep * BK;
+    const int rbase = t.mt * BM;
+#pragma unroll
+    for (int it = 0; it < (BM * BK / 2) / NT; ++it) {
+      const int idx = tid + it * NT;
+      const int r = idx / (BK / 2), c = (idx % (BK / 2)) * 2;
+      const bool ok = (rbase + r < t.rows) && (k0 + c < a.n);
+      const double* src = ok ? a.X + (long long)(t.row0 + rbase + r) * a.ldx + k0 + c : a.X;
+      cp_async16(As + r * LDA + c, src, ok);
+    }
+    const int n0 = t.nt * BN;
+    const int2* nrow = a.nbr + (long long)t.key * a.nbar;
+    const double* tin_call = a.Tin + (long long)t.in_call * a.keys_in * a.blk_in;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i0 = k0 + g * RG;            // first reduction row of the group
+      const int ib = i0 >> LBA;
+      const int e0 = i0 & (BA - 1);
+      const bool grp_ok = i0 < a.n;
+      const int2 nb = __ldg(nrow + (grp_ok ? ib : 0));
+      const int pos = code_p(nb.y);
+      const double* base = tin_call + (long long)nb.x * a.blk_in;
+      double* dst = Bs + g * GR_SIZE;
+      if (tid == 0) modes[g] = pos == 0;
+      if (pos == 0) {
+        // e-contiguous: pairs along e, staged [col][e]
+#pragma unroll
+        for (int it = 0; it < (RG * BN / 2) / NT; ++it) {
+          const int q = tid + it * NT;
+          const int e2 = (q % (RG / 2)) * 2, col = q / (RG / 2);
+          const int cg = n0 + col;
+          const bool ok = grp_ok && cg < a.rest;
+          const double* src = ok ? base + (e0 + e2) + ((long long)cg << LBA) : a.X;
+          cp_async16(dst + col * RG + (e2 ^ swz(col)), src, ok);
+        }
+      } else {
+        // column-contiguous: pairs along col, staged [e][col]
+        const int sh = pos * LBA;
+#pragma unroll
+        for (int it = 0; it < (RG * BN / 2) / NT; ++it) {
+          const int q = tid + it * NT;
+          const int c2 = (q % (BN / 2)) * 2, e = q / (BN / 2);
+          const int cg = n0 + c2;
+          const bool ok = grp_ok && cg < a.rest;
+          const long long off = (long long)(cg & ((1 << sh) - 1)) +
+                                ((long long)(cg >> sh) << (sh + LBA)) + ((long long)(e0 + e) << sh);
+          const double* src = ok ? base + off : a.X;
+          cp_async16(dst + e * LDR + c2, src, ok);
+        }
+      }
+    }
+  }
+
+  static __device__ __forceinline__ void compute_stage(const double* As, const double* Bs, const int* modes,
+                                                       double (&acc)[FM][FN][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const double* ap = As + (wm * WTM + (lane >> 2)) * LDA + (lane & 3);
+    const int colw = wn * WTN + (lane >> 2);
+    const int sw = swz(colw);  // same for colw + 8*fn
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const bool cm = modes[g] != 0;
+      // element (e, col) of group g: cm ? col*RG + (e ^ swz(col)) : e*LDR + col
+      const double* bp = Bs + g * GR_SIZE + (cm ? colw * RG + (lane & 3) : (lane & 3) * LDR + colw);
+      const int sn = cm ? 8 * RG : 8;      // next n fragment
+#pragma unroll
+      for (int kk = 0; kk < RG / 4; ++kk) {
+        const int ko = cm ? ((kk * 4) ^ sw) : kk * 4 * LDR;
+        double af[FM], bf[FN];
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm) af[fm] = ap[fm * 8 * LDA + (g * RG + kk * 4)];
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) bf[fn] = bp[ko + fn * sn];
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) dmma(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+      }
+    }
+  }
+
+  static __device__ __forceinline__ void epilogue(const LevelArgs& a, const TileInfo& t,
+                                                  double (&acc)[FM][FN][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wm = warp / WN, wn = warp % WN;
+    const int jb0 = t.row0 / a.bC;
+    const int kl = a.k * LBA;
+    const long long tstride = (long long)a.bAk * a.bC;
+#pragma unroll
+    for (int fm = 0; fm < FM; ++fm) {
+      const int r = t.mt * BM + wm * WTM + fm * 8 + (lane >> 2);
+      if (r >= t.rows) continue;
+      const int xrow = t.row0 + r;
+      const int jb = xrow / a.bC, c = xrow - jb * a.bC;
+      const int call = __ldg(a.child_call + t.child_off + (jb - jb0));
+      double* base = a.Tout + ((long long)call * a.keys_out + t.key) * a.blk_out + (long long)a.bAk * c;
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) {
+        const int col = t.nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);
+        if (col >= a.rest) continue;
+        if (a.bAk >= 2) {
+          const long long off = (col & (a.bAk - 1)) + tstride * (col >> kl);
+          *reinterpret_cast<double2*>(base + off) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+        } else {  // level 0: columns are the tail modes, stride b_c
+          base[tstride * col] = acc[fm][fn][0];
+          base[tstride * (col + 1)] = acc[fm][fn][1];
+        }
+      }
+    }
+  }
+
+  static __device__ void run(const LevelArgs& a) {
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + STAGES * A_STAGE;
+    int* modes = reinterpret_cast<int*>(Bs + STAGES * B_STAGE);
+    const long long first = blockIdx.x;
+    if (first >= a.total_items) return;
+    const long long my_items = (a.total_items - 1 - first) / gridDim.x + 1;
+    const int ksteps = (a.n + BK - 1) / BK;
+    const long long total_steps = my_items * ksteps;
+    TileInfo ld = decode_item(a, first, BM);
+    TileInfo cp = ld;
+    int ld_k = 0;
+    long long ld_step = 0;
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < STAGES - 1; ++s) {
+      if (ld_step < total_steps) {
+        load_stage(a, ld, ld_k, As + s * A_STAGE, Bs + s * B_STAGE, modes + s * G);
+        ++ld_step;
+        if (++ld_k == ksteps) {
+          ld_k = 0;
+          if (ld_step < total_steps) ld = decode_item(a, ld.item + gridDim.x, BM);
+        }
+      }
+      cp_async_commit();
+    }
+    int cp_k = 0;
+    for (long long step = 0; step < total_steps; ++step) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      if (ld_step < total_steps) {
+        const int slot = (int)(ld_step % STAGES);
+        load_stage(a, ld, ld_k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G);
+        ++ld_step;
+        if (++ld_k == ksteps) {
+          ld_k = 0;
+          if (ld_step < total_steps) ld = decode_item(a, ld.item + gridDim.x, BM);
+        }
+      }
+      cp_async_commit();
+      const int slot = (int)(step % STAGES);
+      compute_stage(As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G, acc);
       if (++cp_k == ksteps) {
         cp_k = 0;
         epilogue(a, cp, acc);
