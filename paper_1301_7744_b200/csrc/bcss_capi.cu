@@ -20,7 +20,7 @@
 
 #include "../../include/bcss_sttsm.h"
 #include "combinatorics.hpp"
-#include "sttsm_kernels.cuh"
+#include "kernel_table.cuh"
 
 namespace {
 
@@ -48,36 +48,71 @@ int ilog2(int64_t v) { int r = 0; while ((int64_t(1) << r) < v) ++r; return r; }
 int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; return r; }
 
 // ---- kernel configurations ----------------------------------------------------
-using GenK = bcss::GenericLevelKernel<32, 64, 16, 2, 2, 2>;
-template <int BA>
-using Fast128 = bcss::FastLevelKernel<128, 128, 2, 4, 3, BA>;
+using bcss::KernelCfg;
+using bcss::N_SHAPES;
 
-template <class K>
-__global__ void __launch_bounds__(K::NT, 1) level_kernel(const bcss::LevelArgs a) { K::run(a); }
+// The fast tile shapes' BM (bcss::BCSS_FAST_SHAPES order).
+int shape_bm(int shape) { return bcss::kFast32[shape].BM; }
 
-struct KernelCfg {
-  int BM, BN, NT;
-  size_t smem;
-  void (*fn)(bcss::LevelArgs);
-};
-const KernelCfg kCfgs[] = {
-    {32, 64, GenK::NT, GenK::SMEM_BYTES, level_kernel<GenK>},
-    {128, 128, Fast128<4>::NT, Fast128<4>::SMEM_BYTES, level_kernel<Fast128<4>>},
-    {128, 128, Fast128<8>::NT, Fast128<8>::SMEM_BYTES, level_kernel<Fast128<8>>},
-    {128, 128, Fast128<16>::NT, Fast128<16>::SMEM_BYTES, level_kernel<Fast128<16>>},
-    {128, 128, Fast128<32>::NT, Fast128<32>::SMEM_BYTES, level_kernel<Fast128<32>>},
-};
+const KernelCfg& kernel_cfg(int cfg) {
+  if (cfg == 0) return bcss::kGeneric;
+  const int shape = (cfg - 1) / 4, ba = (cfg - 1) % 4;
+  const KernelCfg* t = ba == 0 ? bcss::kFast4 : ba == 1 ? bcss::kFast8 : ba == 2 ? bcss::kFast16 : bcss::kFast32;
+  return t[shape];
+}
+constexpr int N_CFGS = 1 + 4 * N_SHAPES;
 enum { CFG_GENERIC = 0 };
-// fast configuration for power-of-two b_a in {4, 8, 16, 32}, else -1
-int fast_cfg(int64_t bA) {
+// fast configuration of tile shape `shape` for power-of-two b_a in {4, 8, 16, 32}, else -1
+int fast_cfg(int64_t bA, int shape) {
+  int i;
   switch (bA) {
-    case 4: return 1;
-    case 8: return 2;
-    case 16: return 3;
-    case 32: return 4;
+    case 4: i = 0; break;
+    case 8: i = 1; break;
+    case 16: i = 2; break;
+    case 32: i = 3; break;
     default: return -1;
   }
+  return 1 + shape * 4 + i;
 }
+
+// Relative DMMA efficiency of each tile shape (larger tiles reuse operands
+// more); the plan picks, per parent, the shape minimizing padded work / eff.
+// BCSS_SHAPE_EFF="e128,e64,e32" overrides, BCSS_FORCE_SHAPE=i forces one.
+struct ShapePolicy {
+  // candidate shapes (indices into BCSS_FAST_SHAPES) and their efficiency
+  int cand[N_SHAPES] = {0, 1, 2};
+  double eff[N_SHAPES] = {1.0, 0.92, 0.85};
+  int n_cand = 3;
+  int force = -1;
+  ShapePolicy() {
+    // BCSS_SHAPES="i:eff,i:eff,..." overrides the candidates; BCSS_FORCE_SHAPE=i forces one
+    if (const char* e = getenv("BCSS_SHAPES")) {
+      n_cand = 0;
+      const char* q = e;
+      while (*q && n_cand < N_SHAPES) {
+        int i; double f; int used = 0;
+        if (sscanf(q, "%d:%lf%n", &i, &f, &used) != 2) break;
+        if (i >= 0 && i < N_SHAPES) { cand[n_cand] = i; eff[n_cand] = f; ++n_cand; }
+        q += used;
+        if (*q == ',') ++q;
+      }
+      if (n_cand == 0) { n_cand = 1; cand[0] = 0; eff[0] = 1.0; }
+    }
+    if (const char* f = getenv("BCSS_FORCE_SHAPE")) force = atoi(f);
+  }
+  int pick(int rows) const {
+    if (force >= 0 && force < N_SHAPES) return force;
+    int best = cand[0];
+    double bt = 1e300;
+    for (int ci = 0; ci < n_cand; ++ci) {
+      const int sidx = cand[ci];
+      const int bm = shape_bm(sidx);
+      const double t = (double)((rows + bm - 1) / bm * bm) / eff[ci];
+      if (t < bt - 1e-9) { bt = t; best = sidx; }
+    }
+    return best;
+  }
+};
 
 // Register-resident DMMA loop: 16 independent m8n8k4 accumulators per warp.
 __global__ void dmma_peak_kernel(double* sink, int iters) {
@@ -98,17 +133,26 @@ __global__ void dmma_peak_kernel(double* sink, int iters) {
 }  // namespace
 
 // ---- plan ----------------------------------------------------------------------
-struct LevelHost {
-  int k = 0, cfg = 0;
-  int64_t keys_out = 0, keys_in = 0, blk_out = 0, blk_in = 0, rest = 0, bAk = 0;
+// One kernel launch: the parents of a level that share a tile configuration.
+struct LaunchHost {
+  int cfg = 0;
   int n_tiles = 0;
+  uint64_t flops = 0;
+  std::vector<int4> parents;       // {in_call, row0, rows, child_off}
+  std::vector<long long> item_off; // prefix sums of work items, size parents+1
+  std::vector<int4> items;         // per work item {parent, key, n-tile, m-tile}
+  size_t off_parents = 0, off_items = 0;  // into the device table buffer
+};
+
+struct LevelHost {
+  int k = 0;
+  int64_t keys_out = 0, keys_in = 0, blk_out = 0, blk_in = 0, rest = 0, bAk = 0;
   int64_t n_calls = 0;
   uint64_t flops = 0;
-  std::vector<int4> parents;
-  std::vector<long long> item_off;
+  std::vector<LaunchHost> launches;
   std::vector<int> child_call;
   std::vector<int32_t> suffixes;  // n_calls x (m-k)
-  size_t off_parents = 0, off_items = 0, off_child = 0;  // into the device table buffer
+  size_t off_child = 0;
 };
 
 struct WaveHost {
@@ -228,29 +272,22 @@ size_t peak_for(const bcss_plan& P, const std::vector<int>& units) {
 }
 
 void build_wave_levels(bcss_plan& P, WaveHost& W) {
-  const int fcfg = (P.reuse && is_pow2(P.bC)) ? fast_cfg(P.bA) : -1;
+  const bool fast = P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0;
+  static const ShapePolicy policy;
   W.levels.clear();
   std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls
   int64_t prev_calls = 0;
   for (int k = P.m - 1; k >= 0; --k) {
     LevelHost L;
     L.k = k;
-    L.cfg = fcfg >= 0 ? fcfg : CFG_GENERIC;
     L.keys_out = keys_at(P, k);
     L.keys_in = keys_at(P, k + 1);
     L.blk_out = blk_at(P, k);
     L.blk_in = blk_at(P, k + 1);
     L.bAk = ipow(P.bA, k);
     L.rest = L.bAk * ipow(P.bC, P.m - 1 - k);
-    const KernelCfg& C = kCfgs[L.cfg];
-    L.n_tiles = (int)((L.rest + C.BN - 1) / C.BN);
     const int sl = P.m - k;  // suffix length of this level's calls
-    long long items = 0;
-    auto add_parent = [&](int in_call, int row0, int rows, int child_off) {
-      L.parents.push_back(int4{in_call, row0, rows, child_off});
-      L.item_off.push_back(items);
-      items += (long long)L.keys_out * L.n_tiles * ((rows + C.BM - 1) / C.BM);
-    };
+    std::vector<int4> parents;
     if (k == P.m - 1) {
       for (size_t i = 0; i < W.units.size(); ++i) {
         L.suffixes.push_back(W.units[i]);
@@ -260,7 +297,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
       while (s < W.units.size()) {
         size_t e = s + 1;
         while (e < W.units.size() && W.units[e] == W.units[e - 1] + 1) ++e;
-        add_parent(0, (int)(W.units[s] * P.bC), (int)((e - s) * P.bC), (int)s);
+        parents.push_back(int4{0, (int)(W.units[s] * P.bC), (int)((e - s) * P.bC), (int)s});
         s = e;
       }
       L.n_calls = (int64_t)W.units.size();
@@ -270,7 +307,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
       for (int64_t c = 0; c < prev_calls; ++c) {
         const int32_t* sp = &prev_suffix[(size_t)(c * (sl - 1))];
         const int J = sp[0];
-        add_parent((int)c, 0, (int)((J + 1) * P.bC), (int)running);
+        parents.push_back(int4{(int)c, 0, (int)((J + 1) * P.bC), (int)running});
         for (int jb = 0; jb <= J; ++jb) {
           L.suffixes.push_back(jb);
           for (int q = 0; q < sl - 1; ++q) L.suffixes.push_back(sp[q]);
@@ -286,7 +323,37 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
       }
       L.n_calls = running;
     }
-    L.item_off.push_back(items);
+    // group parents into launches by tile configuration
+    std::map<int, LaunchHost> by_cfg;
+    for (const int4& par : parents) {
+      const int cfg = fast ? fast_cfg(P.bA, policy.pick(par.z)) : CFG_GENERIC;
+      LaunchHost& X = by_cfg[cfg];
+      const KernelCfg& C = kernel_cfg(cfg);
+      if (X.parents.empty()) {
+        X.cfg = cfg;
+        X.n_tiles = (int)((L.rest + C.BN - 1) / C.BN);
+        X.item_off.push_back(0);
+      }
+      X.parents.push_back(par);
+      X.item_off.push_back(X.item_off.back() +
+                           (long long)L.keys_out * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
+      X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
+    }
+    for (auto& kv : by_cfg) {
+      // flat work list: parent-major, then key, n-tile, m-tile (adjacent CTAs
+      // share the B tile of one (key, n-tile))
+      LaunchHost& X = kv.second;
+      const int BM = kernel_cfg(X.cfg).BM;
+      X.items.reserve((size_t)X.item_off.back());
+      for (size_t pi = 0; pi < X.parents.size(); ++pi) {
+        const int mtiles = (X.parents[pi].z + BM - 1) / BM;
+        for (int64_t key = 0; key < L.keys_out; ++key)
+          for (int nt = 0; nt < X.n_tiles; ++nt)
+            for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});
+      }
+      L.flops += kv.second.flops;
+      L.launches.push_back(std::move(kv.second));
+    }
     prev_suffix = L.suffixes;
     prev_calls = L.n_calls;
     W.levels.push_back(std::move(L));
@@ -354,10 +421,11 @@ int build_plan(bcss_plan& P) {
     for (auto& W : P.waves) {
       build_wave_levels(P, W);
       for (auto& L : W.levels) {
-        L.off_parents = take(L.parents.size() * sizeof(int4));
-        L.off_items = take(L.item_off.size() * sizeof(long long));
+        for (auto& X : L.launches) {
+          X.off_parents = take(X.parents.size() * sizeof(int4));
+          X.off_items = take(X.items.size() * sizeof(int4));
+        }
         L.off_child = take(L.child_call.size() * sizeof(int));
-        L.flops = (uint64_t)2 * L.n_calls * P.bC * P.n * L.keys_out * L.rest;
         P.flops += L.flops;
         if (L.k == 0) P.c_blocks += L.n_calls;
       }
@@ -370,7 +438,11 @@ int build_plan(bcss_plan& P) {
   }
 }
 
-int upload_tables(bcss_plan& P) {
+// Upload the device tables once per plan.  The copy is stream-ordered on the
+// run's stream and synchronized: a plain cudaMemcpy from pageable memory can
+// return before its DMA lands, and kernels on a non-blocking stream would
+// then race it.
+int upload_tables(bcss_plan& P, cudaStream_t stream) {
   int dev;
   CUDA_TRY(cudaGetDevice(&dev));
   if (P.d_tables && P.device == dev) return BCSS_OK;
@@ -380,17 +452,22 @@ int upload_tables(bcss_plan& P) {
     if (!P.nbr[k].empty()) memcpy(&host[P.nbr_off[k]], P.nbr[k].data(), P.nbr[k].size() * sizeof(int2));
   for (auto& W : P.waves)
     for (auto& L : W.levels) {
-      memcpy(&host[L.off_parents], L.parents.data(), L.parents.size() * sizeof(int4));
-      memcpy(&host[L.off_items], L.item_off.data(), L.item_off.size() * sizeof(long long));
+      for (auto& X : L.launches) {
+        memcpy(&host[X.off_parents], X.parents.data(), X.parents.size() * sizeof(int4));
+        memcpy(&host[X.off_items], X.items.data(), X.items.size() * sizeof(int4));
+      }
       memcpy(&host[L.off_child], L.child_call.data(), L.child_call.size() * sizeof(int));
     }
   CUDA_TRY(cudaMalloc(&P.d_tables, std::max<size_t>(P.tables_bytes, 256)));
-  CUDA_TRY(cudaMemcpy(P.d_tables, host.data(), P.tables_bytes, cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpyAsync(P.d_tables, host.data(), P.tables_bytes, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
   P.device = dev;
   static bool attr_done[64] = {false};
   if (dev < 64 && !attr_done[dev]) {
-    for (const auto& C : kCfgs)
+    for (int c = 0; c < N_CFGS; ++c) {
+      const KernelCfg& C = kernel_cfg(c);
       CUDA_TRY(cudaFuncSetAttribute(C.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
+    }
     attr_done[dev] = true;
   }
   return BCSS_OK;
@@ -558,7 +635,8 @@ int bcss_plan_stats(bcss_plan* P, int64_t* waves, int64_t* launches, uint64_t* f
   if (st) return st;
   int64_t nl = 0;
   for (auto& W : P->waves)
-    for (auto& L : W.levels) nl += L.item_off.back() > 0 ? 1 : 0;
+    for (auto& L : W.levels)
+      for (auto& X : L.launches) nl += X.item_off.back() > 0 ? 1 : 0;
   if (waves) *waves = (int64_t)P->waves.size();
   if (launches) *launches = nl;
   if (flops) *flops = P->flops;
@@ -566,14 +644,14 @@ int bcss_plan_stats(bcss_plan* P, int64_t* waves, int64_t* launches, uint64_t* f
   return BCSS_OK;
 }
 
-int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X, double* C, void* stream) {
+int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, void* stream) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
-  if (!A || !X || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
+  if (!A || !X_ || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
   int st = build_plan(*P);
   if (st) return st;
-  if ((st = upload_tables(*P))) return st;
-  if ((st = ensure_workspace(*P))) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = upload_tables(*P, s))) return st;
+  if ((st = ensure_workspace(*P))) return st;
   int dev, sms;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -586,48 +664,50 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X, double* C, vo
   }
   for (auto& W : P->waves) {
     for (auto& L : W.levels) {
-      const long long total = L.item_off.back();
-      if (total == 0) continue;
-      const KernelCfg& K = kCfgs[L.cfg];
-      bcss::LevelArgs a;
-      memset(&a, 0, sizeof(a));
-      a.X = X;
-      a.Tin = (L.k == P->m - 1) ? A : region_for(*P, W, L.k + 1);
-      a.Tout = (L.k == 0) ? C : region_for(*P, W, L.k);
-      a.parents = reinterpret_cast<const int4*>(tbl + L.off_parents);
-      a.item_off = reinterpret_cast<const long long*>(tbl + L.off_items);
-      a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
-      a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
-      a.total_items = total;
-      a.keys_in = L.keys_in; a.keys_out = L.keys_out;
-      a.blk_in = L.blk_in; a.blk_out = L.blk_out;
-      a.n_parents = (int)L.parents.size();
-      a.n = (int)P->n; a.ldx = (int)P->n; a.p_rows = (int)P->p;
-      a.nbar = (int)P->nbar; a.bA = (int)P->bA; a.bC = (int)P->bC;
-      a.lbA = is_pow2(P->bA) ? ilog2(P->bA) : -1;
-      a.k = L.k;
-      a.rest = (int)L.rest; a.bAk = (int)L.bAk;
-      a.n_tiles = L.n_tiles;
-      for (int i = 0; i < 10; ++i) a.pw[i] = (long long)std::min<double>(std::pow((double)P->bA, i), 9.0e18);
-      int occ = 1;
-      CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
-      const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
-      if (P->timing) {
-        while (P->events.size() < (size_t)(2 * (launches + 1))) {
-          cudaEvent_t ev;
-          CUDA_TRY(cudaEventCreate(&ev));
-          P->events.push_back(ev);
+      for (auto& X : L.launches) {
+        const long long total = X.item_off.back();
+        if (total == 0) continue;
+        const KernelCfg& K = kernel_cfg(X.cfg);
+        bcss::LevelArgs a;
+        memset(&a, 0, sizeof(a));
+        a.X = X_;
+        a.Tin = (L.k == P->m - 1) ? A : region_for(*P, W, L.k + 1);
+        a.Tout = (L.k == 0) ? C : region_for(*P, W, L.k);
+        a.parents = reinterpret_cast<const int4*>(tbl + X.off_parents);
+        a.items = reinterpret_cast<const int4*>(tbl + X.off_items);
+        a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
+        a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
+        a.total_items = total;
+        a.keys_in = L.keys_in; a.keys_out = L.keys_out;
+        a.blk_in = L.blk_in; a.blk_out = L.blk_out;
+        a.n_parents = (int)X.parents.size();
+        a.n = (int)P->n; a.ldx = (int)P->n; a.p_rows = (int)P->p;
+        a.nbar = (int)P->nbar; a.bA = (int)P->bA; a.bC = (int)P->bC;
+        a.lbA = is_pow2(P->bA) ? ilog2(P->bA) : -1;
+        a.k = L.k;
+        a.rest = (int)L.rest; a.bAk = (int)L.bAk;
+        a.n_tiles = X.n_tiles;
+        for (int i = 0; i < 10; ++i) a.pw[i] = (long long)std::min<double>(std::pow((double)P->bA, i), 9.0e18);
+        int occ = 1;
+        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
+        const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
+        if (P->timing) {
+          while (P->events.size() < (size_t)(2 * (launches + 1))) {
+            cudaEvent_t ev;
+            CUDA_TRY(cudaEventCreate(&ev));
+            P->events.push_back(ev);
+          }
+          CUDA_TRY(cudaEventRecord(P->events[2 * launches], s));
         }
-        CUDA_TRY(cudaEventRecord(P->events[2 * launches], s));
+        K.fn<<<(unsigned)grid, K.NT, K.smem, s>>>(a);
+        CUDA_TRY(cudaGetLastError());
+        if (P->timing) {
+          CUDA_TRY(cudaEventRecord(P->events[2 * launches + 1], s));
+          P->launch_level.push_back(L.k);
+          P->launch_flops.push_back(X.flops);
+        }
+        ++launches;
       }
-      K.fn<<<(unsigned)grid, K.NT, K.smem, s>>>(a);
-      CUDA_TRY(cudaGetLastError());
-      if (P->timing) {
-        CUDA_TRY(cudaEventRecord(P->events[2 * launches + 1], s));
-        P->launch_level.push_back(L.k);
-        P->launch_flops.push_back(L.flops);
-      }
-      ++launches;
     }
   }
   P->last_launches = launches;

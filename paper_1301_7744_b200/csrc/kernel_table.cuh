@@ -1,0 +1,45 @@
+// Table of compiled level-kernel configurations (one translation unit per
+// b_a so the fast kernels build in parallel).
+#pragma once
+
+#include <cstddef>
+
+#include "sttsm_kernels.cuh"
+#include "sttsm_ws_kernel.cuh"
+
+namespace bcss {
+
+struct KernelCfg {
+  int BM, BN, NT;
+  size_t smem;
+  void (*fn)(LevelArgs);
+  const char* name;
+};
+
+template <class K>
+__global__ void __launch_bounds__(K::NT, 1) level_kernel(const LevelArgs a) { K::run(a); }
+
+template <class K>
+KernelCfg make_cfg(const char* name) {
+  return KernelCfg{K::BM, K::BN, K::NT, K::SMEM_BYTES, level_kernel<K>, name};
+}
+
+// Fast tile shapes (BM, BN, BK, warps WM x WN, stages), in the order the
+// plan's shape policy indexes them.  Every b_a instantiates the same list.
+#define BCSS_FAST_SHAPES(X, BA)                                        \
+  X((WsLevelKernel<128, 128, 32, 2, 4, 3, BA>), "ws128x128c8")    \
+  X((WsLevelKernel<64, 256, 16, 2, 4, 4, BA>), "ws64x256c8")      \
+  X((WsLevelKernel<32, 256, 32, 1, 8, 3, BA>), "ws32x256c8")      \
+  X((WsLevelKernel<128, 128, 32, 4, 4, 3, BA>), "ws128x128c16")   \
+  X((WsLevelKernel<64, 256, 16, 2, 8, 4, BA>), "ws64x256c16")     \
+  X((WsLevelKernel<32, 256, 32, 1, 16, 3, BA>), "ws32x256c16")
+
+constexpr int N_SHAPES = 6;
+
+extern const KernelCfg kFast4[N_SHAPES];
+extern const KernelCfg kFast8[N_SHAPES];
+extern const KernelCfg kFast16[N_SHAPES];
+extern const KernelCfg kFast32[N_SHAPES];
+extern const KernelCfg kGeneric;
+
+}  // namespace bcss

@@ -30,7 +30,7 @@ struct LevelArgs {
   const double* Tin;        // [calls_in][keys_in][blk_in]   (A at the top level)
   double* Tout;             // [calls_out][keys_out][blk_out] (packed C at level 0)
   const int4* parents;      // {in_call, row0, rows, child_off}
-  const long long* item_off;  // n_parents + 1 prefix sums of work items
+  const int4* items;        // per work item {parent, key, n-tile, m-tile}
   const int* child_call;    // output call index of (parent child_off + jb - row0/b_c)
   const int2* nbr;          // [keys_out * nbar] {rank in T(k+1) keys, code}
   long long total_items;
@@ -75,25 +75,18 @@ struct TileInfo {
   int in_call, row0, rows, child_off;
 };
 
-__device__ __forceinline__ TileInfo decode_item(const LevelArgs& a, long long item, int BM) {
+__device__ __forceinline__ TileInfo decode_item(const LevelArgs& a, long long item, int /*BM*/) {
   TileInfo t;
   t.item = item;
-  int lo = 0, hi = a.n_parents - 1;  // largest P with item_off[P] <= item
-  while (lo < hi) {
-    const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(a.item_off + mid) <= item) lo = mid; else hi = mid - 1;
-  }
-  const int4 par = __ldg(a.parents + lo);
+  const int4 it = __ldg(a.items + item);
+  const int4 par = __ldg(a.parents + it.x);
+  t.key = it.y;
+  t.nt = it.z;
+  t.mt = it.w;
   t.in_call = par.x;
   t.row0 = par.y;
   t.rows = par.z;
   t.child_off = par.w;
-  const long long local = item - __ldg(a.item_off + lo);
-  const int mtiles = (t.rows + BM - 1) / BM;
-  t.mt = (int)(local % mtiles);
-  const long long q = local / mtiles;
-  t.nt = (int)(q % a.n_tiles);
-  t.key = (int)(q / a.n_tiles);
   return t;
 }
 
@@ -102,8 +95,9 @@ __device__ __forceinline__ TileInfo decode_item(const LevelArgs& a, long long it
 // reuse mode, any redirection permutation.  Per-element addressing with
 // div/mod and zero-filled bounds; correctness path for small/odd problems.
 // ---------------------------------------------------------------------------
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES>
 struct GenericLevelKernel {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int NT = WM * WN * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
@@ -264,7 +258,7 @@ struct GenericLevelKernel {
 
 // ---------------------------------------------------------------------------
 // Fast kernel: power-of-two b_a = BA (compile time) and b_c, reuse=True
-// (insertion redirection).  Per stage (BK = 32 reduction rows) the B tile is
+// (insertion redirection).  Per stage (BK reduction rows) the B tile is
 // G = BK/RG row groups, one stored block S_ib each.  The element (e, col) of
 // the logical block sits at
 //     off = insert_bits(col, at = p*lg(BA), value = e, width = lg(BA))
@@ -274,9 +268,9 @@ struct GenericLevelKernel {
 // column-contiguous and staged row-major ([e][col], padded stride); both with
 // 16-byte cp.async and bank-conflict-free DMMA fragment loads.
 // ---------------------------------------------------------------------------
-template <int BM, int BN, int WM, int WN, int STAGES, int BA>
+template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, int BA>
 struct FastLevelKernel {
-  static constexpr int BK = 32;
+  static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int NT = WM * WN * 32;
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
@@ -292,71 +286,88 @@ struct FastLevelKernel {
   static constexpr int SW_MASK = RG >= 16 ? 3 : (RG == 8 ? 1 : 0);
   static __device__ __forceinline__ int swz(int col) { return ((col >> SW_SHIFT) & SW_MASK) << 2; }
   static constexpr int A_STAGE = BM * LDA, B_STAGE = G * GR_SIZE;
-  static constexpr size_t SMEM_BYTES =
-      (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) + STAGES * G * sizeof(int);
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) +
+                                       STAGES * G * sizeof(int) + STAGES * 2 * sizeof(int4);
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
-  static_assert((BM * BK / 2) % NT == 0 && (RG * BN / 2) % NT == 0, "loader balance");
+  static_assert((BM * BK / 2) % NT == 0 && (BK * BN / 2) % NT == 0 && (RG * BN / 2) % 32 == 0,
+                "loader balance");
   static_assert((1 << LBA) == BA && RG % 4 == 0, "BA must be a power of two >= 4");
+  static_assert(BK == 16 || BK == 32, "stage depth");
+  static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 
-  // ---- operand staging: 16 cp.async.cg per thread per stage ------------------
-  static __device__ __forceinline__ void load_stage(const LevelArgs& a, const TileInfo& t, int kstep,
-                                                    double* As, double* Bs, int* modes) {
+  // ---- operand staging ---------------------------------------------------------
+  // One stage = NA cp.async.cg of the X tile plus NB of the B tile per thread.
+  // They are issued in KP slices, one after each k4 step of the DMMA loop of
+  // the previous stage, so address arithmetic overlaps the tensor pipe.
+  static constexpr int NA = (BM * BK / 2) / NT;
+  static constexpr int GP = RG * BN / 2;          // 16-byte pairs per group
+  static constexpr int NB = (BK * BN / 2) / NT;    // B pairs per thread per stage
+  static constexpr int NU = NA + NB;
+  static constexpr int KP = BK / 4;              // k4 steps per stage = slices
+
+  static __device__ __forceinline__ void load_unit(const LevelArgs& a, const TileInfo& t, int kstep,
+                                                   double* As, double* Bs, int* modes, int u) {
     const int tid = threadIdx.x;
     const int k0 = kstep * BK;
-    const int rbase = t.mt * BM;
-#pragma unroll
-    for (int it = 0; it < (BM * BK / 2) / NT; ++it) {
-      const int idx = tid + it * NT;
+    if (u < NA) {
+      const int idx = tid + u * NT;
       const int r = idx / (BK / 2), c = (idx % (BK / 2)) * 2;
-      const bool ok = (rbase + r < t.rows) && (k0 + c < a.n);
-      const double* src = ok ? a.X + (long long)(t.row0 + rbase + r) * a.ldx + k0 + c : a.X;
+      const int rr = t.mt * BM + r;
+      const bool ok = (rr < t.rows) && (k0 + c < a.n);
+      const double* src = ok ? a.X + (long long)(t.row0 + rr) * a.ldx + k0 + c : a.X;
       cp_async16(As + r * LDA + c, src, ok);
+      return;
     }
+    const int qs = tid + (u - NA) * NT;  // pair index within the stage
+    const int g = qs / GP, q = qs % GP;  // group (warp-uniform: GP >= 32), pair within group
+    const int i0 = k0 + g * RG;  // first reduction row of the group
+    const bool grp_ok = i0 < a.n;
+    const int2 nb = __ldg(a.nbr + (long long)t.key * a.nbar + (grp_ok ? (i0 >> LBA) : 0));
+    const int pos = code_p(nb.y);
+    const double* base = a.Tin + ((long long)t.in_call * a.keys_in + nb.x) * a.blk_in;
+    const int e0 = i0 & (BA - 1);
     const int n0 = t.nt * BN;
-    const int2* nrow = a.nbr + (long long)t.key * a.nbar;
-    const double* tin_call = a.Tin + (long long)t.in_call * a.keys_in * a.blk_in;
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      const int i0 = k0 + g * RG;            // first reduction row of the group
-      const int ib = i0 >> LBA;
-      const int e0 = i0 & (BA - 1);
-      const bool grp_ok = i0 < a.n;
-      const int2 nb = __ldg(nrow + (grp_ok ? ib : 0));
-      const int pos = code_p(nb.y);
-      const double* base = tin_call + (long long)nb.x * a.blk_in;
-      double* dst = Bs + g * GR_SIZE;
-      if (tid == 0) modes[g] = pos == 0;
-      if (pos == 0) {
-        // e-contiguous: pairs along e, staged [col][e]
-#pragma unroll
-        for (int it = 0; it < (RG * BN / 2) / NT; ++it) {
-          const int q = tid + it * NT;
-          const int e2 = (q % (RG / 2)) * 2, col = q / (RG / 2);
-          const int cg = n0 + col;
-          const bool ok = grp_ok && cg < a.rest;
-          const double* src = ok ? base + (e0 + e2) + ((long long)cg << LBA) : a.X;
-          cp_async16(dst + col * RG + (e2 ^ swz(col)), src, ok);
-        }
-      } else {
-        // column-contiguous: pairs along col, staged [e][col]
-        const int sh = pos * LBA;
-#pragma unroll
-        for (int it = 0; it < (RG * BN / 2) / NT; ++it) {
-          const int q = tid + it * NT;
-          const int c2 = (q % (BN / 2)) * 2, e = q / (BN / 2);
-          const int cg = n0 + c2;
-          const bool ok = grp_ok && cg < a.rest;
-          const long long off = (long long)(cg & ((1 << sh) - 1)) +
-                                ((long long)(cg >> sh) << (sh + LBA)) + ((long long)(e0 + e) << sh);
-          const double* src = ok ? base + off : a.X;
-          cp_async16(dst + e * LDR + c2, src, ok);
-        }
-      }
+    double* dst = Bs + g * GR_SIZE;
+    if (q == 0) modes[g] = pos == 0;
+    if (pos == 0) {
+      // e-contiguous: pairs along e, staged [col][e ^ swz]
+      const int e2 = (q % (RG / 2)) * 2, col = q / (RG / 2);
+      const int cg = n0 + col;
+      const bool ok = grp_ok && cg < a.rest;
+      const double* src = ok ? base + (e0 + e2) + ((long long)cg << LBA) : a.X;
+      cp_async16(dst + col * RG + (e2 ^ swz(col)), src, ok);
+    } else {
+      // column-contiguous: pairs along col, staged [e][col]
+      const int sh = pos * LBA;
+      const int c2 = (q % (BN / 2)) * 2, e = q / (BN / 2);
+      const int cg = n0 + c2;
+      const bool ok = grp_ok && cg < a.rest;
+      const long long off = (long long)(cg & ((1 << sh) - 1)) + ((long long)(cg >> sh) << (sh + LBA)) +
+                            ((long long)(e0 + e) << sh);
+      const double* src = ok ? base + off : a.X;
+      cp_async16(dst + e * LDR + c2, src, ok);
     }
   }
 
+  // slice `part` of a stage's loads (compile-time after unrolling)
+  static __device__ __forceinline__ void load_part(const LevelArgs& a, const TileInfo& t, int kstep,
+                                                   double* As, double* Bs, int* modes, bool on, int part) {
+    if (!on) return;
+#pragma unroll
+    for (int u = (part * NU) / KP; u < ((part + 1) * NU) / KP; ++u) load_unit(a, t, kstep, As, Bs, modes, u);
+  }
+
+  static __device__ __forceinline__ void load_stage(const LevelArgs& a, const TileInfo& t, int kstep,
+                                                    double* As, double* Bs, int* modes) {
+#pragma unroll
+    for (int u = 0; u < NU; ++u) load_unit(a, t, kstep, As, Bs, modes, u);
+  }
+
+  // DMMA over one staged slice, with the next stage's loads interleaved.
   static __device__ __forceinline__ void compute_stage(const double* As, const double* Bs, const int* modes,
-                                                       double (&acc)[FM][FN][2]) {
+                                                       double (&acc)[FM][FN][2], const LevelArgs& a,
+                                                       const TileInfo& lt, int lk, double* lAs, double* lBs,
+                                                       int* lmodes, bool lon) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wm = warp / WN, wn = warp % WN;
     const double* ap = As + (wm * WTM + (lane >> 2)) * LDA + (lane & 3);
@@ -380,6 +391,7 @@ struct FastLevelKernel {
         for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
           for (int fn = 0; fn < FN; ++fn) dmma(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+        load_part(a, lt, lk, lAs, lBs, lmodes, lon, g * (RG / 4) + kk);
       }
     }
   }
@@ -418,14 +430,14 @@ struct FastLevelKernel {
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
     double* Bs = smem + STAGES * A_STAGE;
-    int* modes = reinterpret_cast<int*>(Bs + STAGES * B_STAGE);
+    int4* tiles = reinterpret_cast<int4*>(Bs + STAGES * B_STAGE);  // per slot: tile of the staged data
+    int* modes = reinterpret_cast<int*>(tiles + 2 * STAGES);
     const long long first = blockIdx.x;
     if (first >= a.total_items) return;
     const long long my_items = (a.total_items - 1 - first) / gridDim.x + 1;
     const int ksteps = (a.n + BK - 1) / BK;
     const long long total_steps = my_items * ksteps;
     TileInfo ld = decode_item(a, first, BM);
-    TileInfo cp = ld;
     int ld_k = 0;
     long long ld_step = 0;
     double acc[FM][FN][2];
@@ -433,15 +445,25 @@ struct FastLevelKernel {
     for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+    auto note_tile = [&](int slot) {  // remember which tile a slot belongs to (for the epilogue)
+      if (threadIdx.x == 0) {
+        tiles[2 * slot] = make_int4(ld.key, ld.nt, ld.mt, (int)(ld.item & 0x7fffffff));
+        tiles[2 * slot + 1] = make_int4(ld.in_call, ld.row0, ld.rows, ld.child_off);
+      }
+    };
+    auto advance_ld = [&]() {
+      ++ld_step;
+      if (++ld_k == ksteps) {
+        ld_k = 0;
+        if (ld_step < total_steps) ld = decode_item(a, ld.item + gridDim.x, BM);
+      }
+    };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (ld_step < total_steps) {
+        note_tile(s);
         load_stage(a, ld, ld_k, As + s * A_STAGE, Bs + s * B_STAGE, modes + s * G);
-        ++ld_step;
-        if (++ld_k == ksteps) {
-          ld_k = 0;
-          if (ld_step < total_steps) ld = decode_item(a, ld.item + gridDim.x, BM);
-        }
+        advance_ld();
       }
       cp_async_commit();
     }
@@ -449,26 +471,25 @@ struct FastLevelKernel {
     for (long long step = 0; step < total_steps; ++step) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
-      if (ld_step < total_steps) {
-        const int slot = (int)(ld_step % STAGES);
-        load_stage(a, ld, ld_k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G);
-        ++ld_step;
-        if (++ld_k == ksteps) {
-          ld_k = 0;
-          if (ld_step < total_steps) ld = decode_item(a, ld.item + gridDim.x, BM);
-        }
-      }
-      cp_async_commit();
+      const bool lon = ld_step < total_steps;
+      const int lslot = (int)(ld_step % STAGES);
+      if (lon) note_tile(lslot);
       const int slot = (int)(step % STAGES);
-      compute_stage(As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G, acc);
+      compute_stage(As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G, acc, a, ld, ld_k,
+                    As + lslot * A_STAGE, Bs + lslot * B_STAGE, modes + lslot * G, lon);
+      cp_async_commit();
+      if (lon) advance_ld();
       if (++cp_k == ksteps) {
         cp_k = 0;
+        const int4 t0 = tiles[2 * slot], t1 = tiles[2 * slot + 1];
+        TileInfo cp;
+        cp.key = t0.x; cp.nt = t0.y; cp.mt = t0.z; cp.item = t0.w;
+        cp.in_call = t1.x; cp.row0 = t1.y; cp.rows = t1.z; cp.child_off = t1.w;
         epilogue(a, cp, acc);
 #pragma unroll
         for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
           for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
-        if (step + 1 < total_steps) cp = decode_item(a, cp.item + gridDim.x, BM);
       }
     }
     cp_async_wait<0>();

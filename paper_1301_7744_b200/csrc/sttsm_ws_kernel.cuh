@@ -1,0 +1,276 @@
+// Warp-specialized FP64 DMMA level kernel (sm_100a).
+//
+// Same contraction as FastLevelKernel (see sttsm_kernels.cuh for the algebra:
+// one level of _level_product, change_of_basis.py:185-236, with the jb loop
+// fused into M), but the roles are split:
+//   * NPROD producer warps walk the CTA's work items and stage operands with
+//     16-byte cp.async into a STAGES-deep ring; completion is signalled per
+//     slot on a "full" mbarrier (cp.async.mbarrier.arrive.noinc);
+//   * WM x WN consumer warps only load DMMA fragments from shared memory and
+//     issue mma.sync m8n8k4 f64 (SASS DMMA.8x8x4), release each slot on an
+//     "empty" mbarrier and write finished tiles straight from registers.
+// Consumers never execute address arithmetic or wait on global loads, so the
+// FP64 tensor pipe stays fed while producers run ahead by up to STAGES slots.
+#pragma once
+
+#include "sttsm_kernels.cuh"
+
+namespace bcss {
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n.reg .pred p;\nWAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(a), "r"(parity) : "memory");
+}
+
+template <int R>
+__device__ __forceinline__ void regs_dec() { asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(R)); }
+template <int R>
+__device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(R)); }
+
+// NPROD producer warps form whole warpgroups (setmaxnreg acts per warpgroup):
+// they shrink to PROD_REGS registers and the consumers grow into the rest.
+template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, int BA, int NPROD = 4>
+struct WsLevelKernel {
+  static constexpr int BM = BM_, BN = BN_, BK = BK_;
+  static constexpr int NCW = WM * WN;               // consumer warps
+  static_assert(NPROD % 4 == 0 && NCW % 4 == 0, "roles must be whole warpgroups");
+  static constexpr int NT = (NCW + NPROD) * 32;     // threads per CTA
+  // setmaxnreg.inc blocks until the CTA's launch-time pool has the registers,
+  // so the consumers' share is what the producers give back from that pool.
+  static constexpr int LAUNCH_REGS = (65536 / NT) / 8 * 8 > 255 ? 248 : (65536 / NT) / 8 * 8;
+  static constexpr int PROD_REGS = 40;
+  static constexpr int CONS_REGS_RAW = (LAUNCH_REGS * NT - NPROD * 32 * PROD_REGS) / (NCW * 32);
+  static constexpr int CONS_REGS = (CONS_REGS_RAW > 256 ? 256 : CONS_REGS_RAW) / 8 * 8;
+  static constexpr int PT = NPROD * 32;             // producer threads
+  static constexpr int WTM = BM / WM, WTN = BN / WN;
+  static constexpr int FM = WTM / 8, FN = WTN / 8;
+  static constexpr int LBA = (BA == 2) ? 1 : (BA == 4) ? 2 : (BA == 8) ? 3 : (BA == 16) ? 4 : (BA == 32) ? 5 : 6;
+  static constexpr int RG = BA < BK ? BA : BK;  // rows per group (one ib)
+  static constexpr int G = BK / RG;             // groups per stage
+  static constexpr int LDA = BK + 4;
+  static constexpr int LDR = BN + 4;            // row-major group stride ([e][col])
+  static constexpr int GR_SIZE = RG * LDR;      // >= BN*RG (col-major footprint)
+  static constexpr int SW_SHIFT = RG >= 16 ? 0 : 1;
+  static constexpr int SW_MASK = RG >= 16 ? 3 : (RG == 8 ? 1 : 0);
+  static constexpr int A_STAGE = BM * LDA, B_STAGE = G * GR_SIZE;
+  static constexpr int NA = (BM * BK / 2) / PT;  // X pairs per producer thread per stage
+  static constexpr int GP = RG * BN / 2;         // B pairs per group
+  static constexpr int NB = (BK * BN / 2) / PT;  // B pairs per producer thread per stage
+  static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) +
+                                       STAGES * 2 * sizeof(int4) + STAGES * 2 * sizeof(uint64_t) +
+                                       STAGES * G * sizeof(int);
+  static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
+  static_assert((BM * BK / 2) % PT == 0 && (BK * BN / 2) % PT == 0 && GP % 32 == 0, "loader balance");
+  static_assert((1 << LBA) == BA && RG % 4 == 0, "BA must be a power of two >= 4");
+  static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
+
+  static __device__ __forceinline__ int swz(int col) { return ((col >> SW_SHIFT) & SW_MASK) << 2; }
+
+  // ---- producer: one stage of cp.async (PT threads) ----------------------------
+  static __device__ __forceinline__ void produce(const LevelArgs& a, const TileInfo& t, int kstep, double* As,
+                                                 double* Bs, int* modes, int ptid) {
+    const int k0 = kstep * BK;
+#pragma unroll 4
+    for (int u = 0; u < NA; ++u) {
+      const int idx = ptid + u * PT;
+      const int r = idx / (BK / 2), c = (idx % (BK / 2)) * 2;
+      const int rr = t.mt * BM + r;
+      const bool ok = (rr < t.rows) && (k0 + c < a.n);
+      const double* src = ok ? a.X + (long long)(t.row0 + rr) * a.ldx + k0 + c : a.X;
+      cp_async16(As + r * LDA + c, src, ok);
+    }
+    const int n0 = t.nt * BN;
+    const int2* nrow = a.nbr + (long long)t.key * a.nbar;
+    const double* tin_call = a.Tin + (long long)t.in_call * a.keys_in * a.blk_in;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i0 = k0 + g * RG;
+      const bool grp_ok = i0 < a.n;
+      const int2 nb = __ldg(nrow + (grp_ok ? (i0 >> LBA) : 0));
+      const int pos = code_p(nb.y);
+      const double* base = tin_call + (long long)nb.x * a.blk_in;
+      const int e0 = i0 & (BA - 1);
+      double* dst = Bs + g * GR_SIZE;
+      if (ptid == 0) modes[g] = pos == 0;
+      if (pos == 0) {  // e-contiguous block: pairs along e, staged [col][e ^ swz]
+#pragma unroll 4
+        for (int q = ptid; q < GP; q += PT) {
+          const int e2 = (q % (RG / 2)) * 2, col = q / (RG / 2);
+          const int cg = n0 + col;
+          const bool ok = grp_ok && cg < a.rest;
+          const double* src = ok ? base + (e0 + e2) + ((long long)cg << LBA) : a.X;
+          cp_async16(dst + col * RG + (e2 ^ swz(col)), src, ok);
+        }
+      } else {  // column-contiguous block: pairs along col, staged [e][col]
+        const int sh = pos * LBA;
+        const int lomask = (1 << sh) - 1;
+#pragma unroll 4
+        for (int q = ptid; q < GP; q += PT) {
+          const int c2 = (q % (BN / 2)) * 2, e = q / (BN / 2);
+          const int cg = n0 + c2;
+          const bool ok = grp_ok && cg < a.rest;
+          const long long off = (long long)(cg & lomask) + ((long long)(cg >> sh) << (sh + LBA)) +
+                                ((long long)(e0 + e) << sh);
+          const double* src = ok ? base + off : a.X;
+          cp_async16(dst + e * LDR + c2, src, ok);
+        }
+      }
+    }
+  }
+
+  // ---- consumer: DMMA over one staged slice -------------------------------------
+  static __device__ __forceinline__ void consume(const double* As, const double* Bs, const int* modes, int cw,
+                                                 double (&acc)[FM][FN][2]) {
+    const int lane = threadIdx.x & 31;
+    const int wm = cw / WN, wn = cw % WN;
+    const double* ap = As + (wm * WTM + (lane >> 2)) * LDA + (lane & 3);
+    const int colw = wn * WTN + (lane >> 2);
+    const int sw = swz(colw);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const bool cm = modes[g] != 0;
+      const double* bp = Bs + g * GR_SIZE + (cm ? colw * RG + (lane & 3) : (lane & 3) * LDR + colw);
+      const int sn = cm ? 8 * RG : 8;
+#pragma unroll
+      for (int kk = 0; kk < RG / 4; ++kk) {
+        const int ko = cm ? ((kk * 4) ^ sw) : kk * 4 * LDR;
+        double af[FM], bf[FN];
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm) af[fm] = ap[fm * 8 * LDA + (g * RG + kk * 4)];
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) bf[fn] = bp[ko + fn * sn];
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) dmma(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+      }
+    }
+  }
+
+  static __device__ __forceinline__ void epilogue(const LevelArgs& a, const TileInfo& t, int cw,
+                                                  double (&acc)[FM][FN][2]) {
+    const int lane = threadIdx.x & 31;
+    const int wm = cw / WN, wn = cw % WN;
+    const int jb0 = t.row0 / a.bC;
+    const int kl = a.k * LBA;
+    const long long tstride = (long long)a.bAk * a.bC;
+#pragma unroll
+    for (int fm = 0; fm < FM; ++fm) {
+      const int r = t.mt * BM + wm * WTM + fm * 8 + (lane >> 2);
+      if (r >= t.rows) continue;
+      const int xrow = t.row0 + r;
+      const int jb = xrow / a.bC, c = xrow - jb * a.bC;
+      const int call = __ldg(a.child_call + t.child_off + (jb - jb0));
+      double* base = a.Tout + ((long long)call * a.keys_out + t.key) * a.blk_out + (long long)a.bAk * c;
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) {
+        const int col = t.nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);
+        if (col >= a.rest) continue;
+        if (a.bAk >= 2) {
+          const long long off = (col & (a.bAk - 1)) + tstride * (col >> kl);
+          *reinterpret_cast<double2*>(base + off) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+        } else {  // level 0: columns are the tail modes, stride b_c
+          base[tstride * col] = acc[fm][fn][0];
+          base[tstride * (col + 1)] = acc[fm][fn][1];
+        }
+      }
+    }
+  }
+
+  static __device__ void run(const LevelArgs& a) {
+    extern __shared__ __align__(16) double smem[];
+    double* As = smem;
+    double* Bs = smem + STAGES * A_STAGE;
+    int4* tiles = reinterpret_cast<int4*>(Bs + STAGES * B_STAGE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + 2 * STAGES);
+    uint64_t* empty = full + STAGES;
+    int* modes = reinterpret_cast<int*>(empty + STAGES);
+    const long long first = blockIdx.x;
+    if (first >= a.total_items) return;
+    const long long my_items = (a.total_items - 1 - first) / gridDim.x + 1;
+    const int ksteps = (a.n + BK - 1) / BK;
+    const long long total_steps = my_items * ksteps;
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(full + s, PT + 1);   // every producer thread's cp.async batch + one release arrive
+        mbar_init(empty + s, NCW);     // one arrive per consumer warp
+      }
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp >= NCW) {
+      // ---------------- producer warps ----------------
+      regs_dec<PROD_REGS>();
+      const int ptid = threadIdx.x - NCW * 32;
+      TileInfo t = decode_item(a, first, BM);
+      int k = 0;
+      for (long long step = 0; step < total_steps; ++step) {
+        const int slot = (int)(step % STAGES);
+        const unsigned round = (unsigned)(step / STAGES);
+        if (round > 0) mbar_wait(empty + slot, (round - 1) & 1);
+        produce(a, t, k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G, ptid);
+        mbar_arrive_cp_async(full + slot);
+        if (ptid == 0) {
+          tiles[2 * slot] = make_int4(t.key, t.nt, t.mt, k);
+          tiles[2 * slot + 1] = make_int4(t.in_call, t.row0, t.rows, t.child_off);
+          mbar_arrive(full + slot);  // release: tiles / modes visible to consumers
+        }
+        if (++k == ksteps) {
+          k = 0;
+          if (step + 1 < total_steps) t = decode_item(a, t.item + gridDim.x, BM);
+        }
+      }
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      return;
+    }
+    // ---------------- consumer warps ----------------
+    regs_inc<CONS_REGS>();
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+    int k = 0;
+    for (long long step = 0; step < total_steps; ++step) {
+      const int slot = (int)(step % STAGES);
+      mbar_wait(full + slot, (unsigned)(step / STAGES) & 1);
+      consume(As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G, warp, acc);
+      const bool last = (++k == ksteps);
+      TileInfo t;
+      if (last) {
+        const int4 t0 = tiles[2 * slot], t1 = tiles[2 * slot + 1];
+        t.key = t0.x; t.nt = t0.y; t.mt = t0.z; t.item = 0;
+        t.in_call = t1.x; t.row0 = t1.y; t.rows = t1.z; t.child_off = t1.w;
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(empty + slot);
+      if (last) {
+        k = 0;
+        epilogue(a, t, warp, acc);
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm)
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
+      }
+    }
+  }
+};
+
+}  // namespace bcss

@@ -71,7 +71,7 @@ def test_plan_work_equals_cost_model(cfg, reuse):
     m, p, bc = cfg[0], cfg[2], cfg[4]
     ranks = plan.c_block_ranks()
     assert sorted(ranks.tolist()) == list(range(bs.simplex_count(p // bc, m)))
-    assert st["launches"] == m and st["waves"] == 1
+    assert st["launches"] >= m and st["waves"] == 1
 
 
 def test_units_partition_c_blocks_and_flops():

@@ -30,8 +30,15 @@ def main():
             s.record(); plan.run(A, X, C); e.record(); e.synchronize(); ts.append(s.elapsed_time(e))
         ms = sorted(ts)[len(ts) // 2]
         fl = plan.stats()["flops"]
+        plan.set_timing(True)
+        plan.run(A, X, C)
+        lv = {}
+        for k, f, t in plan.launch_times():
+            lv.setdefault(k, [0, 0.0]); lv[k][0] += f; lv[k][1] += t
+        plan.set_timing(False)
         print(json.dumps({"config": c, "ms": ms, "tflops": fl / ms / 1e9, "frac_of_37.1": fl / ms / 1e9 / 37.1,
-                          "ws_gb": plan.workspace_bytes / 1e9}), flush=True)
+                          "ws_gb": plan.workspace_bytes / 1e9, "launches": plan.last_launches,
+                          "levels": {k: [round(v[1], 3), round(v[0] / v[1] / 1e9, 2)] for k, v in lv.items()}}), flush=True)
         del A, X, C, plan
         torch.cuda.empty_cache()
 
