@@ -79,35 +79,45 @@ int fast_cfg(int64_t bA, int shape) {
 // more); the plan picks, per parent, the shape minimizing padded work / eff.
 // BCSS_SHAPE_EFF="e128,e64,e32" overrides, BCSS_FORCE_SHAPE=i forces one.
 struct ShapePolicy {
-  // candidate shapes (indices into BCSS_FAST_SHAPES) and their efficiency
-  int cand[N_SHAPES] = {0, 1, 2};
-  double eff[N_SHAPES] = {1.0, 0.92, 0.85};
-  int n_cand = 3;
+  // Measured full-tile FP64 TFLOP/s of each shape (BCSS_FAST_SHAPES order) per
+  // b_a in {4, 8, 16, 32} on B200 (tools/quick_bench.py with BCSS_FORCE_SHAPE,
+  // unpadded levels); b_a = 4 borrows the b_a = 8 row.
+  double eff[4][N_SHAPES] = {
+      {31.2, 27.5, 26.0, 32.6, 31.5, 27.1},
+      {31.2, 27.5, 26.0, 32.6, 31.5, 27.1},
+      {31.2, 31.9, 30.1, 32.9, 32.0, 29.6},
+      {33.0, 32.2, 31.5, 33.0, 32.2, 30.3},
+  };
   int force = -1;
   ShapePolicy() {
-    // BCSS_SHAPES="i:eff,i:eff,..." overrides the candidates; BCSS_FORCE_SHAPE=i forces one
-    if (const char* e = getenv("BCSS_SHAPES")) {
-      n_cand = 0;
+    // BCSS_SHAPE_EFF="e0,e1,...,e5" overrides every b_a's row; BCSS_FORCE_SHAPE=i forces one
+    if (const char* e = getenv("BCSS_SHAPE_EFF")) {
+      double v[N_SHAPES];
+      int got = 0;
       const char* q = e;
-      while (*q && n_cand < N_SHAPES) {
-        int i; double f; int used = 0;
-        if (sscanf(q, "%d:%lf%n", &i, &f, &used) != 2) break;
-        if (i >= 0 && i < N_SHAPES) { cand[n_cand] = i; eff[n_cand] = f; ++n_cand; }
+      while (got < N_SHAPES) {
+        int used = 0;
+        if (sscanf(q, "%lf%n", &v[got], &used) != 1) break;
+        ++got;
         q += used;
         if (*q == ',') ++q;
       }
-      if (n_cand == 0) { n_cand = 1; cand[0] = 0; eff[0] = 1.0; }
+      if (got == N_SHAPES)
+        for (auto& row : eff)
+          for (int i = 0; i < N_SHAPES; ++i) row[i] = v[i];
     }
     if (const char* f = getenv("BCSS_FORCE_SHAPE")) force = atoi(f);
   }
-  int pick(int rows) const {
+  // shape minimizing padded rows / throughput for a parent with `rows` rows
+  int pick(int rows, int64_t bA) const {
     if (force >= 0 && force < N_SHAPES) return force;
-    int best = cand[0];
+    const int bi = bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3;
+    int best = 0;
     double bt = 1e300;
-    for (int ci = 0; ci < n_cand; ++ci) {
-      const int sidx = cand[ci];
+    for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
+      if (eff[bi][sidx] <= 0) continue;
       const int bm = shape_bm(sidx);
-      const double t = (double)((rows + bm - 1) / bm * bm) / eff[ci];
+      const double t = (double)((rows + bm - 1) / bm * bm) / eff[bi][sidx];
       if (t < bt - 1e-9) { bt = t; best = sidx; }
     }
     return best;
@@ -326,7 +336,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
     // group parents into launches by tile configuration
     std::map<int, LaunchHost> by_cfg;
     for (const int4& par : parents) {
-      const int cfg = fast ? fast_cfg(P.bA, policy.pick(par.z)) : CFG_GENERIC;
+      const int cfg = fast ? fast_cfg(P.bA, policy.pick(par.z, P.bA)) : CFG_GENERIC;
       LaunchHost& X = by_cfg[cfg];
       const KernelCfg& C = kernel_cfg(cfg);
       if (X.parents.empty()) {
