@@ -1,0 +1,152 @@
+"""Parity at BASELINE.json's full sizes.
+
+The numpy oracle is too slow for whole full-size problems, so these tests use
+(1) the oracle on sampled top-level subtrees of the full problem,
+(2) exact structural identities (a permutation / truncation X turns the
+    change of basis into a pure re-indexing of A: bitwise equality),
+(3) a multilinear checksum  C(v,..,v) == A(X^T v,..,X^T v)  evaluated
+    independently in torch fp64, and
+(4) linearity in A.
+"""
+
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import paper_1301_7744_b200 as bs  # noqa: E402
+from oracle import bcss_oracle as orc  # noqa: E402
+from paper_1301_7744_b200.generate import random_bcss_device, random_matrix_device  # noqa: E402
+
+CFG = {2: (3, 512, 512, 32, 32), 3: (4, 192, 192, 16, 16), 4: (5, 96, 96, 8, 8), 5: (4, 512, 256, 32, 32)}
+
+
+def run(cfg, a, x):
+    m, n, p, ba, bc = cfg
+    plan = bs.SttsmPlan(m, n, p, ba, bc)
+    c = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
+    plan.run(a, x, c)
+    torch.cuda.synchronize()
+    plan.close()
+    return c
+
+
+@pytest.mark.parametrize("cfg_id,units", [(2, [0, 1, 15]), (3, [0, 1]), (4, [0, 1])])
+def test_full_size_subtrees_match_oracle(cfg_id, units):
+    """Oracle on whole top-level subtrees of the full-size problem."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 11 + cfg_id)
+    x = random_matrix_device(p, n, 12 + cfg_id)
+    c = run(CFG[cfg_id], a, x).cpu().numpy()
+    want = orc.sttsm_bcss_packed(a.cpu().numpy(), x.cpu().numpy(), m, n, ba, bc, units=units)
+    mask = np.zeros(bs.simplex_count(p // bc, m), dtype=bool)
+    for r in bs.SttsmPlan(m, n, p, ba, bc, units=units).c_block_ranks():
+        mask[r] = True
+    got_b = c.reshape(-1, bc**m)[mask]
+    want_b = want.reshape(-1, bc**m)[mask]
+    assert orc.rel_frobenius(got_b, want_b) <= 1e-12
+    assert orc.max_rel(got_b, want_b) <= 1e-10
+
+
+def _block_perm(nbar, b, seed):
+    """X = permutation matrix mapping output index j -> input index pi(j) with
+    pi = (block permutation sigma) x (within-block permutation tau)."""
+    rng = np.random.default_rng(seed)
+    sigma = rng.permutation(nbar)
+    tau = rng.permutation(b)
+    return sigma, tau
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3, 5])
+def test_permutation_x_reindexes_a_bitwise(cfg_id):
+    """X[j, pi(j)] = 1: C[j_0..j_{m-1}] = A[pi(j_0)..pi(j_{m-1})] exactly (every
+    output is one product of ones with one entry of A).  With p < n (config 5)
+    X is a truncated permutation.  Checks every C block at full size."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    assert ba == bc
+    nbar, pbar = n // ba, p // bc
+    sigma, tau = _block_perm(nbar, ba, 100 + cfg_id)
+    sigma = sigma[:pbar]
+    pi = (sigma[:, None] * ba + tau[None, :]).reshape(-1)  # output row j -> input col
+    x = torch.zeros(p, n, dtype=torch.float64, device="cuda")
+    x[torch.arange(p, device="cuda"), torch.as_tensor(pi, device="cuda")] = 1.0
+    a = random_bcss_device(m, n, ba, 21 + cfg_id)
+    c = run(CFG[cfg_id], a, x)
+    blocks_a = a.view(-1, *([ba] * m))  # torch axes = F-order modes reversed
+    blocks_c = c.view(-1, *([bc] * m))
+    tau_t = torch.as_tensor(tau, device="cuda")
+    keys = list(itertools.combinations_with_replacement(range(pbar), m))
+    # group output blocks by the canonicalize permutation of their source index
+    for r, key in enumerate(keys):
+        src = tuple(int(sigma[j]) for j in key)
+        canon, mapping = bs.canonicalize(src)
+        blk = blocks_a[bs.hypertriangle_rank(canon, nbar)]
+        # logical block (modes d) = stored block transposed by mapping; torch axes reversed
+        order = [m - 1 - mapping[m - 1 - ax] for ax in range(m)]
+        logical = blk.permute(*order)
+        for ax in range(m):
+            logical = logical.index_select(ax, tau_t)
+        assert torch.equal(blocks_c[r], logical), (key, src)
+
+
+def _mult(key):
+    cnt = {}
+    for v in key:
+        cnt[v] = cnt.get(v, 0) + 1
+    out = math.factorial(len(key))
+    for c in cnt.values():
+        out //= math.factorial(c)
+    return out
+
+
+def multilinear_form(packed, m, dim, b, v):
+    """sum over the dense tensor of T[i] * prod_d v[i_d], from canonical blocks
+    with their orbit multiplicities (each block's entries summed densely)."""
+    g = dim // b
+    keys = list(itertools.combinations_with_replacement(range(g), m))
+    blocks = packed.view(len(keys), *([b] * m))
+    vb = v.view(g, b)
+    idx = torch.as_tensor(keys, device=v.device)           # (nblk, m)
+    mult = torch.as_tensor([_mult(k) for k in keys], dtype=torch.float64, device=v.device)
+    vals, absvals = torch.zeros((), dtype=torch.float64, device=v.device), 0.0
+    step = 256
+    letters = "abcdefgh"[:m]
+    for s in range(0, len(keys), step):
+        blk = blocks[s:s + step]
+        ops = [vb[idx[s:s + step, m - 1 - ax]] for ax in range(m)]  # torch axis ax = mode m-1-ax
+        expr = "z" + letters + "," + ",".join("z" + letters[ax] for ax in range(m)) + "->z"
+        per = torch.einsum(expr, blk, *ops)
+        vals = vals + (mult[s:s + step] * per).sum()
+        per_abs = torch.einsum(expr, blk.abs(), *[o.abs() for o in ops])
+        absvals += float((mult[s:s + step] * per_abs).sum())
+    return float(vals), absvals
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3, 4, 5])
+def test_multilinear_checksum(cfg_id):
+    """C(v, .., v) == A(X^T v, .., X^T v) for a random v (torch fp64)."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 31 + cfg_id)
+    x = random_matrix_device(p, n, 32 + cfg_id)
+    c = run(CFG[cfg_id], a, x)
+    v = torch.randn(p, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(7))
+    lhs, lhs_abs = multilinear_form(c, m, p, bc, v)
+    rhs, rhs_abs = multilinear_form(a, m, n, ba, x.t() @ v)
+    assert abs(lhs - rhs) <= 1e-11 * max(lhs_abs, rhs_abs)
+
+
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_linearity_in_a(cfg_id):
+    m, n, p, ba, bc = CFG[cfg_id]
+    a1 = random_bcss_device(m, n, ba, 41)
+    a2 = random_bcss_device(m, n, ba, 42)
+    x = random_matrix_device(p, n, 43)
+    c1, c2 = run(CFG[cfg_id], a1, x), run(CFG[cfg_id], a2, x)
+    c12 = run(CFG[cfg_id], a1 - 0.5 * a2, x)
+    ref = c1 - 0.5 * c2
+    assert float((c12 - ref).norm() / ref.norm()) <= 1e-13
