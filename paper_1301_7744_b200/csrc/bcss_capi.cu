@@ -80,13 +80,13 @@ int fast_cfg(int64_t bA, int shape) {
 // BCSS_SHAPE_EFF="e128,e64,e32" overrides, BCSS_FORCE_SHAPE=i forces one.
 struct ShapePolicy {
   // Measured full-tile FP64 TFLOP/s of each shape (BCSS_FAST_SHAPES order) per
-  // b_a in {4, 8, 16, 32} on B200 (tools/quick_bench.py with BCSS_FORCE_SHAPE,
-  // unpadded levels); b_a = 4 borrows the b_a = 8 row.
+  // b_a in {4, 8, 16, 32} on B200 (tools/calibrate_shapes.py: top level of configs 2/3/4, padding
+  // corrected); b_a = 4 borrows the b_a = 8 row.
   double eff[4][N_SHAPES] = {
-      {31.2, 27.5, 26.0, 32.6, 31.5, 27.1},
-      {31.2, 27.5, 26.0, 32.6, 31.5, 27.1},
-      {31.2, 31.9, 30.1, 32.9, 32.0, 29.6},
-      {33.0, 32.2, 31.5, 33.0, 32.2, 30.3},
+      {32.41, 29.79, 29.22, 31.77, 31.21, 28.96, 19.84, 31.05},
+      {32.41, 29.79, 29.22, 31.77, 31.21, 28.96, 19.84, 31.05},
+      {32.87, 31.52, 30.56, 32.53, 31.61, 30.48, 23.08, 31.46},
+      {33.01, 32.24, 31.73, 32.62, 32.04, 30.96, 21.68, 32.01},
   };
   int force = -1;
   ShapePolicy() {

@@ -53,7 +53,7 @@ struct WsLevelKernel {
   // setmaxnreg.inc blocks until the CTA's launch-time pool has the registers,
   // so the consumers' share is what the producers give back from that pool.
   static constexpr int LAUNCH_REGS = (65536 / NT) / 8 * 8 > 255 ? 248 : (65536 / NT) / 8 * 8;
-  static constexpr int PROD_REGS = 40;
+  static constexpr int PROD_REGS = 56;
   static constexpr int CONS_REGS_RAW = (LAUNCH_REGS * NT - NPROD * 32 * PROD_REGS) / (NCW * 32);
   static constexpr int CONS_REGS = (CONS_REGS_RAW > 256 ? 256 : CONS_REGS_RAW) / 8 * 8;
   static constexpr int PT = NPROD * 32;             // producer threads
@@ -71,9 +71,12 @@ struct WsLevelKernel {
   static constexpr int NA = (BM * BK / 2) / PT;  // X pairs per producer thread per stage
   static constexpr int GP = RG * BN / 2;         // B pairs per group
   static constexpr int NB = (BK * BN / 2) / PT;  // B pairs per producer thread per stage
+  static constexpr int GPAD = (G + 3) / 4 * 4;   // modes per slot, int4-aligned
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) +
-                                       STAGES * 2 * sizeof(int4) + STAGES * 2 * sizeof(uint64_t) +
-                                       STAGES * G * sizeof(int);
+                                       (size_t)STAGES * BM * sizeof(long long) +  // output row offsets
+                                       STAGES * sizeof(int4) + STAGES * 2 * sizeof(uint64_t) +
+                                       STAGES * GPAD * sizeof(int);
+  static_assert(BM <= PT, "one producer thread per output row");
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
   static_assert((BM * BK / 2) % PT == 0 && (BK * BN / 2) % PT == 0 && GP % 32 == 0, "loader balance");
   static_assert((1 << LBA) == BA && RG % 4 == 0, "BA must be a power of two >= 4");
@@ -141,9 +144,15 @@ struct WsLevelKernel {
     const double* ap = As + (wm * WTM + (lane >> 2)) * LDA + (lane & 3);
     const int colw = wn * WTN + (lane >> 2);
     const int sw = swz(colw);
+    int md[GPAD];
+#pragma unroll
+    for (int g4 = 0; g4 < GPAD; g4 += 4) {
+      const int4 v = *reinterpret_cast<const int4*>(modes + g4);
+      md[g4] = v.x; md[g4 + 1] = v.y; md[g4 + 2] = v.z; md[g4 + 3] = v.w;
+    }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const bool cm = modes[g] != 0;
+      const bool cm = md[g] != 0;
       const double* bp = Bs + g * GR_SIZE + (cm ? colw * RG + (lane & 3) : (lane & 3) * LDR + colw);
       const int sn = cm ? 8 * RG : 8;
 #pragma unroll
@@ -162,24 +171,31 @@ struct WsLevelKernel {
     }
   }
 
-  static __device__ __forceinline__ void epilogue(const LevelArgs& a, const TileInfo& t, int cw,
+  // Output offset (in doubles, relative to Tout) of row r of the tile, or -1:
+  // the inverse fronting puts row (jb, c) of call `child_call[...]`, key K at
+  // (call*keys_out + K)*blk_out + b_A^k*c (change_of_basis.py:231-235).
+  static __device__ __forceinline__ long long row_offset(const LevelArgs& a, const TileInfo& t, int r_local) {
+    const int r = t.mt * BM + r_local;
+    if (r >= t.rows) return -1;
+    const int xrow = t.row0 + r;
+    const int jb = xrow / a.bC, c = xrow - jb * a.bC;
+    const int call = __ldg(a.child_call + t.child_off + (jb - t.row0 / a.bC));
+    return ((long long)call * a.keys_out + t.key) * a.blk_out + (long long)a.bAk * c;
+  }
+
+  static __device__ __forceinline__ void epilogue(const LevelArgs& a, const long long (&roff)[FM], int nt, int cw,
                                                   double (&acc)[FM][FN][2]) {
     const int lane = threadIdx.x & 31;
-    const int wm = cw / WN, wn = cw % WN;
-    const int jb0 = t.row0 / a.bC;
+    const int wn = cw % WN;
     const int kl = a.k * LBA;
     const long long tstride = (long long)a.bAk * a.bC;
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
-      const int r = t.mt * BM + wm * WTM + fm * 8 + (lane >> 2);
-      if (r >= t.rows) continue;
-      const int xrow = t.row0 + r;
-      const int jb = xrow / a.bC, c = xrow - jb * a.bC;
-      const int call = __ldg(a.child_call + t.child_off + (jb - jb0));
-      double* base = a.Tout + ((long long)call * a.keys_out + t.key) * a.blk_out + (long long)a.bAk * c;
+      if (roff[fm] < 0) continue;
+      double* base = a.Tout + roff[fm];
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) {
-        const int col = t.nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);
+        const int col = nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);
         if (col >= a.rest) continue;
         if (a.bAk >= 2) {
           const long long off = (col & (a.bAk - 1)) + tstride * (col >> kl);
@@ -196,8 +212,9 @@ struct WsLevelKernel {
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
     double* Bs = smem + STAGES * A_STAGE;
-    int4* tiles = reinterpret_cast<int4*>(Bs + STAGES * B_STAGE);
-    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + 2 * STAGES);
+    long long* rowoff = reinterpret_cast<long long*>(Bs + STAGES * B_STAGE);
+    int4* tiles = reinterpret_cast<int4*>(rowoff + STAGES * BM);
+    uint64_t* full = reinterpret_cast<uint64_t*>(tiles + STAGES);
     uint64_t* empty = full + STAGES;
     int* modes = reinterpret_cast<int*>(empty + STAGES);
     const long long first = blockIdx.x;
@@ -208,7 +225,7 @@ struct WsLevelKernel {
     const int warp = threadIdx.x >> 5;
     if (threadIdx.x == 0) {
       for (int s = 0; s < STAGES; ++s) {
-        mbar_init(full + s, PT + 1);   // every producer thread's cp.async batch + one release arrive
+        mbar_init(full + s, 2 * PT);   // every producer thread: its cp.async batch + a release arrive
         mbar_init(empty + s, NCW);     // one arrive per consumer warp
       }
       asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -220,21 +237,24 @@ struct WsLevelKernel {
       regs_dec<PROD_REGS>();
       const int ptid = threadIdx.x - NCW * 32;
       TileInfo t = decode_item(a, first, BM);
-      int k = 0;
+      long long my_roff = ptid < BM ? row_offset(a, t, ptid) : -1;  // fetched a tile ahead of use
+      int k = 0, slot = 0;
+      unsigned phase = 0;
       for (long long step = 0; step < total_steps; ++step) {
-        const int slot = (int)(step % STAGES);
-        const unsigned round = (unsigned)(step / STAGES);
-        if (round > 0) mbar_wait(empty + slot, (round - 1) & 1);
-        produce(a, t, k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G, ptid);
+        if (step >= STAGES) mbar_wait(empty + slot, phase ^ 1);
+        produce(a, t, k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * GPAD, ptid);
         mbar_arrive_cp_async(full + slot);
-        if (ptid == 0) {
-          tiles[2 * slot] = make_int4(t.key, t.nt, t.mt, k);
-          tiles[2 * slot + 1] = make_int4(t.in_call, t.row0, t.rows, t.child_off);
-          mbar_arrive(full + slot);  // release: tiles / modes visible to consumers
-        }
+        const bool last = (k == ksteps - 1);
+        if (last && ptid < BM) rowoff[slot * BM + ptid] = my_roff;
+        if (last && ptid == 0) tiles[slot] = make_int4(t.nt, 0, 0, 0);
+        mbar_arrive(full + slot);  // release this thread's modes / rowoff / tiles writes
+        if (++slot == STAGES) { slot = 0; phase ^= 1; }
         if (++k == ksteps) {
           k = 0;
-          if (step + 1 < total_steps) t = decode_item(a, t.item + gridDim.x, BM);
+          if (step + 1 < total_steps) {
+            t = decode_item(a, t.item + gridDim.x, BM);
+            if (ptid < BM) my_roff = row_offset(a, t, ptid);
+          }
         }
       }
       asm volatile("cp.async.wait_all;\n" ::: "memory");
@@ -242,28 +262,32 @@ struct WsLevelKernel {
     }
     // ---------------- consumer warps ----------------
     regs_inc<CONS_REGS>();
+    const int lane = threadIdx.x & 31;
+    const int wm = warp / WN;
     double acc[FM][FN][2];
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
-    int k = 0;
+    int k = 0, slot = 0;
+    unsigned phase = 0;
     for (long long step = 0; step < total_steps; ++step) {
-      const int slot = (int)(step % STAGES);
-      mbar_wait(full + slot, (unsigned)(step / STAGES) & 1);
-      consume(As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * G, warp, acc);
+      mbar_wait(full + slot, phase);
+      consume(As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * GPAD, warp, acc);
       const bool last = (++k == ksteps);
-      TileInfo t;
-      if (last) {
-        const int4 t0 = tiles[2 * slot], t1 = tiles[2 * slot + 1];
-        t.key = t0.x; t.nt = t0.y; t.mt = t0.z; t.item = 0;
-        t.in_call = t1.x; t.row0 = t1.y; t.rows = t1.z; t.child_off = t1.w;
+      long long roff[FM];
+      int nt = 0;
+      if (last) {  // read the tile's output rows before the slot is released
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm) roff[fm] = rowoff[slot * BM + wm * WTM + fm * 8 + (lane >> 2)];
+        nt = tiles[slot].x;
       }
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(empty + slot);
+      if (lane == 0) mbar_arrive(empty + slot);
+      if (++slot == STAGES) { slot = 0; phase ^= 1; }
       if (last) {
         k = 0;
-        epilogue(a, t, warp, acc);
+        epilogue(a, roff, nt, warp, acc);
 #pragma unroll
         for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
