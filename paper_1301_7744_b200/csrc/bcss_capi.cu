@@ -199,7 +199,14 @@ struct bcss_plan {
   cudaStream_t host_stream = nullptr;
   int64_t last_launches = 0;
   bool timing = false;
-  std::vector<cudaEvent_t> events;  // 2 per launch
+  bool dynamic = false;             // dynamic work queues (kernels use the static stride today)
+  bool concurrent = true;           // concurrent launches per level (BCSS_SERIAL_LAUNCH=1 disables)
+  unsigned* d_counters = nullptr;
+  size_t counters_n = 0;
+  std::vector<cudaStream_t> side;   // concurrent launches of one level
+  std::vector<cudaEvent_t> join;
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> events;  // 2 per timed level
   std::vector<int> launch_level;
   std::vector<uint64_t> launch_flops;
   cudaStream_t timed_stream = nullptr;
@@ -575,6 +582,8 @@ int bcss_plan_create(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int 
   if (!P) return fail(BCSS_ERR_NOMEM, "out of host memory");
   P->m = m; P->n = n; P->p = p; P->bA = b_a; P->bC = b_c;
   P->nbar = n / b_a; P->pbar = p / b_c; P->reuse = reuse != 0;
+  if (const char* e = getenv("BCSS_DYNAMIC_SCHEDULE")) P->dynamic = atoi(e) != 0;
+  if (const char* e = getenv("BCSS_SERIAL_LAUNCH")) P->concurrent = atoi(e) == 0;
   *out_plan = P;
   return BCSS_OK;
 }
@@ -588,6 +597,10 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->hC) cudaFree(P->hC);
   if (P->host_stream) cudaStreamDestroy(P->host_stream);
   for (auto ev : P->events) cudaEventDestroy(ev);
+  for (auto ev : P->join) cudaEventDestroy(ev);
+  for (auto ss : P->side) cudaStreamDestroy(ss);
+  if (P->fork) cudaEventDestroy(P->fork);
+  if (P->d_counters) cudaFree(P->d_counters);
   delete P;
   return BCSS_OK;
 }
@@ -672,10 +685,51 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
     P->launch_flops.clear();
     P->timed_stream = s;
   }
+  // Launches of one level (one per tile shape) are independent: they run
+  // concurrently on side streams and pull items from per-launch work queues,
+  // so a launch's tail overlaps the next one's CTAs instead of idling SMs.
+  size_t n_launch_total = 0;
+  for (auto& W : P->waves)
+    for (auto& L : W.levels) n_launch_total += L.launches.size();
+  if (P->counters_n < n_launch_total) {
+    if (P->d_counters) cudaFree(P->d_counters);
+    P->d_counters = nullptr;
+    CUDA_TRY(cudaMalloc(&P->d_counters, n_launch_total * sizeof(unsigned)));
+    P->counters_n = n_launch_total;
+  }
+  CUDA_TRY(cudaMemsetAsync(P->d_counters, 0, n_launch_total * sizeof(unsigned), s));
+  size_t counter_idx = 0;
+  int level_idx = 0;
   for (auto& W : P->waves) {
     for (auto& L : W.levels) {
-      for (auto& X : L.launches) {
+      const int nl = (int)L.launches.size();
+      const bool conc = P->concurrent && nl > 1;
+      while (conc && (int)P->side.size() < nl - 1) {
+        cudaStream_t ss;
+        CUDA_TRY(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+        P->side.push_back(ss);
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        P->join.push_back(ev);
+      }
+      if (!P->fork) CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+      if (P->timing) {
+        while (P->events.size() < (size_t)(2 * (level_idx + 1))) {
+          cudaEvent_t ev;
+          CUDA_TRY(cudaEventCreate(&ev));
+          P->events.push_back(ev);
+        }
+        CUDA_TRY(cudaEventRecord(P->events[2 * level_idx], s));
+      }
+      if (conc) {
+        CUDA_TRY(cudaEventRecord(P->fork, s));
+        for (int i = 1; i < nl; ++i) CUDA_TRY(cudaStreamWaitEvent(P->side[i - 1], P->fork, 0));
+      }
+      for (int li = 0; li < nl; ++li) {
+        auto& X = L.launches[li];
+        cudaStream_t ls = (li == 0 || !conc) ? s : P->side[li - 1];
         const long long total = X.item_off.back();
+        unsigned* counter = P->d_counters + counter_idx++;
         if (total == 0) continue;
         const KernelCfg& K = kernel_cfg(X.cfg);
         bcss::LevelArgs a;
@@ -687,6 +741,7 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
         a.items = reinterpret_cast<const int4*>(tbl + X.off_items);
         a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
         a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
+        a.counter = P->dynamic ? counter : nullptr;
         a.total_items = total;
         a.keys_in = L.keys_in; a.keys_out = L.keys_out;
         a.blk_in = L.blk_in; a.blk_out = L.blk_out;
@@ -701,23 +756,22 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
         int occ = 1;
         CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
         const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
-        if (P->timing) {
-          while (P->events.size() < (size_t)(2 * (launches + 1))) {
-            cudaEvent_t ev;
-            CUDA_TRY(cudaEventCreate(&ev));
-            P->events.push_back(ev);
-          }
-          CUDA_TRY(cudaEventRecord(P->events[2 * launches], s));
-        }
-        K.fn<<<(unsigned)grid, K.NT, K.smem, s>>>(a);
+        K.fn<<<(unsigned)grid, K.NT, K.smem, ls>>>(a);
         CUDA_TRY(cudaGetLastError());
-        if (P->timing) {
-          CUDA_TRY(cudaEventRecord(P->events[2 * launches + 1], s));
-          P->launch_level.push_back(L.k);
-          P->launch_flops.push_back(X.flops);
-        }
         ++launches;
       }
+      if (conc) {
+        for (int i = 1; i < nl; ++i) {
+          CUDA_TRY(cudaEventRecord(P->join[i - 1], P->side[i - 1]));
+          CUDA_TRY(cudaStreamWaitEvent(s, P->join[i - 1], 0));
+        }
+      }
+      if (P->timing) {
+        CUDA_TRY(cudaEventRecord(P->events[2 * level_idx + 1], s));
+        P->launch_level.push_back(L.k);
+        P->launch_flops.push_back(L.flops);
+      }
+      ++level_idx;
     }
   }
   P->last_launches = launches;
