@@ -64,6 +64,8 @@ def parse_args():
                     help="target CPU seconds of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--pipeline", type=int, default=4,
+                    help="waves of the e2e transfer/compute pipeline (0 = serial copies)")
     return ap.parse_args()
 
 
@@ -270,12 +272,14 @@ def run_ours(args) -> None:
         x_h = X.cpu().pin_memory()
         c_h = torch.empty(plan.c_elems, dtype=torch.float64).pin_memory()
         a_np, x_np, c_np = a_h.numpy(), x_h.numpy(), c_h.numpy()
-        plan.run_host(a_np, x_np, c_np)  # warm: allocates the plan's device buffers
+        plan_e2e = plan if (world > 1 or not args.pipeline) else bs.SttsmPlan(m, n, p, ba, bc,
+                                                                               pipeline=args.pipeline)
+        plan_e2e.run_host(a_np, x_np, c_np)  # warm: allocates the plan's device buffers
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            plan.run_host(a_np, x_np, c_np)
+            plan_e2e.run_host(a_np, x_np, c_np)
         e2e_s = time.perf_counter() - t0
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
@@ -285,7 +289,10 @@ def run_ours(args) -> None:
                "h2d_bytes_per_step": int(a_h.numel() * 8 + x_h.numel() * 8),
                "d2h_bytes_per_step": int(c_h.numel() * 8),
                "ms_per_step": round(e2e_s / args.steps * 1e3, 3),
-               "api": "SttsmPlan.run_host (C ABI bcss_sttsm_run_host), pinned host buffers"}
+               "api": "SttsmPlan.run_host (C ABI bcss_sttsm_run_host), pinned host buffers",
+               "pipeline_waves": args.pipeline if plan_e2e is not plan else 0}
+        if plan_e2e is not plan:
+            plan_e2e.close()
         del a_h, x_h, c_h
 
     cpu = None

@@ -117,9 +117,16 @@ int bcss_sttsm_run(bcss_plan* plan, const double* A_packed, const double* X, dou
 
 /* Host-buffer run (the reference's call shape): copies A and X to the device,
  * runs, copies C back and synchronizes.  Pinned host memory gives full
- * PCIe bandwidth; pageable memory works too. */
+ * PCIe bandwidth; pageable memory works too.  With a pipeline set (below) and
+ * pinned buffers, the A upload, the compute and the C download overlap. */
 int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X,
                         double* C_packed);
+
+/* Overlap host transfers with compute in bcss_sttsm_run_host: A is uploaded
+ * in chunks (blocks with first index a) that gate the first wave's top-level
+ * work, and the top-level units are split into `waves` flop-balanced groups
+ * whose C blocks download while later groups compute.  0 = off. */
+int bcss_plan_set_pipeline(bcss_plan* plan, int waves);
 
 /* Device pointer and element count of the temporary T(k) produced for the
  * call whose suffix is (jb_k, ..., jb_{m-1}) (nondecreasing, m-k entries),

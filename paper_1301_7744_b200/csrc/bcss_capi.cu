@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cmath>
@@ -166,9 +167,11 @@ struct LevelHost {
 };
 
 struct WaveHost {
-  std::vector<int> units;
-  std::vector<LevelHost> levels;  // levels[i] has k = m-1-i
-  std::vector<size_t> level_off;  // byte offset of T(k)'s region in the workspace
+  std::vector<int> units;          // top-level units whose lower levels this wave computes
+  std::vector<LevelHost> levels;   // k = m-1 (if top_units is non-empty) down to 0
+  std::vector<size_t> level_off;   // byte offset of T(k)'s region in the workspace
+  std::vector<int> top_units;      // units of the top level computed in this wave (may be a superset)
+  std::vector<int> top_call;       // per unit of `units`: its call index in the T(m-1) buffer
 };
 
 struct bcss_plan {
@@ -201,6 +204,12 @@ struct bcss_plan {
   bool timing = false;
   bool dynamic = false;             // dynamic work queues (kernels use the static stride today)
   bool concurrent = true;           // concurrent launches per level (BCSS_SERIAL_LAUNCH=1 disables)
+  int pipeline_waves = 0;           // run_host: overlap H2D / compute / D2H over this many waves
+  bool top_first = false;           // first wave computes T(m-1) for all units
+  cudaStream_t copy_in = nullptr, copy_out = nullptr, copy_out2 = nullptr;
+  cudaEvent_t out2_done = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;  // A chunk (first block index a) landed
+  std::vector<cudaEvent_t> wave_ev;   // a wave's C blocks are final
   unsigned* d_counters = nullptr;
   size_t counters_n = 0;
   std::vector<cudaStream_t> side;   // concurrent launches of one level
@@ -293,8 +302,17 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
   static const ShapePolicy policy;
   W.levels.clear();
   std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls
+  std::vector<int> prev_call;        // their call index in the T(k+1) buffer
   int64_t prev_calls = 0;
-  for (int k = P.m - 1; k >= 0; --k) {
+  const bool has_top = !W.top_units.empty();
+  if (!has_top) {  // the top level was computed by an earlier wave
+    for (size_t i = 0; i < W.units.size(); ++i) {
+      prev_suffix.push_back(W.units[i]);
+      prev_call.push_back(W.top_call[i]);
+    }
+    prev_calls = (int64_t)W.units.size();
+  }
+  for (int k = has_top ? P.m - 1 : P.m - 2; k >= 0; --k) {
     LevelHost L;
     L.k = k;
     L.keys_out = keys_at(P, k);
@@ -306,25 +324,28 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
     const int sl = P.m - k;  // suffix length of this level's calls
     std::vector<int4> parents;
     if (k == P.m - 1) {
-      for (size_t i = 0; i < W.units.size(); ++i) {
-        L.suffixes.push_back(W.units[i]);
+      const std::vector<int>& tu = W.top_units;
+      for (size_t i = 0; i < tu.size(); ++i) {
+        L.suffixes.push_back(tu[i]);
         L.child_call.push_back((int)i);
       }
       size_t s = 0;
-      while (s < W.units.size()) {
+      while (s < tu.size()) {
         size_t e = s + 1;
-        while (e < W.units.size() && W.units[e] == W.units[e - 1] + 1) ++e;
-        parents.push_back(int4{0, (int)(W.units[s] * P.bC), (int)((e - s) * P.bC), (int)s});
+        while (e < tu.size() && tu[e] == tu[e - 1] + 1) ++e;
+        parents.push_back(int4{0, (int)(tu[s] * P.bC), (int)((e - s) * P.bC), (int)s});
         s = e;
       }
-      L.n_calls = (int64_t)W.units.size();
+      L.n_calls = (int64_t)tu.size();
+      // the lower levels of this wave start from its own units
+      prev_call.assign(W.top_call.begin(), W.top_call.end());
     } else {
       int64_t running = 0;
       std::vector<int64_t> full(P.m);
       for (int64_t c = 0; c < prev_calls; ++c) {
         const int32_t* sp = &prev_suffix[(size_t)(c * (sl - 1))];
         const int J = sp[0];
-        parents.push_back(int4{(int)c, 0, (int)((J + 1) * P.bC), (int)running});
+        parents.push_back(int4{prev_call[(size_t)c], 0, (int)((J + 1) * P.bC), (int)running});
         for (int jb = 0; jb <= J; ++jb) {
           L.suffixes.push_back(jb);
           for (int q = 0; q < sl - 1; ++q) L.suffixes.push_back(sp[q]);
@@ -371,10 +392,28 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
       L.flops += kv.second.flops;
       L.launches.push_back(std::move(kv.second));
     }
-    prev_suffix = L.suffixes;
-    prev_calls = L.n_calls;
+    if (k == P.m - 1) {
+      prev_suffix.clear();
+      for (int u : W.units) prev_suffix.push_back(u);
+      prev_calls = (int64_t)W.units.size();
+    } else {
+      prev_suffix = L.suffixes;
+      prev_call.resize((size_t)L.n_calls);
+      for (int64_t c = 0; c < L.n_calls; ++c) prev_call[(size_t)c] = (int)c;
+      prev_calls = L.n_calls;
+    }
     W.levels.push_back(std::move(L));
   }
+}
+
+// Exact flops of top-level subtree u: sum over levels of (calls of the
+// subtree at level k) x 2*b_c*n*keys(k)*rest(k).
+double unit_cost(const bcss_plan& P, int u) {
+  double f = 0;
+  for (int k = P.m - 1; k >= 0; --k)
+    f += (double)calls_for(P, {u}, k) * 2.0 * P.bC * P.n * keys_at(P, k) *
+         (double)(ipow(P.bA, k) * ipow(P.bC, P.m - 1 - k));
+  return f;
 }
 
 int build_plan(bcss_plan& P) {
@@ -385,37 +424,87 @@ int build_plan(bcss_plan& P) {
       for (int u = 0; u < P.pbar; ++u) units.push_back(u);
     std::sort(units.begin(), units.end());
     units.erase(std::unique(units.begin(), units.end()), units.end());
+    // pipeline groups: contiguous units with ~equal flops, largest units first
+    // (run_host downloads one group's C while later groups compute, so the
+    // last group - the one whose download is not overlapped - is the smallest)
+    std::vector<std::vector<int>> groups;
+    if (P.pipeline_waves > 1 && !P.keep_temps && units.size() > 1) {
+      double tot = 0;
+      for (int u : units) tot += unit_cost(P, u);
+      const double target = tot / P.pipeline_waves;
+      double acc = 0;
+      groups.emplace_back();
+      for (auto it = units.rbegin(); it != units.rend(); ++it) {
+        const double c = unit_cost(P, *it);
+        if (!groups.back().empty() && acc + c / 2 > target * groups.size() &&
+            (int)groups.size() < P.pipeline_waves)
+          groups.emplace_back();
+        groups.back().push_back(*it);
+        acc += c;
+      }
+      for (auto& g : groups) std::sort(g.begin(), g.end());
+    } else {
+      groups.push_back(units);
+    }
     // waves: greedy groups of units whose live temporaries fit the limit
     P.waves.clear();
-    std::vector<int> cur;
-    for (int u : units) {
-      std::vector<int> trial = cur;
-      trial.push_back(u);
-      if (!cur.empty() && !P.keep_temps && P.ws_limit > 0 && peak_for(P, trial) > P.ws_limit) {
-        P.waves.push_back(WaveHost{cur, {}, {}});
-        cur = {u};
-      } else {
-        cur = trial;
+    for (const auto& grp : groups) {
+      std::vector<int> cur;
+      for (int u : grp) {
+        std::vector<int> trial = cur;
+        trial.push_back(u);
+        if (!cur.empty() && !P.keep_temps && P.ws_limit > 0 && peak_for(P, trial) > P.ws_limit) {
+          P.waves.push_back(WaveHost{cur, {}, {}, {}, {}});
+          cur = {u};
+        } else {
+          cur = trial;
+        }
       }
+      if (!cur.empty()) P.waves.push_back(WaveHost{cur, {}, {}, {}, {}});
     }
-    if (!cur.empty()) P.waves.push_back(WaveHost{cur, {}, {}});
     if (!P.keep_temps && P.ws_limit > 0) {
       for (auto& W : P.waves)
         if (peak_for(P, W.units) > P.ws_limit)
           return fail(BCSS_ERR_NOMEM, "one top-level unit needs %zu workspace bytes > limit %zu",
                       peak_for(P, W.units), P.ws_limit);
     }
+    // Top level: with a pipeline, the first wave computes T(m-1) for every
+    // unit (it overlaps the chunked upload of A) and later waves only run the
+    // levels below; otherwise every wave computes its own units' top level.
+    P.top_first = P.pipeline_waves > 1 && P.waves.size() > 1 && !P.keep_temps;
+    {
+      std::vector<int> all;
+      for (auto& W : P.waves) all.insert(all.end(), W.units.begin(), W.units.end());
+      std::sort(all.begin(), all.end());
+      for (size_t wi = 0; wi < P.waves.size(); ++wi) {
+        WaveHost& W = P.waves[wi];
+        W.top_units = P.top_first ? (wi == 0 ? all : std::vector<int>{}) : W.units;
+        const std::vector<int>& ref = P.top_first ? all : W.units;
+        W.top_call.clear();
+        for (int u : W.units)
+          W.top_call.push_back((int)(std::lower_bound(ref.begin(), ref.end(), u) - ref.begin()));
+      }
+    }
     // Workspace layout per wave: keep_temps gives every level its own region;
     // otherwise levels alternate between two regions (T(k+1) is read while
-    // T(k) is written).  The workspace is the largest wave's footprint.
+    // T(k) is written); with top_first, T(m-1) of all units has its own
+    // region and the lower levels alternate behind it.
     P.ws_bytes = 0;
     auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+    size_t top_bytes = 0;
+    if (P.top_first) top_bytes = al(level_bytes(P, P.waves[0].top_units)[P.m - 1]);
     for (auto& W : P.waves) {
       auto b = level_bytes(P, W.units);
       W.level_off.assign(P.m + 1, 0);
       size_t end = 0;
       if (P.keep_temps) {
         for (int k = 1; k < P.m; ++k) { W.level_off[k] = end; end += al(b[k]); }
+      } else if (P.top_first) {
+        size_t r[2] = {0, 0};
+        for (int k = 1; k < P.m - 1; ++k) r[(P.m - 2 - k) % 2] = std::max(r[(P.m - 2 - k) % 2], al(b[k]));
+        W.level_off[P.m - 1] = 0;
+        for (int k = 1; k < P.m - 1; ++k) W.level_off[k] = top_bytes + ((P.m - 2 - k) % 2 == 0 ? 0 : r[0]);
+        end = top_bytes + r[0] + r[1];
       } else {
         size_t r[2] = {0, 0};
         for (int k = 1; k < P.m; ++k) r[(P.m - 1 - k) % 2] = std::max(r[(P.m - 1 - k) % 2], al(b[k]));
@@ -600,6 +689,12 @@ int bcss_plan_destroy(bcss_plan* P) {
   for (auto ev : P->join) cudaEventDestroy(ev);
   for (auto ss : P->side) cudaStreamDestroy(ss);
   if (P->fork) cudaEventDestroy(P->fork);
+  for (auto ev : P->chunk_ev) cudaEventDestroy(ev);
+  for (auto ev : P->wave_ev) cudaEventDestroy(ev);
+  if (P->copy_in) cudaStreamDestroy(P->copy_in);
+  if (P->copy_out) cudaStreamDestroy(P->copy_out);
+  if (P->copy_out2) cudaStreamDestroy(P->copy_out2);
+  if (P->out2_done) cudaEventDestroy(P->out2_done);
   if (P->d_counters) cudaFree(P->d_counters);
   delete P;
   return BCSS_OK;
@@ -667,18 +762,94 @@ int bcss_plan_stats(bcss_plan* P, int64_t* waves, int64_t* launches, uint64_t* f
   return BCSS_OK;
 }
 
-int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, void* stream) {
-  if (!P) return fail(BCSS_ERR_STATE, "null plan");
-  if (!A || !X_ || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
+}  // extern "C"
+
+namespace {
+
+// Host-transfer pipeline of run_host: A arrives in chunks (blocks whose first
+// index is a, a contiguous range of the packed payload), wave 0's top level
+// is split by key ranges that need only the chunks already landed, and each
+// wave's C blocks are downloaded while later waves compute.
+struct Pipe {
+  double* c_host = nullptr;
+  // BCSS_TRACE=1: timing events (name, event) printed after the run
+  std::vector<std::pair<std::string, cudaEvent_t>>* trace = nullptr;
+};
+
+void trace_mark(const Pipe* pipe, const std::string& name, cudaStream_t s) {
+  if (!pipe || !pipe->trace) return;
+  cudaEvent_t ev;
+  cudaError_t e1 = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaError_t e2 = cudaEventRecord(ev, s);
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    fprintf(stderr, "[bcss trace] %s: %s / %s\n", name.c_str(), cudaGetErrorString(e1), cudaGetErrorString(e2));
+  pipe->trace->emplace_back(name, ev);
+}
+
+int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const LaunchHost& X, const double* A,
+               const double* X_, double* C, long long item_lo, long long item_hi, unsigned* counter,
+               cudaStream_t ls, int sms) {
+  const long long total = item_hi - item_lo;
+  if (total <= 0) return BCSS_OK;
+  const KernelCfg& K = kernel_cfg(X.cfg);
+  char* tbl = static_cast<char*>(P->d_tables);
+  bcss::LevelArgs a;
+  memset(&a, 0, sizeof(a));
+  a.X = X_;
+  a.Tin = (L.k == P->m - 1) ? A : region_for(*P, W, L.k + 1);
+  a.Tout = (L.k == 0) ? C : region_for(*P, W, L.k);
+  a.parents = reinterpret_cast<const int4*>(tbl + X.off_parents);
+  a.items = reinterpret_cast<const int4*>(tbl + X.off_items) + item_lo;
+  a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
+  a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
+  a.counter = P->dynamic ? counter : nullptr;
+  a.total_items = total;
+  a.keys_in = L.keys_in; a.keys_out = L.keys_out;
+  a.blk_in = L.blk_in; a.blk_out = L.blk_out;
+  a.n_parents = (int)X.parents.size();
+  a.n = (int)P->n; a.ldx = (int)P->n; a.p_rows = (int)P->p;
+  a.nbar = (int)P->nbar; a.bA = (int)P->bA; a.bC = (int)P->bC;
+  a.lbA = is_pow2(P->bA) ? ilog2(P->bA) : -1;
+  a.k = L.k;
+  a.rest = (int)L.rest; a.bAk = (int)L.bAk;
+  a.n_tiles = X.n_tiles;
+  for (int i = 0; i < 10; ++i) a.pw[i] = (long long)std::min<double>(std::pow((double)P->bA, i), 9.0e18);
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
+  const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
+  K.fn<<<(unsigned)grid, K.NT, K.smem, ls>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return BCSS_OK;
+}
+
+int ensure_side(bcss_plan* P, int n) {
+  while ((int)P->side.size() < n) {
+    cudaStream_t ss;
+    CUDA_TRY(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    P->side.push_back(ss);
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    P->join.push_back(ev);
+  }
+  if (!P->fork) CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+  return BCSS_OK;
+}
+
+// first packed rank of the m-tuples over `extent` whose first index is a
+int64_t first_rank_with(int64_t a, int m, int64_t extent) {
+  if (a >= extent) return bcss::simplex_count(extent, m);
+  std::vector<int64_t> t(m, a);
+  return bcss::hypertriangle_rank(t.data(), m, extent);
+}
+
+int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStream_t s, const Pipe* pipe) {
   int st = build_plan(*P);
   if (st) return st;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   if ((st = upload_tables(*P, s))) return st;
   if ((st = ensure_workspace(*P))) return st;
   int dev, sms;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  char* tbl = static_cast<char*>(P->d_tables);
   int64_t launches = 0;
   if (P->timing) {
     P->launch_level.clear();
@@ -686,8 +857,8 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
     P->timed_stream = s;
   }
   // Launches of one level (one per tile shape) are independent: they run
-  // concurrently on side streams and pull items from per-launch work queues,
-  // so a launch's tail overlaps the next one's CTAs instead of idling SMs.
+  // concurrently on side streams, so one launch's tail overlaps the next
+  // launch's CTAs instead of idling SMs.
   size_t n_launch_total = 0;
   for (auto& W : P->waves)
     for (auto& L : W.levels) n_launch_total += L.launches.size();
@@ -700,19 +871,17 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
   CUDA_TRY(cudaMemsetAsync(P->d_counters, 0, n_launch_total * sizeof(unsigned), s));
   size_t counter_idx = 0;
   int level_idx = 0;
-  for (auto& W : P->waves) {
-    for (auto& L : W.levels) {
+  const size_t blk_c = (size_t)ipow(P->bC, P->m);
+  for (size_t wi = 0; wi < P->waves.size(); ++wi) {
+    const WaveHost& W = P->waves[wi];
+    for (const LevelHost& L : W.levels) {
       const int nl = (int)L.launches.size();
-      const bool conc = P->concurrent && nl > 1;
-      while (conc && (int)P->side.size() < nl - 1) {
-        cudaStream_t ss;
-        CUDA_TRY(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
-        P->side.push_back(ss);
-        cudaEvent_t ev;
-        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        P->join.push_back(ev);
-      }
-      if (!P->fork) CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+      // chunk-gated top level of the first wave (pipelined host run)
+      const bool gate = pipe && wi == 0 && L.k == P->m - 1;
+      const bool gate_split = gate && nl == 1 && L.launches[0].parents.size() == 1;
+      if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev.back(), 0));
+      const bool conc = (P->concurrent && nl > 1) || gate_split;
+      if (conc && (st = ensure_side(P, std::max(nl - 1, 1)))) return st;
       if (P->timing) {
         while (P->events.size() < (size_t)(2 * (level_idx + 1))) {
           cudaEvent_t ev;
@@ -723,45 +892,38 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
       }
       if (conc) {
         CUDA_TRY(cudaEventRecord(P->fork, s));
-        for (int i = 1; i < nl; ++i) CUDA_TRY(cudaStreamWaitEvent(P->side[i - 1], P->fork, 0));
+        for (int i = 1; i < std::max(nl, 2); ++i) CUDA_TRY(cudaStreamWaitEvent(P->side[i - 1], P->fork, 0));
       }
-      for (int li = 0; li < nl; ++li) {
-        auto& X = L.launches[li];
-        cudaStream_t ls = (li == 0 || !conc) ? s : P->side[li - 1];
-        const long long total = X.item_off.back();
+      if (gate_split) {
+        // keys with first index <= a need only A chunks 0..a; ~8 sub-launches
+        // alternate between two streams, each waiting for its last chunk
+        const LaunchHost& X = L.launches[0];
+        const int64_t per_key = X.item_off.back() / L.keys_out;
+        const int64_t nb = P->nbar;
+        const int groups = (int)std::min<int64_t>(8, nb);
+        int64_t a0 = 0;
         unsigned* counter = P->d_counters + counter_idx++;
-        if (total == 0) continue;
-        const KernelCfg& K = kernel_cfg(X.cfg);
-        bcss::LevelArgs a;
-        memset(&a, 0, sizeof(a));
-        a.X = X_;
-        a.Tin = (L.k == P->m - 1) ? A : region_for(*P, W, L.k + 1);
-        a.Tout = (L.k == 0) ? C : region_for(*P, W, L.k);
-        a.parents = reinterpret_cast<const int4*>(tbl + X.off_parents);
-        a.items = reinterpret_cast<const int4*>(tbl + X.off_items);
-        a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
-        a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
-        a.counter = P->dynamic ? counter : nullptr;
-        a.total_items = total;
-        a.keys_in = L.keys_in; a.keys_out = L.keys_out;
-        a.blk_in = L.blk_in; a.blk_out = L.blk_out;
-        a.n_parents = (int)X.parents.size();
-        a.n = (int)P->n; a.ldx = (int)P->n; a.p_rows = (int)P->p;
-        a.nbar = (int)P->nbar; a.bA = (int)P->bA; a.bC = (int)P->bC;
-        a.lbA = is_pow2(P->bA) ? ilog2(P->bA) : -1;
-        a.k = L.k;
-        a.rest = (int)L.rest; a.bAk = (int)L.bAk;
-        a.n_tiles = X.n_tiles;
-        for (int i = 0; i < 10; ++i) a.pw[i] = (long long)std::min<double>(std::pow((double)P->bA, i), 9.0e18);
-        int occ = 1;
-        CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
-        const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
-        K.fn<<<(unsigned)grid, K.NT, K.smem, ls>>>(a);
-        CUDA_TRY(cudaGetLastError());
-        ++launches;
+        for (int g = 0; g < groups; ++g) {
+          int64_t a1 = (g == groups - 1) ? nb : std::max(a0 + 1, (nb * (g + 1)) / groups);
+          const int64_t k_lo = first_rank_with(a0, P->m - 1, nb), k_hi = first_rank_with(a1, P->m - 1, nb);
+          cudaStream_t ls = (g % 2 == 0) ? s : P->side[0];
+          CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[a1 - 1], 0));
+          if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, counter, ls, sms))) return st;
+          ++launches;
+          a0 = a1;
+        }
+      } else {
+        for (int li = 0; li < nl; ++li) {
+          const LaunchHost& X = L.launches[li];
+          cudaStream_t ls = (li == 0 || !conc) ? s : P->side[li - 1];
+          unsigned* counter = P->d_counters + counter_idx++;
+          if (X.item_off.back() == 0) continue;
+          if ((st = launch_one(P, W, L, X, A, X_, C, 0, X.item_off.back(), counter, ls, sms))) return st;
+          ++launches;
+        }
       }
       if (conc) {
-        for (int i = 1; i < nl; ++i) {
+        for (int i = 1; i < std::max(nl, 2); ++i) {
           CUDA_TRY(cudaEventRecord(P->join[i - 1], P->side[i - 1]));
           CUDA_TRY(cudaStreamWaitEvent(s, P->join[i - 1], 0));
         }
@@ -772,16 +934,68 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
         P->launch_flops.push_back(L.flops);
       }
       ++level_idx;
+      trace_mark(pipe, "wave" + std::to_string(wi) + " level" + std::to_string(L.k) + " done", s);
+      if (pipe && L.k == 0) {
+        // this wave's C blocks are final: download them (runs of consecutive ranks)
+        CUDA_TRY(cudaEventRecord(P->wave_ev[wi], s));
+        CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->wave_ev[wi], 0));
+        CUDA_TRY(cudaStreamWaitEvent(P->copy_out2, P->wave_ev[wi], 0));
+        int which = 0;  // alternate two DMA streams so per-copy setup overlaps
+        std::vector<int> ranks(L.child_call.begin(), L.child_call.end());
+        std::sort(ranks.begin(), ranks.end());
+        size_t i = 0;
+        while (i < ranks.size()) {
+          size_t j = i + 1;
+          while (j < ranks.size() && ranks[j] == ranks[j - 1] + 1) ++j;
+          const size_t off = (size_t)ranks[i] * blk_c;
+          CUDA_TRY(cudaMemcpyAsync(pipe->c_host + off, C + off, (j - i) * blk_c * sizeof(double),
+                                   cudaMemcpyDeviceToHost, (which ^= 1) ? P->copy_out : P->copy_out2));
+          i = j;
+        }
+        trace_mark(pipe, "wave" + std::to_string(wi) + " C downloaded", P->copy_out);
+        // submit what is queued so far (the driver otherwise batches it until a sync)
+        cudaStreamQuery(s);
+        cudaStreamQuery(P->copy_out);
+        cudaStreamQuery(P->copy_out2);
+      }
     }
   }
   P->last_launches = launches;
   return BCSS_OK;
 }
 
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" {
+
+int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, void* stream) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (!A || !X_ || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
+  return run_impl(P, A, X_, C, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int bcss_plan_set_pipeline(bcss_plan* P, int waves) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (waves < 0) return fail(BCSS_ERR_PARAMETER, "negative wave count");
+  P->pipeline_waves = waves;
+  invalidate(P);
+  return BCSS_OK;
+}
+
 int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* C) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
   if (!A || !X || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
-  const size_t a_bytes = (size_t)bcss::simplex_count(P->nbar, P->m) * ipow(P->bA, P->m) * sizeof(double);
+  const size_t blk_a = (size_t)ipow(P->bA, P->m);
+  const size_t a_bytes = (size_t)bcss::simplex_count(P->nbar, P->m) * blk_a * sizeof(double);
   const size_t x_bytes = (size_t)(P->p * P->n) * sizeof(double);
   const size_t c_bytes = (size_t)bcss::simplex_count(P->pbar, P->m) * ipow(P->bC, P->m) * sizeof(double);
   auto grow = [&](double*& ptr, size_t& cap, size_t need) -> int {
@@ -797,12 +1011,83 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
   if ((st = grow(P->hX, P->hX_bytes, x_bytes))) return st;
   if ((st = grow(P->hC, P->hC_bytes, c_bytes))) return st;
   if (!P->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->host_stream, cudaStreamNonBlocking));
-  CUDA_TRY(cudaMemcpyAsync(P->hA, A, a_bytes, cudaMemcpyHostToDevice, P->host_stream));
-  CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->host_stream));
-  if (P->units_set) CUDA_TRY(cudaMemsetAsync(P->hC, 0, c_bytes, P->host_stream));
-  if ((st = bcss_sttsm_run(P, P->hA, P->hX, P->hC, P->host_stream))) return st;
-  CUDA_TRY(cudaMemcpyAsync(C, P->hC, c_bytes, cudaMemcpyDeviceToHost, P->host_stream));
+  const bool pipelined = P->pipeline_waves > 0 && !P->units_set && !P->keep_temps && is_pinned(A) &&
+                         is_pinned(X) && is_pinned(C);
+  if (!pipelined) {
+    CUDA_TRY(cudaMemcpyAsync(P->hA, A, a_bytes, cudaMemcpyHostToDevice, P->host_stream));
+    CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->host_stream));
+    if (P->units_set) CUDA_TRY(cudaMemsetAsync(P->hC, 0, c_bytes, P->host_stream));
+    if ((st = run_impl(P, P->hA, P->hX, P->hC, P->host_stream, nullptr))) return st;
+    CUDA_TRY(cudaMemcpyAsync(C, P->hC, c_bytes, cudaMemcpyDeviceToHost, P->host_stream));
+    CUDA_TRY(cudaStreamSynchronize(P->host_stream));
+    return BCSS_OK;
+  }
+  const auto h0 = std::chrono::steady_clock::now();
+  if ((st = build_plan(*P))) return st;
+  if (!P->copy_in) CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_in, cudaStreamNonBlocking));
+  if (!P->copy_out) CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_out, cudaStreamNonBlocking));
+  if (!P->copy_out2) CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_out2, cudaStreamNonBlocking));
+  if (!P->out2_done) CUDA_TRY(cudaEventCreateWithFlags(&P->out2_done, cudaEventDisableTiming));
+  auto need_events = [&](std::vector<cudaEvent_t>& v, size_t n) -> int {
+    while (v.size() < n) {
+      cudaEvent_t ev;
+      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      v.push_back(ev);
+    }
+    return BCSS_OK;
+  };
+  if ((st = need_events(P->chunk_ev, (size_t)P->nbar))) return st;
+  if ((st = need_events(P->wave_ev, P->waves.size()))) return st;
+  // everything below is ordered after work already queued on the host stream
+  CUDA_TRY(cudaEventRecord(P->chunk_ev[0], P->host_stream));
+  CUDA_TRY(cudaStreamWaitEvent(P->copy_in, P->chunk_ev[0], 0));
+  CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->chunk_ev[0], 0));
+  CUDA_TRY(cudaStreamWaitEvent(P->copy_out2, P->chunk_ev[0], 0));
+  Pipe pipe;
+  pipe.c_host = C;
+  std::vector<std::pair<std::string, cudaEvent_t>> trace;
+  const char* tr = getenv("BCSS_TRACE");
+  if (tr && atoi(tr) == 1) pipe.trace = &trace;
+  trace_mark(&pipe, "upload start", P->copy_in);
+  CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->copy_in));
+  for (int64_t a = 0; a < P->nbar; ++a) {
+    const size_t r0 = (size_t)first_rank_with(a, P->m, P->nbar), r1 = (size_t)first_rank_with(a + 1, P->m, P->nbar);
+    CUDA_TRY(cudaMemcpyAsync(P->hA + r0 * blk_a, A + r0 * blk_a, (r1 - r0) * blk_a * sizeof(double),
+                             cudaMemcpyHostToDevice, P->copy_in));
+    CUDA_TRY(cudaEventRecord(P->chunk_ev[a], P->copy_in));
+    trace_mark(&pipe, "A chunk " + std::to_string(a) + " landed", P->copy_in);
+  }
+  cudaStreamQuery(P->copy_in);  // kick the driver to submit queued work now
+  if ((st = run_impl(P, P->hA, P->hX, P->hC, P->host_stream, &pipe))) return st;
+  if (pipe.trace) {
+    fprintf(stderr, "[bcss trace] host enqueue took %.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
+    // host-side polling timeline (first time each event is seen complete)
+    std::vector<double> seen(trace.size(), -1.0);
+    const auto t0 = std::chrono::steady_clock::now();
+    size_t left = trace.size();
+    while (left) {
+      const double now = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      for (size_t i = 0; i < trace.size(); ++i)
+        if (seen[i] < 0 && cudaEventQuery(trace[i].second) == cudaSuccess) { seen[i] = now; --left; }
+    }
+    fprintf(stderr, "[bcss trace] run_host pipeline timeline (host-polled ms, relative to upload start):\n");
+    for (size_t i = 0; i < trace.size(); ++i) {
+      fprintf(stderr, "  %-28s %8.3f\n", trace[i].first.c_str(), seen[i] - seen[0]);
+      cudaEventDestroy(trace[i].second);
+    }
+  }
+  const auto h1 = std::chrono::steady_clock::now();
+  CUDA_TRY(cudaStreamSynchronize(P->copy_out));
+  const auto h2 = std::chrono::steady_clock::now();
+  CUDA_TRY(cudaStreamSynchronize(P->copy_out2));
   CUDA_TRY(cudaStreamSynchronize(P->host_stream));
+  const auto h3 = std::chrono::steady_clock::now();
+  if (tr && atoi(tr) == 2)
+    fprintf(stderr, "[bcss trace] enqueue %.3f ms, copy_out sync at %.3f ms, all synced at %.3f ms\n",
+            std::chrono::duration<double, std::milli>(h1 - h0).count(),
+            std::chrono::duration<double, std::milli>(h2 - h0).count(),
+            std::chrono::duration<double, std::milli>(h3 - h0).count());
   return BCSS_OK;
 }
 

@@ -40,7 +40,7 @@ class SttsmPlan:
     """
 
     def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, reuse: bool = True,
-                 units=None, workspace_limit: int = 0, keep_temps: bool = False):
+                 units=None, workspace_limit: int = 0, keep_temps: bool = False, pipeline: int = 0):
         lib = _native.lib()
         self.m, self.n, self.p, self.b_a, self.b_c, self.reuse = m, n, p, b_a, b_c, bool(reuse)
         h = ctypes.c_void_p()
@@ -54,6 +54,9 @@ class SttsmPlan:
             _native.check(lib.bcss_plan_set_workspace_limit(h, int(workspace_limit)))
         if keep_temps:
             _native.check(lib.bcss_plan_set_keep_temps(h, 1))
+        if pipeline:
+            # run_host overlaps A upload / compute / C download over `pipeline` waves
+            _native.check(lib.bcss_plan_set_pipeline(h, int(pipeline)))
         self.units = None if units is None else sorted(set(int(u) for u in units))
         self.a_elems = simplex_count(n // b_a, m) * b_a**m
         self.c_elems = simplex_count(p // b_c, m) * b_c**m

@@ -150,3 +150,22 @@ def test_linearity_in_a(cfg_id):
     c12 = run(CFG[cfg_id], a1 - 0.5 * a2, x)
     ref = c1 - 0.5 * c2
     assert float((c12 - ref).norm() / ref.norm()) <= 1e-13
+
+
+@pytest.mark.parametrize("cfg_id,waves", [(2, 4), (3, 3), (4, 2)])
+def test_pipelined_host_run_is_bitwise_identical(cfg_id, waves):
+    """run_host with the transfer/compute pipeline (pinned buffers, chunk-gated
+    top level, per-wave C downloads) returns exactly the device-path result."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 51 + cfg_id)
+    x = random_matrix_device(p, n, 52 + cfg_id)
+    want = run(CFG[cfg_id], a, x).cpu()
+    plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=waves)
+    assert plan.stats()["waves"] == waves
+    a_h, x_h = a.cpu().pin_memory(), x.cpu().pin_memory()
+    c_h = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    plan.run_host(a_h.numpy(), x_h.numpy(), c_h.numpy())
+    assert torch.equal(c_h, want)
+    c_h.fill_(float("nan"))
+    plan.run_host(a_h.numpy(), x_h.numpy(), c_h.numpy())  # reuse of streams / events
+    assert torch.equal(c_h, want)
