@@ -64,6 +64,8 @@ def parse_args():
                     help="target CPU seconds of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dense", action="store_true",
+                    help="also time the dense mode-product baseline (cuBLAS) when it fits")
     ap.add_argument("--pipeline", type=int, default=4,
                     help="waves of the e2e transfer/compute pipeline (0 = serial copies)")
     return ap.parse_args()
@@ -295,6 +297,32 @@ def run_ours(args) -> None:
             plan_e2e.close()
         del a_h, x_h, c_h
 
+    dense_line = None
+    if args.dense and rank == 0 and world == 1:
+        from paper_1301_7744_b200 import dense as dn
+        need = 3 * max(n, p) ** m * 8
+        free, _ = torch.cuda.mem_get_info(dev)
+        if need < 0.8 * free:
+            a_dense = dn.bcss_to_dense_device(A, m, n, ba)
+            for _ in range(2):
+                dn.sttsm_dense_ttm_device(a_dense, X)
+            torch.cuda.synchronize()
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s0.record()
+            for _ in range(args.steps):
+                dn.sttsm_dense_ttm_device(a_dense, X)
+            s1.record()
+            s1.synchronize()
+            dms = s0.elapsed_time(s1) / args.steps
+            dfl = dn.dense_flops(m, n, p)
+            dense_line = {"ms_per_step": round(dms, 4), "flops_per_step": dfl,
+                          "tflops": round(dfl / dms / 1e9, 3),
+                          "speedup_bcss_vs_dense": round(dms / (job_ms / args.steps), 3),
+                          "impl": "dense mode-product chain, cuBLAS DGEMM via torch.tensordot"}
+            del a_dense
+        else:
+            dense_line = {"skipped": f"dense A needs ~{need / 1e9:.0f} GB"}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         a_np = A.cpu().numpy()
@@ -326,6 +354,7 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
+            "dense_baseline": dense_line,
             "clocks": clocks,
             "flops_per_step": total_flops,
         }

@@ -12,23 +12,8 @@ payloads to both sides instead of regenerating.
 
 from __future__ import annotations
 
-import itertools
-import math
-
-from .indexing import hypertriangle_iter, simplex_count
-
-
-def _runs(key) -> tuple[int, ...]:
-    """Run lengths of equal consecutive values of a sorted block index."""
-    out, cur = [], 1
-    for a, b in zip(key, key[1:]):
-        if a == b:
-            cur += 1
-        else:
-            out.append(cur)
-            cur = 1
-    out.append(cur)
-    return tuple(out)
+from .dense import symmetrize_bcss_device
+from .indexing import simplex_count
 
 
 def random_bcss_device(m: int, n: int, b: int, seed: int, device="cuda", chunk_bytes: int = 1 << 30):
@@ -44,35 +29,8 @@ def random_bcss_device(m: int, n: int, b: int, seed: int, device="cuda", chunk_b
     for s in range(0, nblk, step):  # chunked fill keeps the generator's peak small
         e = min(nblk, s + step)
         out[s * bs:e * bs].uniform_(-1.0, 1.0, generator=g)
-    # group the blocks that need symmetrizing by their repeated-index pattern
-    by_pattern: dict[tuple[int, ...], list[int]] = {}
-    for r, key in enumerate(hypertriangle_iter(grid, m)):
-        runs = _runs(key)
-        if max(runs) > 1:
-            by_pattern.setdefault(runs, []).append(r)
-    blocks = out.view(nblk, *([b] * m))  # torch axes are the F-order modes reversed
-    for runs, ranks in by_pattern.items():
-        groups, start = [], 0
-        for ln in runs:
-            if ln > 1:
-                # modes start..start+ln-1 live on torch axes 1+(m-1-d)
-                groups.append([1 + (m - 1 - d) for d in range(start, start + ln)])
-            start += ln
-        idx_all = torch.tensor(ranks, dtype=torch.long, device=device)
-        for c0 in range(0, len(ranks), step):
-            idx = idx_all[c0:c0 + step]
-            x = blocks.index_select(0, idx)
-            for axes in groups:
-                acc = torch.zeros_like(x)
-                perms = list(itertools.permutations(axes))
-                for perm in perms:
-                    order = list(range(m + 1))
-                    for src, dst in zip(axes, perm):
-                        order[src] = dst
-                    acc += x.permute(order)
-                x = acc / math.factorial(len(axes))
-            blocks.index_copy_(0, idx, x)
-    return out
+    # average every block over its repeated-index mode groups (generate.py:41-50)
+    return symmetrize_bcss_device(out, m, n, b, chunk_blocks=step)
 
 
 def random_matrix_device(p: int, n: int, seed: int, device="cuda"):
