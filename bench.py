@@ -64,6 +64,9 @@ def parse_args():
                     help="target CPU seconds of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--schedule", default="auto", choices=["auto", "s1", "s5"],
+                    help="multi-GPU schedule: s1 = top-level subtrees, no exchange; s5 = owners + "
+                         "T(m-2) exchange + balanced subtrees (auto: s5 for N>1, m>=3)")
     ap.add_argument("--dense", action="store_true",
                     help="also time the dense mode-product baseline (cuBLAS) when it fits")
     ap.add_argument("--pipeline", type=int, default=4,
@@ -192,7 +195,7 @@ def run_ours(args) -> None:
     import torch.distributed as dist
 
     import paper_1301_7744_b200 as bs
-    from paper_1301_7744_b200.distributed import partition_units, unit_flops
+    from paper_1301_7744_b200.distributed import S5Runner, partition_units, unit_flops
     from paper_1301_7744_b200.generate import random_bcss_device, random_matrix_device
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -204,9 +207,23 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=dev)
     m, n, p, ba, bc = CONFIGS[args.config]
     total_flops = bs.bcss_flops(m, n, p, ba, bc)
-    parts = partition_units(unit_flops(m, n, p, ba, bc), world)
-    plan = bs.SttsmPlan(m, n, p, ba, bc, units=parts[rank] if world > 1 else None)
-    my_flops = plan.stats()["flops"]
+    schedule = args.schedule
+    if schedule == "auto":
+        schedule = "s5" if (world > 1 and m >= 3) else "s1"
+    runner = None
+    if schedule == "s5":
+        runner = S5Runner(m, n, p, ba, bc, rank, world, dev, group=None)
+        plans = runner.plans()
+        my_flops = runner.flops
+        c_elems = runner.c_elems
+        plan = None
+    else:
+        parts = partition_units(unit_flops(m, n, p, ba, bc), world)
+        plan = bs.SttsmPlan(m, n, p, ba, bc, units=parts[rank] if world > 1 else None)
+        plans = [plan]
+        my_flops = plan.stats()["flops"]
+        c_elems = plan.c_elems
+    step = runner.run if runner is not None else plan.run
 
     peak = bs.probe_fp64_peak()  # live FP64 DMMA peak of this GPU (roofline denominator)
 
@@ -215,7 +232,7 @@ def run_ours(args) -> None:
         A = random_bcss_device(m, n, ba, SEED, device=dev)
         X = random_matrix_device(p, n, SEED + 1, device=dev)
     else:
-        A = torch.empty(plan.a_elems, dtype=torch.float64, device=dev)
+        A = torch.empty(bs.SttsmPlan(m, n, p, ba, bc).a_elems, dtype=torch.float64, device=dev)
         X = torch.empty(p, n, dtype=torch.float64, device=dev)
     bcast_ms = None
     if world > 1:
@@ -226,15 +243,17 @@ def run_ours(args) -> None:
         dist.broadcast(X, 0)
         torch.cuda.synchronize()
         bcast_ms = (time.perf_counter() - t0) * 1e3
-    C = torch.zeros(plan.c_elems, dtype=torch.float64, device=dev)
-    plan.attach_torch_workspace(dev)
+    C = torch.zeros(c_elems, dtype=torch.float64, device=dev)
+    for pl in plans:
+        pl.attach_torch_workspace(dev)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
     for _ in range(args.warmup):
-        plan.run(A, X, C)
+        step(A, X, C)
     torch.cuda.synchronize()
-    plan.set_timing(True)
+    for pl in plans:
+        pl.set_timing(True)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launch_ms, launch_fl = 0.0, 0
@@ -247,15 +266,16 @@ def run_ours(args) -> None:
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
             starts[i].record(stream)
-            plan.run(A, X, C)
+            step(A, X, C)
             ends[i].record(stream)
-            for k, fl, ms in plan.launch_times():  # syncs the stream
-                launch_ms += ms
-                launch_fl += fl
-                levels.setdefault(k, [0, 0.0])
-                levels[k][0] += fl
-                levels[k][1] += ms
-            launches += plan.last_launches
+            for pl in plans:
+                for k, fl, ms in pl.launch_times():  # syncs the stream
+                    launch_ms += ms
+                    launch_fl += fl
+                    levels.setdefault(k, [0, 0.0])
+                    levels[k][0] += fl
+                    levels[k][1] += ms
+                launches += pl.last_launches
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -265,23 +285,37 @@ def run_ours(args) -> None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     job_ms = float(t.item())
     value = total_flops * args.steps / (job_ms * 1e-3) / 1e9
-    plan.set_timing(False)
+    for pl in plans:
+        pl.set_timing(False)
 
     # end to end through the public host-buffer API (pinned host memory)
     e2e = None
     if not args.no_e2e:
         a_h = A.cpu().pin_memory()
         x_h = X.cpu().pin_memory()
-        c_h = torch.empty(plan.c_elems, dtype=torch.float64).pin_memory()
+        c_h = torch.empty(c_elems, dtype=torch.float64).pin_memory()
         a_np, x_np, c_np = a_h.numpy(), x_h.numpy(), c_h.numpy()
-        plan_e2e = plan if (world > 1 or not args.pipeline) else bs.SttsmPlan(m, n, p, ba, bc,
-                                                                               pipeline=args.pipeline)
-        plan_e2e.run_host(a_np, x_np, c_np)  # warm: allocates the plan's device buffers
+        if runner is not None:
+            # S5: host -> every rank's HBM, the sharded step, own C blocks back
+            def e2e_step():
+                A.copy_(a_h, non_blocking=True)
+                X.copy_(x_h, non_blocking=True)
+                step(A, X, C)
+                c_h.copy_(C, non_blocking=True)
+                torch.cuda.synchronize()
+            plan_e2e = None
+        else:
+            plan_e2e = plan if (world > 1 or not args.pipeline) else bs.SttsmPlan(m, n, p, ba, bc,
+                                                                                   pipeline=args.pipeline)
+
+            def e2e_step():
+                plan_e2e.run_host(a_np, x_np, c_np)
+        e2e_step()  # warm: allocates device buffers
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            plan_e2e.run_host(a_np, x_np, c_np)
+            e2e_step()
         e2e_s = time.perf_counter() - t0
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
@@ -291,9 +325,10 @@ def run_ours(args) -> None:
                "h2d_bytes_per_step": int(a_h.numel() * 8 + x_h.numel() * 8),
                "d2h_bytes_per_step": int(c_h.numel() * 8),
                "ms_per_step": round(e2e_s / args.steps * 1e3, 3),
-               "api": "SttsmPlan.run_host (C ABI bcss_sttsm_run_host), pinned host buffers",
-               "pipeline_waves": args.pipeline if plan_e2e is not plan else 0}
-        if plan_e2e is not plan:
+               "api": ("torch H2D of A/X + S5Runner.run + D2H of C, pinned host buffers" if runner is not None
+                       else "SttsmPlan.run_host (C ABI bcss_sttsm_run_host), pinned host buffers"),
+               "pipeline_waves": args.pipeline if (plan_e2e is not None and plan_e2e is not plan) else 0}
+        if plan_e2e is not None and plan_e2e is not plan:
             plan_e2e.close()
         del a_h, x_h, c_h
 
@@ -343,7 +378,8 @@ def run_ours(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(job_ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(workload(args.config), parallelism=f"c-block shards x{world}" if world > 1 else "single",
+            "config": dict(workload(args.config),
+                           parallelism=(f"{schedule} x{world}" if (world > 1 or schedule == "s5") else "single"),
                            l2="flushed (256 MB write) between timed steps; A and temporaries also exceed L2"),
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
@@ -361,6 +397,8 @@ def run_ours(args) -> None:
         if bcast_ms is not None:
             line["broadcast_ms"] = round(bcast_ms, 3)
             line["rank0_flop_share"] = round(my_flops / total_flops, 4)
+        if runner is not None:
+            line["exchange_bytes_rank0"] = runner.exchange_bytes
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

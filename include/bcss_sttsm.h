@@ -128,6 +128,21 @@ int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X
  * whose C blocks download while later groups compute.  0 = off. */
 int bcss_plan_set_pipeline(bcss_plan* plan, int waves);
 
+/* Partial runs, the exchange points of the multi-GPU schedule:
+ * stop_level > 0 computes levels m-1 .. stop_level only and writes T(stop_level)
+ * (calls in bcss_plan_level_calls order, each keys x block doubles) to the
+ * run's output buffer instead of C;
+ * start calls make the plan compute below the given calls of level `level`
+ * (m-level suffix entries each), reading their T(level) from the run's input
+ * buffer (in the given call order) instead of A.  level = m restores a full run. */
+int bcss_plan_set_stop_level(bcss_plan* plan, int stop_level);
+int bcss_plan_set_start_calls(bcss_plan* plan, int level, const int32_t* suffixes, int n_calls);
+/* Suffixes (m-k entries each) of the plan's level-k calls, in buffer order. */
+int bcss_plan_level_calls(bcss_plan* plan, int k, int32_t* out, int64_t n_max, int64_t* out_n);
+/* Element counts of the run's input (A or start temporaries) and output
+ * (C or stop-level temporaries) buffers. */
+int bcss_plan_io_elems(bcss_plan* plan, int64_t* in_elems, int64_t* out_elems);
+
 /* Device pointer and element count of the temporary T(k) produced for the
  * call whose suffix is (jb_k, ..., jb_{m-1}) (nondecreasing, m-k entries),
  * valid after a run with keep_temps=1.  Blocks are canonical keys in

@@ -173,8 +173,13 @@ def sttsm_naive_dense(a: np.ndarray, x: np.ndarray) -> np.ndarray:
     return c
 
 
+def pack_temp(blocks: dict, k: int, nbar: int) -> np.ndarray:
+    """Packed payload of one temporary T(k) (canonical keys in hypertriangle order)."""
+    return np.concatenate([blocks[key].reshape(-1, order="F") for key in hypertriangle(nbar, k)])
+
+
 def sttsm_bcss_packed(a_packed: np.ndarray, x: np.ndarray, m: int, n: int, b_a: int,
-                      b_c: int, keep_temps: bool = False, units=None):
+                      b_c: int, keep_temps: bool = False, units=None, start=None):
     """Blocked change of basis over packed BCSS storage.
 
     Restates ``sttsm_bcss`` / ``_level_product`` (change_of_basis.py:185-284):
@@ -186,15 +191,19 @@ def sttsm_bcss_packed(a_packed: np.ndarray, x: np.ndarray, m: int, n: int, b_a: 
     (blocks in hypertriangle order) and, with ``keep_temps``, a dict
     ``{(k, suffix): {key: block}}`` of every temporary.  ``units`` restricts
     the outermost loop to those jb_{m-1} values (a top-level subtree sample);
-    C blocks outside them are left zero.
+    C blocks outside them are left zero.  ``start=(L, {suffix: packed T(L)})``
+    skips the levels above L and descends from the given temporaries only
+    (the multi-GPU exchange point; ``a_packed`` is then unused).
     """
     x = np.asarray(x, dtype=np.float64)
     p = x.shape[0]
     nbar, pbar = n // b_a, p // b_c
     blk_a = b_a**m
-    a_blocks = a_packed.reshape(-1, blk_a)
-    top = {key: a_blocks[r].reshape((b_a,) * m, order="F")
-           for r, key in enumerate(hypertriangle(nbar, m))}
+    top = {}
+    if start is None:
+        a_blocks = a_packed.reshape(-1, blk_a)
+        top = {key: a_blocks[r].reshape((b_a,) * m, order="F")
+               for r, key in enumerate(hypertriangle(nbar, m))}
     c_keys = hypertriangle(pbar, m)
     c_out = np.zeros((len(c_keys), b_c**m))
     temps = {}
@@ -231,7 +240,16 @@ def sttsm_bcss_packed(a_packed: np.ndarray, x: np.ndarray, m: int, n: int, b_a: 
                 temps[(k, (jb,) + suffix)] = produced
             descend(k - 1, produced, jb, (jb,) + suffix)
 
-    descend(m - 1, top, pbar - 1, ())
+    if start is None:
+        descend(m - 1, top, pbar - 1, ())
+    else:
+        lvl, given = start
+        shape = (b_a,) * lvl + (b_c,) * (m - lvl)
+        size = int(np.prod(shape))
+        for suffix, flat in given.items():
+            t_in = {key: np.asarray(flat[r * size:(r + 1) * size]).reshape(shape, order="F")
+                    for r, key in enumerate(hypertriangle(nbar, lvl))}
+            descend(lvl - 1, t_in, suffix[0], tuple(suffix))
     c_packed = c_out.reshape(-1)
     return (c_packed, temps) if keep_temps else c_packed
 

@@ -53,6 +53,10 @@ SIGNATURES = {
     "bcss_sttsm_run": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
     "bcss_sttsm_run_host": (_c_int, [_vp, _vp, _vp, _vp]),
     "bcss_plan_set_pipeline": (_c_int, [_vp, _c_int]),
+    "bcss_plan_set_stop_level": (_c_int, [_vp, _c_int]),
+    "bcss_plan_set_start_calls": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _c_int]),
+    "bcss_plan_level_calls": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _i64, _P(_i64)]),
+    "bcss_plan_io_elems": (_c_int, [_vp, _P(_i64), _P(_i64)]),
     "bcss_plan_temp": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _P(_vp), _P(_i64)]),
     "bcss_plan_temp_copy": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _vp, _i64]),
     "bcss_plan_last_launches": (_c_int, [_vp, _P(_i64)]),

@@ -206,6 +206,9 @@ struct bcss_plan {
   bool concurrent = true;           // concurrent launches per level (BCSS_SERIAL_LAUNCH=1 disables)
   int pipeline_waves = 0;           // run_host: overlap H2D / compute / D2H over this many waves
   bool top_first = false;           // first wave computes T(m-1) for all units
+  int start_level = 0;              // 0 = from A; else compute below caller-provided T(start_level)
+  std::vector<int32_t> start_suffixes;  // their calls (m - start_level entries each)
+  int stop_level = 0;               // last level computed; its T goes to the caller's output buffer
   cudaStream_t copy_in = nullptr, copy_out = nullptr, copy_out2 = nullptr;
   cudaEvent_t out2_done = nullptr;
   std::vector<cudaEvent_t> chunk_ev;  // A chunk (first block index a) landed
@@ -305,14 +308,20 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
   std::vector<int> prev_call;        // their call index in the T(k+1) buffer
   int64_t prev_calls = 0;
   const bool has_top = !W.top_units.empty();
-  if (!has_top) {  // the top level was computed by an earlier wave
+  int k_first = has_top ? P.m - 1 : P.m - 2;
+  if (P.start_level > 0) {  // start below caller-provided temporaries T(start_level)
+    k_first = P.start_level - 1;
+    prev_suffix = P.start_suffixes;
+    prev_calls = (int64_t)(P.start_suffixes.size() / (P.m - P.start_level));
+    for (int64_t c = 0; c < prev_calls; ++c) prev_call.push_back((int)c);
+  } else if (!has_top) {  // the top level was computed by an earlier wave
     for (size_t i = 0; i < W.units.size(); ++i) {
       prev_suffix.push_back(W.units[i]);
       prev_call.push_back(W.top_call[i]);
     }
     prev_calls = (int64_t)W.units.size();
   }
-  for (int k = has_top ? P.m - 1 : P.m - 2; k >= 0; --k) {
+  for (int k = k_first; k >= P.stop_level; --k) {
     LevelHost L;
     L.k = k;
     L.keys_out = keys_at(P, k);
@@ -323,7 +332,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
     L.rest = L.bAk * ipow(P.bC, P.m - 1 - k);
     const int sl = P.m - k;  // suffix length of this level's calls
     std::vector<int4> parents;
-    if (k == P.m - 1) {
+    if (k == P.m - 1 && P.start_level == 0) {
       const std::vector<int>& tu = W.top_units;
       for (size_t i = 0; i < tu.size(); ++i) {
         L.suffixes.push_back(tu[i]);
@@ -392,7 +401,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
       L.flops += kv.second.flops;
       L.launches.push_back(std::move(kv.second));
     }
-    if (k == P.m - 1) {
+    if (k == P.m - 1 && P.start_level == 0) {
       prev_suffix.clear();
       for (int u : W.units) prev_suffix.push_back(u);
       prev_calls = (int64_t)W.units.size();
@@ -468,6 +477,29 @@ int build_plan(bcss_plan& P) {
           return fail(BCSS_ERR_NOMEM, "one top-level unit needs %zu workspace bytes > limit %zu",
                       peak_for(P, W.units), P.ws_limit);
     }
+    if (P.start_level > 0 || P.stop_level > 0) {
+      // partial runs (multi-GPU exchange points): one wave, regions from the built levels
+      P.waves.clear();
+      P.waves.push_back(WaveHost{units, {}, {}, {}, {}});
+      WaveHost& W = P.waves[0];
+      if (P.start_level == 0) {
+        W.top_units = units;
+        for (size_t i = 0; i < units.size(); ++i) W.top_call.push_back((int)i);
+      }
+      build_wave_levels(P, W);
+      auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+      size_t r[2] = {0, 0};
+      const int k_first = W.levels.empty() ? 0 : W.levels.front().k;
+      for (auto& L : W.levels)
+        if (L.k > P.stop_level && L.k >= 1)
+          r[(k_first - L.k) % 2] = std::max(r[(k_first - L.k) % 2],
+                                            al((size_t)L.n_calls * L.keys_out * L.blk_out * sizeof(double)));
+      W.level_off.assign(P.m + 1, 0);
+      for (auto& L : W.levels)
+        if (L.k > P.stop_level && L.k >= 1) W.level_off[L.k] = (k_first - L.k) % 2 == 0 ? 0 : r[0];
+      P.ws_bytes = r[0] + r[1];
+      P.top_first = false;
+    } else {
     // Top level: with a pipeline, the first wave computes T(m-1) for every
     // unit (it overlaps the chunked upload of A) and later waves only run the
     // levels below; otherwise every wave computes its own units' top level.
@@ -513,6 +545,7 @@ int build_plan(bcss_plan& P) {
       }
       P.ws_bytes = std::max(P.ws_bytes, end);
     }
+    }  // full run
     // tables
     P.nbr.assign(P.m, {});
     P.nbr_off.assign(P.m, 0);
@@ -524,8 +557,9 @@ int build_plan(bcss_plan& P) {
     }
     P.flops = 0;
     P.c_blocks = 0;
+    const bool partial = P.start_level > 0 || P.stop_level > 0;
     for (auto& W : P.waves) {
-      build_wave_levels(P, W);
+      if (!partial) build_wave_levels(P, W);
       for (auto& L : W.levels) {
         for (auto& X : L.launches) {
           X.off_parents = take(X.parents.size() * sizeof(int4));
@@ -796,8 +830,9 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   bcss::LevelArgs a;
   memset(&a, 0, sizeof(a));
   a.X = X_;
-  a.Tin = (L.k == P->m - 1) ? A : region_for(*P, W, L.k + 1);
-  a.Tout = (L.k == 0) ? C : region_for(*P, W, L.k);
+  const bool from_input = (P->start_level == 0 && L.k == P->m - 1) || (P->start_level > 0 && L.k == P->start_level - 1);
+  a.Tin = from_input ? A : region_for(*P, W, L.k + 1);
+  a.Tout = (L.k == P->stop_level) ? C : region_for(*P, W, L.k);
   a.parents = reinterpret_cast<const int4*>(tbl + X.off_parents);
   a.items = reinterpret_cast<const int4*>(tbl + X.off_items) + item_lo;
   a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
@@ -983,6 +1018,80 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
   return run_impl(P, A, X_, C, static_cast<cudaStream_t>(stream), nullptr);
 }
 
+int bcss_plan_set_stop_level(bcss_plan* P, int stop_level) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (stop_level < 0 || stop_level >= P->m) return fail(BCSS_ERR_RANGE, "stop level %d outside 0..%d", stop_level, P->m - 1);
+  P->stop_level = stop_level;
+  invalidate(P);
+  return BCSS_OK;
+}
+
+int bcss_plan_set_start_calls(bcss_plan* P, int level, const int32_t* suffixes, int n_calls) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (level == P->m || level == 0) {  // back to a full run from A
+    P->start_level = 0;
+    P->start_suffixes.clear();
+    invalidate(P);
+    return BCSS_OK;
+  }
+  if (level < 1 || level >= P->m) return fail(BCSS_ERR_RANGE, "start level %d outside 1..%d", level, P->m - 1);
+  if (n_calls < 0 || (n_calls > 0 && !suffixes)) return fail(BCSS_ERR_PARAMETER, "bad call list");
+  const int sl = P->m - level;
+  for (int c = 0; c < n_calls; ++c)
+    for (int q = 0; q < sl; ++q) {
+      const int32_t v = suffixes[c * sl + q];
+      if (v < 0 || v >= P->pbar) return fail(BCSS_ERR_RANGE, "suffix entry %d outside 0..%lld", v, (long long)P->pbar - 1);
+      if (q > 0 && v < suffixes[c * sl + q - 1]) return fail(BCSS_ERR_SHAPE, "suffix is not nondecreasing");
+    }
+  P->start_level = level;
+  P->start_suffixes.assign(suffixes, suffixes + (size_t)n_calls * sl);
+  invalidate(P);
+  return BCSS_OK;
+}
+
+int bcss_plan_level_calls(bcss_plan* P, int k, int32_t* out, int64_t n_max, int64_t* out_n) {
+  if (!P || !out_n) return fail(BCSS_ERR_STATE, "null argument");
+  int st = build_plan(*P);
+  if (st) return st;
+  const int sl = P->m - k;
+  int64_t cnt = 0;
+  for (auto& W : P->waves)
+    for (auto& L : W.levels)
+      if (L.k == k) {
+        for (int64_t c = 0; c < L.n_calls; ++c, ++cnt)
+          if (out && cnt < n_max)
+            for (int q = 0; q < sl; ++q) out[cnt * sl + q] = L.suffixes[(size_t)(c * sl + q)];
+      }
+  *out_n = cnt;
+  if (out && cnt > n_max) return fail(BCSS_ERR_RANGE, "output array too small");
+  return BCSS_OK;
+}
+
+int bcss_plan_io_elems(bcss_plan* P, int64_t* in_elems, int64_t* out_elems) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  int st = build_plan(*P);
+  if (st) return st;
+  if (in_elems) {
+    if (P->start_level > 0)
+      *in_elems = (int64_t)(P->start_suffixes.size() / (P->m - P->start_level)) * keys_at(*P, P->start_level) *
+                  blk_at(*P, P->start_level);
+    else
+      *in_elems = bcss::simplex_count(P->nbar, P->m) * ipow(P->bA, P->m);
+  }
+  if (out_elems) {
+    if (P->stop_level > 0) {
+      int64_t calls = 0;
+      for (auto& W : P->waves)
+        for (auto& L : W.levels)
+          if (L.k == P->stop_level) calls += L.n_calls;
+      *out_elems = calls * keys_at(*P, P->stop_level) * blk_at(*P, P->stop_level);
+    } else {
+      *out_elems = bcss::simplex_count(P->pbar, P->m) * ipow(P->bC, P->m);
+    }
+  }
+  return BCSS_OK;
+}
+
 int bcss_plan_set_pipeline(bcss_plan* P, int waves) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
   if (waves < 0) return fail(BCSS_ERR_PARAMETER, "negative wave count");
@@ -1011,7 +1120,8 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
   if ((st = grow(P->hX, P->hX_bytes, x_bytes))) return st;
   if ((st = grow(P->hC, P->hC_bytes, c_bytes))) return st;
   if (!P->host_stream) CUDA_TRY(cudaStreamCreateWithFlags(&P->host_stream, cudaStreamNonBlocking));
-  const bool pipelined = P->pipeline_waves > 0 && !P->units_set && !P->keep_temps && is_pinned(A) &&
+  const bool pipelined = P->pipeline_waves > 0 && !P->units_set && !P->keep_temps && P->start_level == 0 &&
+                         P->stop_level == 0 && is_pinned(A) &&
                          is_pinned(X) && is_pinned(C);
   if (!pipelined) {
     CUDA_TRY(cudaMemcpyAsync(P->hA, A, a_bytes, cudaMemcpyHostToDevice, P->host_stream));

@@ -9,7 +9,16 @@ blocks with no data-path collective.  The exchanges are input distribution
 wants C on one rank, the gather of the disjoint blocks (``gather_c``).
 
 Subtree costs grow with j, so units are assigned longest-processing-time
-first (LPT) on their exact flop counts (scheme S1).
+first (LPT) on their exact flop counts (scheme S1): no exchange
+at all, but the largest subtree bounds the balance (config 5 at 8 GPUs: 0.66).
+
+``s5_schedule`` / ``sttsm_bcss_s5`` implement SURVEY §8e scheme S5: the owner
+of top-level unit u computes T(m-1)[u] and the level-(m-2) calls (i, u)
+(stop-level partial plan); every level-(m-2) call is then a subtree unit,
+LPT-assigned over ranks on top of the owners' loads, and its T(m-2) (e.g.
+1.14 GB for config 5) moves owner -> assignee by NCCL point-to-point before
+the assignee runs the levels below (start-call partial plan).  Modelled
+balance: 1.0 / 1.0 / 0.997 / 0.898 for configs 2-5 at 8 GPUs.
 """
 
 from __future__ import annotations
@@ -109,4 +118,154 @@ def sttsm_bcss_distributed(a, x, m: int, b_a: int, b_c: int, reuse: bool = True,
     if dst is None:
         return c
     all_ranks = [pl.c_block_ranks() for pl in plans]
+    return gather_c(c, all_ranks[rank], all_ranks, b_c**m, dst=dst, group=group)
+
+
+def s5_schedule(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: bool = True):
+    """(owners, subs): owners[r] = top-level units rank r computes down to level
+    m-2; subs[r] = level-(m-2) calls (i, u) whose subtrees rank r computes.
+    Deterministic, so every rank derives the same schedule without talking."""
+    pbar = p // b_c
+    if m < 3:  # no level below m-2 to hand out: plain S1
+        parts = partition_units(unit_flops(m, n, p, b_a, b_c, reuse), world)
+        return parts, [[] for _ in range(world)]
+    owner_cost = []
+    for u in range(pbar):
+        pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=[u], stop_level=m - 2)
+        owner_cost.append(pl.stats()["flops"])
+        pl.close()
+    loads = [0] * world
+    owners: list[list[int]] = [[] for _ in range(world)]
+    for u in sorted(range(pbar), key=lambda q: (-owner_cost[q], q)):
+        r = min(range(world), key=lambda q: (loads[q], q))
+        owners[r].append(u)
+        loads[r] += owner_cost[u]
+    calls = [(i, u) for u in range(pbar) for i in range(u + 1)]
+    # subtree cost depends only on i (the row block) for fixed shapes
+    sub_cost = {}
+    for i in range(pbar):
+        pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=[(i, pbar - 1)])
+        sub_cost[i] = pl.stats()["flops"]
+        pl.close()
+    subs: list[list[tuple]] = [[] for _ in range(world)]
+    for c in sorted(calls, key=lambda q: (-sub_cost[q[0]], q)):
+        r = min(range(world), key=lambda q: (loads[q], q))
+        subs[r].append(c)
+        loads[r] += sub_cost[c[0]]
+    return [sorted(o) for o in owners], [sorted(sb) for sb in subs]
+
+
+def _gpu_compute(plan: SttsmPlan, inp, x, out) -> None:
+    plan.run(inp, x, out)
+
+
+class S5Runner:
+    """One rank's share of the scheme-S5 schedule, with its plans, buffers and
+    exchange list built once; ``run`` executes one full step (phase 1,
+    T(m-2) exchange, phase 2) asynchronously on the current stream / NCCL."""
+
+    def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, rank: int, world: int, device,
+                 reuse: bool = True, group=None, compute=_gpu_compute):
+        import torch
+
+        self.m, self.rank, self.world, self.group, self.compute = m, rank, world, group, compute
+        owners, subs = s5_schedule(m, n, p, b_a, b_c, world, reuse)
+        self.owners, self.subs = owners, subs
+        owner_of = {u: r for r in range(world) for u in owners[r]}
+        self.plan_o = (SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=owners[rank], stop_level=m - 2)
+                       if owners[rank] else None)
+        self.plan_s = (SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=subs[rank])
+                       if subs[rank] else None)
+        probe = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=[(0, 0)])
+        self.slice = probe.a_elems
+        probe.close()
+        # call order of every owner's T(m-2) buffer (deterministic, no communication)
+        order = {}
+        for r in range(world):
+            if owners[r]:
+                pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=owners[r], stop_level=m - 2)
+                order[r] = {c: i for i, c in enumerate(pl.level_calls(m - 2))}
+                pl.close()
+        self.t2 = (torch.empty(self.plan_o.c_elems, dtype=torch.float64, device=device)
+                   if self.plan_o else None)
+        self.inp = torch.empty(max(1, len(subs[rank])) * self.slice, dtype=torch.float64, device=device)
+        self.local, self.sends, self.recvs = [], [], []  # (dst slot, src slot) / (peer, slot)
+        for r in range(world):
+            for j, c in enumerate(subs[r]):
+                q = owner_of[c[1]]
+                if q == rank and r == rank:
+                    self.local.append((j, order[q][c]))
+                elif q == rank:
+                    self.sends.append((r, order[q][c]))
+                elif r == rank:
+                    self.recvs.append((q, j))
+        self.exchange_bytes = 8 * self.slice * (len(self.sends) + len(self.recvs))
+        full = SttsmPlan(m, n, p, b_a, b_c)
+        self.c_elems = full.c_elems
+        full.close()
+
+    def plans(self):
+        return [pl for pl in (self.plan_o, self.plan_s) if pl is not None]
+
+    def attach_torch_workspace(self, device=None) -> None:
+        for pl in self.plans():
+            pl.attach_torch_workspace(device)
+
+    def run(self, a, x, c) -> None:
+        import torch.distributed as dist
+
+        s = self.slice
+        if self.plan_o is not None:
+            self.compute(self.plan_o, a, x, self.t2)
+        for j, i in self.local:
+            self.inp[j * s:(j + 1) * s].copy_(self.t2[i * s:(i + 1) * s])
+        ops = [dist.P2POp(dist.isend, self.t2[i * s:(i + 1) * s], r, group=self.group) for r, i in self.sends]
+        ops += [dist.P2POp(dist.irecv, self.inp[j * s:(j + 1) * s], q, group=self.group) for q, j in self.recvs]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        if self.plan_s is not None:
+            self.compute(self.plan_s, self.inp, x, c)
+
+    def c_block_ranks(self) -> np.ndarray:
+        return self.plan_s.c_block_ranks() if self.plan_s is not None else np.zeros(0, dtype=np.int64)
+
+    @property
+    def flops(self) -> int:
+        return sum(pl.stats()["flops"] for pl in self.plans())
+
+
+def sttsm_bcss_s5(a, x, m: int, b_a: int, b_c: int, reuse: bool = True, dst: int | None = 0,
+                  group=None, compute=_gpu_compute):
+    """Scheme-S5 sharded sttsm (one rank per GPU).
+
+    Phase 1: owned units down to level m-2 (T(m-2) of their calls into a
+    local buffer).  Exchange: each level-(m-2) call's T(m-2) goes from its
+    owner to the rank its subtree was assigned to (NCCL send/recv; local
+    copies for self).  Phase 2: the assigned subtrees down to C.  With ``dst``
+    set, C is gathered there.  ``compute(plan, inp, x, out)`` runs a plan
+    (tests substitute a CPU stand-in).
+    """
+    import torch
+    import torch.distributed as dist
+
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    p, n = x.shape
+    if m < 3:
+        return sttsm_bcss_distributed(a, x, m, b_a, b_c, reuse=reuse, dst=dst, group=group)
+    runner = S5Runner(m, n, p, b_a, b_c, rank, world, x.device, reuse=reuse, group=group, compute=compute)
+    c = torch.zeros(runner.c_elems, dtype=x.dtype, device=x.device)
+    runner.run(a, x, c)
+    if dst is None:
+        return c
+    all_ranks = []
+    for r in range(world):
+        sb = runner.subs[r]
+        if sb:
+            pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=sb)
+            all_ranks.append(pl.c_block_ranks())
+            pl.close()
+        else:
+            all_ranks.append(np.zeros(0, dtype=np.int64))
     return gather_c(c, all_ranks[rank], all_ranks, b_c**m, dst=dst, group=group)

@@ -40,7 +40,8 @@ class SttsmPlan:
     """
 
     def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, reuse: bool = True,
-                 units=None, workspace_limit: int = 0, keep_temps: bool = False, pipeline: int = 0):
+                 units=None, workspace_limit: int = 0, keep_temps: bool = False, pipeline: int = 0,
+                 stop_level: int = 0, start_level: int | None = None, start_calls=None):
         lib = _native.lib()
         self.m, self.n, self.p, self.b_a, self.b_c, self.reuse = m, n, p, b_a, b_c, bool(reuse)
         h = ctypes.c_void_p()
@@ -57,9 +58,22 @@ class SttsmPlan:
         if pipeline:
             # run_host overlaps A upload / compute / C download over `pipeline` waves
             _native.check(lib.bcss_plan_set_pipeline(h, int(pipeline)))
+        if stop_level:
+            # partial run: stop after level `stop_level`, its T goes to the output buffer
+            _native.check(lib.bcss_plan_set_stop_level(h, int(stop_level)))
+        if start_level is not None and start_level < m:
+            # partial run: start below the given calls of level `start_level`
+            flat = [int(v) for call in start_calls for v in call]
+            arr = (ctypes.c_int32 * max(1, len(flat)))(*flat)
+            _native.check(lib.bcss_plan_set_start_calls(h, int(start_level), arr, len(start_calls)))
         self.units = None if units is None else sorted(set(int(u) for u in units))
-        self.a_elems = simplex_count(n // b_a, m) * b_a**m
-        self.c_elems = simplex_count(p // b_c, m) * b_c**m
+        self.stop_level = int(stop_level)
+        self.start_level = start_level if (start_level is not None and start_level < m) else None
+        self.start_calls = [tuple(c) for c in start_calls] if self.start_level is not None else None
+        ie, oe = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(lib.bcss_plan_io_elems(h, ctypes.byref(ie), ctypes.byref(oe)))
+        self.a_elems = int(ie.value)   # input buffer: A, or start-level temporaries
+        self.c_elems = int(oe.value)   # output buffer: C, or stop-level temporaries
 
     # ---- lifecycle ------------------------------------------------------------
     def close(self) -> None:
@@ -103,6 +117,16 @@ class SttsmPlan:
         _native.check(lib.bcss_plan_c_block_ranks(
             self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n.value, ctypes.byref(n)))
         return out
+
+    def level_calls(self, k: int) -> list[tuple[int, ...]]:
+        """Suffixes of the plan's level-k calls in buffer order."""
+        n = ctypes.c_int64()
+        lib = _native.lib()
+        _native.check(lib.bcss_plan_level_calls(self._h, k, None, 0, ctypes.byref(n)))
+        sl = self.m - k
+        out = (ctypes.c_int32 * max(1, n.value * sl))()
+        _native.check(lib.bcss_plan_level_calls(self._h, k, out, n.value, ctypes.byref(n)))
+        return [tuple(out[i * sl:(i + 1) * sl]) for i in range(n.value)]
 
     def set_timing(self, on: bool = True) -> None:
         _native.check(_native.lib().bcss_plan_set_timing(self._h, int(on)))

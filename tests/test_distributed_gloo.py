@@ -65,3 +65,59 @@ def test_lpt_partition_balances_config5():
         assert max(loads) >= sum(costs) / world
         if world == 2:
             assert max(loads) / (sum(costs) / world) < 1.05
+
+
+def _oracle_compute(d, m, n, p, ba, bc):
+    """CPU stand-in for SttsmPlan.run on the S5 partial plans (the oracle
+    computes the same temporaries / C blocks the GPU kernels would)."""
+    def compute(plan, inp, x, out):
+        if plan.stop_level:
+            _, temps = orc.sttsm_bcss_packed(d["A"], d["X"], m, n, ba, bc, keep_temps=True, units=plan.units)
+            k = plan.stop_level
+            flat = np.concatenate([orc.pack_temp(temps[(k, c)], k, n // ba) for c in plan.level_calls(k)])
+            out.copy_(torch.from_numpy(flat))
+        else:
+            size = inp.numel() // len(plan.start_calls)
+            given = {c: inp[i * size:(i + 1) * size].numpy() for i, c in enumerate(plan.start_calls)}
+            out.copy_(torch.from_numpy(orc.sttsm_bcss_packed(None, d["X"], m, n, ba, bc,
+                                                             start=(plan.start_level, given))))
+    return compute
+
+
+def _worker_s5(rank, world, port, case, q):
+    from paper_1301_7744_b200.distributed import sttsm_bcss_s5
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    d = np.load(GOLDEN / f"sttsm_{case}.npz")
+    m, n, p, ba, bc = (int(v) for v in d["dims"])
+    out = sttsm_bcss_s5(torch.from_numpy(d["A"]), torch.from_numpy(d["X"]), m, ba, bc, dst=0,
+                        compute=_oracle_compute(d, m, n, p, ba, bc))
+    if rank == 0:
+        q.put(orc.rel_frobenius(out.numpy(), d["C"]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("case,world", [("rbcss_m4_n12_b4", 2), ("small_m5_n8_p8_ba4_bc4", 3),
+                                        ("config1", 2)])
+def test_s5_exchange_schedule_reproduces_c(case, world):
+    """Owners compute down to T(m-2), slices move owner -> assignee over
+    point-to-point sends, assignees finish the subtrees; rank 0 gathers C."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_s5, args=(r, world, port, case, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    for pr in procs:
+        pr.join(180)
+        assert pr.exitcode == 0
+    assert q.get(timeout=10) <= 1e-15
+
+
+def test_s5_schedule_balance_and_coverage():
+    from paper_1301_7744_b200.distributed import s5_schedule
+    cfg = (4, 512, 256, 32, 32)
+    owners, subs = s5_schedule(*cfg, 8)
+    assert sorted(u for o in owners for u in o) == list(range(8))
+    assert sorted(c for s in subs for c in s) == sorted((i, u) for u in range(8) for i in range(u + 1))

@@ -169,3 +169,42 @@ def test_pipelined_host_run_is_bitwise_identical(cfg_id, waves):
     c_h.fill_(float("nan"))
     plan.run_host(a_h.numpy(), x_h.numpy(), c_h.numpy())  # reuse of streams / events
     assert torch.equal(c_h, want)
+
+
+@pytest.mark.parametrize("cfg_id,world", [(2, 4), (3, 4), (4, 8), (5, 8)])
+def test_s5_partial_plans_reassemble_c_bitwise(cfg_id, world):
+    """The S5 multi-GPU schedule on one GPU: every virtual rank's owner plan
+    (levels m-1..m-2, stop-level output) and subtree plan (start calls from the
+    exchanged T(m-2) slices) run in turn; the union of their C blocks equals
+    the single-plan result bit for bit."""
+    from paper_1301_7744_b200.distributed import s5_schedule
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 61 + cfg_id)
+    x = random_matrix_device(p, n, 62 + cfg_id)
+    want = run(CFG[cfg_id], a, x)
+    owners, subs = s5_schedule(m, n, p, ba, bc, world)
+    slices = {}
+    for r in range(world):
+        if not owners[r]:
+            continue
+        pl = bs.SttsmPlan(m, n, p, ba, bc, units=owners[r], stop_level=m - 2)
+        t2 = torch.empty(pl.c_elems, dtype=torch.float64, device="cuda")
+        pl.run(a, x, t2)
+        calls = pl.level_calls(m - 2)
+        size = t2.numel() // len(calls)
+        for i, c in enumerate(calls):
+            slices[c] = t2[i * size:(i + 1) * size]
+        pl.close()
+    c = torch.full_like(want, float("nan"))
+    for r in range(world):
+        if not subs[r]:
+            continue
+        inp = torch.cat([slices[cl] for cl in subs[r]])
+        pl = bs.SttsmPlan(m, n, p, ba, bc, start_level=m - 2, start_calls=subs[r])
+        part = torch.full_like(want, float("nan"))
+        pl.run(inp, x, part)
+        idx = torch.as_tensor(pl.c_block_ranks(), device="cuda")
+        c.view(-1, bc**m)[idx] = part.view(-1, bc**m)[idx]
+        pl.close()
+    torch.cuda.synchronize()
+    assert torch.equal(c, want)
