@@ -189,6 +189,35 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def run_dense(args, A, X, m, n, p, ba, rank, world, dev, job_ms):
+    """Dense mode-product baseline (cuBLAS) on the same inputs, when it fits."""
+    import torch
+
+    from paper_1301_7744_b200 import dense as dn
+
+    if rank != 0 or world != 1:
+        return None
+    need = 3 * max(n, p) ** m * 8
+    free, _ = torch.cuda.mem_get_info(dev)
+    if need >= 0.8 * free:
+        return {"skipped": f"dense A needs ~{need / 1e9:.0f} GB"}
+    a_dense = dn.bcss_to_dense_device(A, m, n, ba)
+    for _ in range(2):
+        dn.sttsm_dense_ttm_device(a_dense, X)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(args.steps):
+        dn.sttsm_dense_ttm_device(a_dense, X)
+    s1.record()
+    s1.synchronize()
+    dms = s0.elapsed_time(s1) / args.steps
+    dfl = dn.dense_flops(m, n, p)
+    return {"ms_per_step": round(dms, 4), "flops_per_step": dfl, "tflops": round(dfl / dms / 1e9, 3),
+            "speedup_bcss_vs_dense": round(dms / (job_ms / args.steps), 3),
+            "impl": "dense mode-product chain, cuBLAS DGEMM via torch.tensordot"}
+
+
 def run_ours(args) -> None:
     import numpy as np
     import torch
@@ -288,11 +317,22 @@ def run_ours(args) -> None:
     for pl in plans:
         pl.set_timing(False)
 
+    dense_line = run_dense(args, A, X, m, n, p, ba, rank, world, dev, job_ms) if args.dense else None
+    a_np_cpu = x_np_cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        a_np_cpu, x_np_cpu = A.cpu().numpy(), X.cpu().numpy()
+
     # end to end through the public host-buffer API (pinned host memory)
     e2e = None
     if not args.no_e2e:
         a_h = A.cpu().pin_memory()
         x_h = X.cpu().pin_memory()
+        if runner is None and world == 1 and args.pipeline:
+            # the host path owns its device buffers: release the device-resident run's
+            del A, X, C
+            for pl in plans:
+                pl.close()
+            torch.cuda.empty_cache()
         c_h = torch.empty(c_elems, dtype=torch.float64).pin_memory()
         a_np, x_np, c_np = a_h.numpy(), x_h.numpy(), c_h.numpy()
         if runner is not None:
@@ -332,37 +372,9 @@ def run_ours(args) -> None:
             plan_e2e.close()
         del a_h, x_h, c_h
 
-    dense_line = None
-    if args.dense and rank == 0 and world == 1:
-        from paper_1301_7744_b200 import dense as dn
-        need = 3 * max(n, p) ** m * 8
-        free, _ = torch.cuda.mem_get_info(dev)
-        if need < 0.8 * free:
-            a_dense = dn.bcss_to_dense_device(A, m, n, ba)
-            for _ in range(2):
-                dn.sttsm_dense_ttm_device(a_dense, X)
-            torch.cuda.synchronize()
-            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            s0.record()
-            for _ in range(args.steps):
-                dn.sttsm_dense_ttm_device(a_dense, X)
-            s1.record()
-            s1.synchronize()
-            dms = s0.elapsed_time(s1) / args.steps
-            dfl = dn.dense_flops(m, n, p)
-            dense_line = {"ms_per_step": round(dms, 4), "flops_per_step": dfl,
-                          "tflops": round(dfl / dms / 1e9, 3),
-                          "speedup_bcss_vs_dense": round(dms / (job_ms / args.steps), 3),
-                          "impl": "dense mode-product chain, cuBLAS DGEMM via torch.tensordot"}
-            del a_dense
-        else:
-            dense_line = {"skipped": f"dense A needs ~{need / 1e9:.0f} GB"}
-
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        a_np = A.cpu().numpy()
-        x_np = X.cpu().numpy()
-        rate, desc, dt = cpu_sample(a_np, x_np, m, n, p, ba, bc, args.cpu_budget_s)
+    if a_np_cpu is not None:
+        rate, desc, dt = cpu_sample(a_np_cpu, x_np_cpu, m, n, p, ba, bc, args.cpu_budget_s)
         cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
                "sample": desc, "seconds": round(dt, 2)}
 
