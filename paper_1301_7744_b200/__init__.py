@@ -24,6 +24,7 @@ from .storage import BcssTensor, PartialSymTensor, packed_payload
 from .sttsm import (
     DenseBlockTable,
     SttsmPlan,
+    clear_plan_cache,
     probe_fp64_peak,
     sttsm_bcss,
     sttsm_bcss_device,

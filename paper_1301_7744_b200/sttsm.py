@@ -16,6 +16,8 @@ benchmark, the multi-GPU layer and anyone who keeps A resident in HBM.
 from __future__ import annotations
 
 import ctypes
+import threading
+from collections import OrderedDict
 from typing import Callable
 
 import numpy as np
@@ -267,17 +269,54 @@ def sttsm_bcss(a, x, b_c: int, counter: OpCounter | None = None, reuse: bool = T
     a_payload = np.ascontiguousarray(packed_payload(a), dtype=np.float64)
     xc = np.ascontiguousarray(x)
     c_payload = np.empty(simplex_count(p // b_c, m) * b_c**m, dtype=np.float64)
-    plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, keep_temps=temp_hook is not None)
-    try:
-        plan.run_host(a_payload, xc, c_payload)
-        if temp_hook is not None:
+    if temp_hook is not None:
+        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, keep_temps=True)
+        try:
+            plan.run_host(a_payload, xc, c_payload)
             _replay_temps(plan, temp_hook)
-    finally:
-        plan.close()
+        finally:
+            plan.close()
+    else:
+        with _PLAN_CACHE_LOCK:
+            plan = _cached_plan(m, n, p, b_a, b_c, reuse)
+            plan.run_host(a_payload, xc, c_payload)
     if counter is not None:
         counter.count_flops(bcss_flops(m, n, p, b_a, b_c, reuse))
         counter.count_memops(bcss_memops(m, n, p, b_a, b_c, reuse))
     return BcssTensor(m, p, b_c, payload=c_payload)
+
+
+# Plans (tables + device workspace + transfer buffers) are reused across
+# drop-in calls with the same problem shape, so repeated sttsm_bcss calls do
+# not pay plan construction and cudaMalloc each time.  Small LRU; plans are
+# not shared across threads (the lock serializes drop-in calls).
+_PLAN_CACHE: "OrderedDict[tuple, SttsmPlan]" = None  # type: ignore[assignment]
+_PLAN_CACHE_SIZE = 4
+_PLAN_CACHE_LOCK = threading.Lock()
+
+
+def _cached_plan(m, n, p, b_a, b_c, reuse) -> SttsmPlan:
+    global _PLAN_CACHE
+    if _PLAN_CACHE is None:
+        _PLAN_CACHE = OrderedDict()
+    key = (m, n, p, b_a, b_c, bool(reuse))
+    plan = _PLAN_CACHE.pop(key, None)
+    if plan is None:
+        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse)
+    _PLAN_CACHE[key] = plan
+    while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
+        _, old = _PLAN_CACHE.popitem(last=False)
+        old.close()
+    return plan
+
+
+def clear_plan_cache() -> None:
+    """Release the drop-in's cached plans (device workspace and buffers)."""
+    with _PLAN_CACHE_LOCK:
+        if _PLAN_CACHE:
+            for pl in _PLAN_CACHE.values():
+                pl.close()
+            _PLAN_CACHE.clear()
 
 
 def _replay_temps(plan: SttsmPlan, hook: TempHook) -> None:
