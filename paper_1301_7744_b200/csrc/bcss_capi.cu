@@ -84,10 +84,10 @@ struct ShapePolicy {
   // b_a in {4, 8, 16, 32} on B200 (tools/calibrate_shapes.py: top level of configs 2/3/4, padding
   // corrected); b_a = 4 borrows the b_a = 8 row.
   double eff[4][N_SHAPES] = {
-      {32.41, 29.79, 29.22, 31.77, 31.21, 28.96, 19.84, 31.05},
-      {32.41, 29.79, 29.22, 31.77, 31.21, 28.96, 19.84, 31.05},
-      {32.87, 31.52, 30.56, 32.53, 31.61, 30.48, 23.08, 31.46},
-      {33.01, 32.24, 31.73, 32.62, 32.04, 30.96, 21.68, 32.01},
+      {32.52, 29.87, 29.28, 31.85, 31.28, 28.90, 19.83, 31.09, 31.91, 29.94},
+      {32.52, 29.87, 29.28, 31.85, 31.28, 28.90, 19.83, 31.09, 31.91, 29.94},
+      {32.80, 31.61, 30.58, 32.51, 31.64, 30.48, 23.06, 31.47, 32.96, 31.15},
+      {33.11, 32.26, 31.74, 32.62, 32.04, 30.95, 21.70, 31.99, 33.08, 31.32},
   };
   int force = -1;
   ShapePolicy() {
@@ -122,6 +122,40 @@ struct ShapePolicy {
       if (t < bt - 1e-9) { bt = t; best = sidx; }
     }
     return best;
+  }
+  // Row decomposition of a parent with `rows` rows into contiguous pieces, one
+  // tile shape each (largest tiles first), minimizing padded rows / throughput
+  // (knapsack over row counts): e.g. 160 rows -> 128 + 32.
+  std::vector<std::pair<int, int>> split(int rows, int64_t bA) const {
+    if (force >= 0 && force < N_SHAPES) return {{force, rows}};
+    const int bi = bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3;
+    std::vector<double> cost(rows + 1, 1e300);
+    std::vector<int> choice(rows + 1, -1);
+    cost[0] = 0;
+    for (int r = 1; r <= rows; ++r)
+      for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
+        if (eff[bi][sidx] <= 0) continue;
+        const int bm = shape_bm(sidx);
+        const double c = cost[std::max(0, r - bm)] + bm / eff[bi][sidx];
+        if (c < cost[r] - 1e-12) { cost[r] = c; choice[r] = sidx; }
+      }
+    std::map<int, int, std::greater<int>> tiles_by_bm;  // bm -> (shape, count) via two maps
+    std::map<int, int> shape_of_bm, count_of_bm;
+    for (int r = rows; r > 0;) {
+      const int sidx = choice[r];
+      const int bm = shape_bm(sidx);
+      shape_of_bm[bm] = sidx;
+      count_of_bm[bm] += 1;
+      r = std::max(0, r - bm);
+    }
+    std::vector<std::pair<int, int>> out;
+    int left = rows;
+    for (auto it = count_of_bm.rbegin(); it != count_of_bm.rend(); ++it) {
+      const int take = std::min(left, it->first * it->second);
+      if (take > 0) out.push_back({shape_of_bm[it->first], take});
+      left -= take;
+    }
+    return out;
   }
 };
 
@@ -372,19 +406,33 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
     }
     // group parents into launches by tile configuration
     std::map<int, LaunchHost> by_cfg;
-    for (const int4& par : parents) {
-      const int cfg = fast ? fast_cfg(P.bA, policy.pick(par.z, P.bA)) : CFG_GENERIC;
-      LaunchHost& X = by_cfg[cfg];
-      const KernelCfg& C = kernel_cfg(cfg);
-      if (X.parents.empty()) {
-        X.cfg = cfg;
-        X.n_tiles = (int)((L.rest + C.BN - 1) / C.BN);
-        X.item_off.push_back(0);
+    for (const int4& whole : parents) {
+      // a parent's rows may be split into pieces of different tile shapes; a
+      // piece is a parent with a later row0 (its child index follows from
+      // child_off + (jb - row0/b_c) in the epilogue)
+      std::vector<std::pair<int, int>> pieces;
+      if (fast) pieces = policy.split(whole.z, P.bA);
+      else pieces = {{-1, whole.z}};
+      int r0 = 0;
+      for (const auto& pc : pieces) {
+        const int cfg = fast ? fast_cfg(P.bA, pc.first) : CFG_GENERIC;
+        int4 par = whole;
+        par.y = whole.y + r0;
+        par.z = pc.second;
+        par.w = whole.w + r0 / (int)P.bC;
+        r0 += pc.second;
+        LaunchHost& X = by_cfg[cfg];
+        const KernelCfg& C = kernel_cfg(cfg);
+        if (X.parents.empty()) {
+          X.cfg = cfg;
+          X.n_tiles = (int)((L.rest + C.BN - 1) / C.BN);
+          X.item_off.push_back(0);
+        }
+        X.parents.push_back(par);
+        X.item_off.push_back(X.item_off.back() +
+                             (long long)L.keys_out * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
+        X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
       }
-      X.parents.push_back(par);
-      X.item_off.push_back(X.item_off.back() +
-                           (long long)L.keys_out * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
-      X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
     }
     for (auto& kv : by_cfg) {
       // flat work list: parent-major, then key, n-tile, m-tile (adjacent CTAs

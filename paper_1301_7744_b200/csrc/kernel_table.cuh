@@ -34,9 +34,11 @@ KernelCfg make_cfg(const char* name) {
   X((WsLevelKernel<64, 256, 16, 2, 8, 4, BA>), "ws64x256c16")     \
   X((WsLevelKernel<32, 256, 32, 1, 16, 3, BA>), "ws32x256c16")     \
   X((WsLevelKernel<16, 512, 16, 1, 16, 3, BA>), "ws16x512c16k16") \
-  X((WsLevelKernel<64, 256, 16, 2, 8, 5, BA>), "ws64x256c16k16s5")
+  X((WsLevelKernel<64, 256, 16, 2, 8, 5, BA>), "ws64x256c16k16s5") \
+  X((WsLevelKernel<96, 128, 32, 3, 4, 3, BA>), "ws96x128c12")      \
+  X((WsLevelKernel<48, 256, 16, 3, 4, 4, BA>), "ws48x256c12k16")
 
-constexpr int N_SHAPES = 8;
+constexpr int N_SHAPES = 10;
 
 extern const KernelCfg kFast4[N_SHAPES];
 extern const KernelCfg kFast8[N_SHAPES];

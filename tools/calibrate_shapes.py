@@ -7,7 +7,7 @@ import os
 import subprocess
 import sys
 
-SHAPES_BM = [128, 64, 32, 128, 64, 32, 16, 64]
+SHAPES_BM = [128, 64, 32, 128, 64, 32, 16, 64, 96, 48]
 CASES = {32: (2, 512), 16: (3, 192), 8: (4, 96)}  # b_a -> (config, rows at top level)
 out = {}
 for shape, bm in enumerate(SHAPES_BM):
