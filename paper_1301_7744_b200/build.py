@@ -22,9 +22,11 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xptxas", "-v",
           "-I", str(ROOT / "include")]
 UNITS = [("bcss_capi", CSRC / "bcss_capi.cu", []),
+         ("plan", CSRC / "plan.cu", []),
+         ("run", CSRC / "run.cu", []),
          ("kernels_generic", CSRC / "kernels_generic.cu", [])] + [
     (f"kernels_fast_ba{ba}", CSRC / "kernels_fast.cu", [f"-DBCSS_BA={ba}"]) for ba in (4, 8, 16, 32)]
-HEADERS = [CSRC / "sttsm_kernels.cuh", CSRC / "sttsm_ws_kernel.cuh", CSRC / "kernel_table.cuh", CSRC / "combinatorics.hpp",
+HEADERS = [CSRC / "plan.hpp", CSRC / "sttsm_kernels.cuh", CSRC / "sttsm_ws_kernel.cuh", CSRC / "kernel_table.cuh", CSRC / "combinatorics.hpp",
            ROOT / "include" / "bcss_sttsm.h"]
 
 

@@ -1,0 +1,567 @@
+// Plan construction: neighbour tables, waves, levels, per-shape launches and
+// workspace layout; device tables and workspace (declared in plan.hpp).
+// Replaces the reference's depth-first `descend` (change_of_basis.py:269-283)
+// by breadth-first levels over waves of top-level units.
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+
+#include "plan.hpp"
+
+namespace bcss_host {
+
+thread_local std::string g_last_error;
+
+// ---- kernel configurations ----------------------------------------------------
+
+// The fast tile shapes' BM (bcss::BCSS_FAST_SHAPES order).
+int shape_bm(int shape) { return bcss::kFast32[shape].BM; }
+
+const KernelCfg& kernel_cfg(int cfg) {
+  if (cfg == 0) return bcss::kGeneric;
+  const int shape = (cfg - 1) / 4, ba = (cfg - 1) % 4;
+  const KernelCfg* t = ba == 0 ? bcss::kFast4 : ba == 1 ? bcss::kFast8 : ba == 2 ? bcss::kFast16 : bcss::kFast32;
+  return t[shape];
+}
+// fast configuration of tile shape `shape` for power-of-two b_a in {4, 8, 16, 32}, else -1
+int fast_cfg(int64_t bA, int shape) {
+  int i;
+  switch (bA) {
+    case 4: i = 0; break;
+    case 8: i = 1; break;
+    case 16: i = 2; break;
+    case 32: i = 3; break;
+    default: return -1;
+  }
+  return 1 + shape * 4 + i;
+}
+
+// Relative DMMA efficiency of each tile shape (larger tiles reuse operands
+// more); the plan picks, per parent, the shape minimizing padded work / eff.
+// BCSS_SHAPE_EFF="e128,e64,e32" overrides, BCSS_FORCE_SHAPE=i forces one.
+struct ShapePolicy {
+  // Measured full-tile FP64 TFLOP/s of each shape (BCSS_FAST_SHAPES order) per
+  // b_a in {4, 8, 16, 32} on B200 (tools/calibrate_shapes.py: top level of configs 2/3/4, padding
+  // corrected); b_a = 4 borrows the b_a = 8 row.
+  double eff[4][N_SHAPES] = {
+      {32.52, 29.87, 29.28, 31.85, 31.28, 28.90, 19.83, 31.09, 31.91, 29.94},
+      {32.52, 29.87, 29.28, 31.85, 31.28, 28.90, 19.83, 31.09, 31.91, 29.94},
+      {32.80, 31.61, 30.58, 32.51, 31.64, 30.48, 23.06, 31.47, 32.96, 31.15},
+      {33.11, 32.26, 31.74, 32.62, 32.04, 30.95, 21.70, 31.99, 33.08, 31.32},
+  };
+  int force = -1;
+  ShapePolicy() {
+    // BCSS_SHAPE_EFF="e0,e1,...,e5" overrides every b_a's row; BCSS_FORCE_SHAPE=i forces one
+    if (const char* e = getenv("BCSS_SHAPE_EFF")) {
+      double v[N_SHAPES];
+      int got = 0;
+      const char* q = e;
+      while (got < N_SHAPES) {
+        int used = 0;
+        if (sscanf(q, "%lf%n", &v[got], &used) != 1) break;
+        ++got;
+        q += used;
+        if (*q == ',') ++q;
+      }
+      if (got == N_SHAPES)
+        for (auto& row : eff)
+          for (int i = 0; i < N_SHAPES; ++i) row[i] = v[i];
+    }
+    if (const char* f = getenv("BCSS_FORCE_SHAPE")) force = atoi(f);
+  }
+  // shape minimizing padded rows / throughput for a parent with `rows` rows
+  int pick(int rows, int64_t bA) const {
+    if (force >= 0 && force < N_SHAPES) return force;
+    const int bi = bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3;
+    int best = 0;
+    double bt = 1e300;
+    for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
+      if (eff[bi][sidx] <= 0) continue;
+      const int bm = shape_bm(sidx);
+      const double t = (double)((rows + bm - 1) / bm * bm) / eff[bi][sidx];
+      if (t < bt - 1e-9) { bt = t; best = sidx; }
+    }
+    return best;
+  }
+  // Row decomposition of a parent with `rows` rows into contiguous pieces, one
+  // tile shape each (largest tiles first), minimizing padded rows / throughput
+  // (knapsack over row counts): e.g. 160 rows -> 128 + 32.
+  std::vector<std::pair<int, int>> split(int rows, int64_t bA) const {
+    if (force >= 0 && force < N_SHAPES) return {{force, rows}};
+    const int bi = bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3;
+    std::vector<double> cost(rows + 1, 1e300);
+    std::vector<int> choice(rows + 1, -1);
+    cost[0] = 0;
+    for (int r = 1; r <= rows; ++r)
+      for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
+        if (eff[bi][sidx] <= 0) continue;
+        const int bm = shape_bm(sidx);
+        const double c = cost[std::max(0, r - bm)] + bm / eff[bi][sidx];
+        if (c < cost[r] - 1e-12) { cost[r] = c; choice[r] = sidx; }
+      }
+    std::map<int, int, std::greater<int>> tiles_by_bm;  // bm -> (shape, count) via two maps
+    std::map<int, int> shape_of_bm, count_of_bm;
+    for (int r = rows; r > 0;) {
+      const int sidx = choice[r];
+      const int bm = shape_bm(sidx);
+      shape_of_bm[bm] = sidx;
+      count_of_bm[bm] += 1;
+      r = std::max(0, r - bm);
+    }
+    std::vector<std::pair<int, int>> out;
+    int left = rows;
+    for (auto it = count_of_bm.rbegin(); it != count_of_bm.rend(); ++it) {
+      const int take = std::min(left, it->first * it->second);
+      if (take > 0) out.push_back({shape_of_bm[it->first], take});
+      left -= take;
+    }
+    return out;
+  }
+};
+
+int64_t keys_at(const bcss_plan& P, int k) {
+  if (k == 0) return 1;
+  if (k == P.m) return bcss::simplex_count(P.nbar, P.m);  // A is always BCSS
+  return P.reuse ? bcss::simplex_count(P.nbar, k) : ipow(P.nbar, k);
+}
+int64_t blk_at(const bcss_plan& P, int k) { return ipow(P.bA, k) * ipow(P.bC, P.m - k); }
+
+// Neighbour table of level k: for every output key K and every ib, the rank of
+// the stored block of T(k+1) that holds the logical block (K, ib) and the
+// redirection (stored position of each logical mode).  Reuse: K sorted,
+// stored = sorted(K u {ib}) with the canonicalize mapping (insertion).
+// No reuse: K runs over all k-tuples; T(k+1) below the top is itself a dense
+// block table (identity mapping), the top level redirects through A's BCSS.
+void build_nbr(bcss_plan& P, int k, std::vector<int2>& out) {
+  const int64_t nkeys = keys_at(P, k);
+  out.assign((size_t)(nkeys * P.nbar), int2{0, 0});
+  std::vector<int32_t> key(k), idx(k + 1), canon(k + 1), map(k + 1);
+  std::vector<int64_t> canon64(k + 1);
+  for (int64_t kr = 0; kr < nkeys; ++kr) {
+    if (k > 0) {
+      if (P.reuse) {
+        std::vector<int64_t> tmp(k);
+        bcss::hypertriangle_unrank(kr, k, P.nbar, tmp.data());
+        for (int d = 0; d < k; ++d) key[d] = (int32_t)tmp[d];
+      } else {
+        int64_t r = kr;
+        for (int d = k - 1; d >= 0; --d) { key[d] = (int32_t)(r % P.nbar); r /= P.nbar; }
+      }
+    }
+    for (int64_t ib = 0; ib < P.nbar; ++ib) {
+      for (int d = 0; d < k; ++d) idx[d] = key[d];
+      idx[k] = (int32_t)ib;
+      int64_t rank;
+      int pos;
+      if (P.reuse || k + 1 == P.m) {
+        bcss::canonical_mapping(idx.data(), k + 1, canon.data(), map.data());
+        for (int d = 0; d <= k; ++d) canon64[d] = canon[d];
+        rank = bcss::hypertriangle_rank(canon64.data(), k + 1, P.nbar);
+        pos = map[k];
+      } else {
+        rank = kr * P.nbar + ib;
+        for (int d = 0; d <= k; ++d) map[d] = d;
+        pos = k;
+      }
+      int code = pos;
+      for (int d = 0; d <= k; ++d) code |= map[d] << (4 + 3 * d);
+      out[(size_t)(kr * P.nbar + ib)] = int2{(int)rank, code};
+    }
+  }
+}
+
+// Calls (suffixes) of level k generated by the units in `units`:
+// number of nondecreasing (m-1-k)-tuples over [0, u] per unit u.
+int64_t calls_for(const bcss_plan& P, const std::vector<int>& units, int k) {
+  int64_t c = 0;
+  for (int u : units) c += (P.m - 1 - k == 0) ? 1 : bcss::simplex_count(u + 1, P.m - 1 - k);
+  return c;
+}
+
+std::vector<size_t> level_bytes(const bcss_plan& P, const std::vector<int>& units) {
+  std::vector<size_t> b(P.m, 0);
+  for (int k = 1; k < P.m; ++k)
+    b[k] = (size_t)calls_for(P, units, k) * keys_at(P, k) * blk_at(P, k) * sizeof(double);
+  return b;
+}
+
+size_t peak_for(const bcss_plan& P, const std::vector<int>& units) {
+  const auto b = level_bytes(P, units);
+  if (P.keep_temps) { size_t s = 0; for (auto v : b) s += v; return s; }
+  size_t r[2] = {0, 0};
+  for (int k = 1; k < P.m; ++k) r[(P.m - 1 - k) % 2] = std::max(r[(P.m - 1 - k) % 2], b[k]);
+  return r[0] + r[1];
+}
+
+void build_wave_levels(bcss_plan& P, WaveHost& W) {
+  const bool fast = P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0;
+  static const ShapePolicy policy;
+  W.levels.clear();
+  std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls
+  std::vector<int> prev_call;        // their call index in the T(k+1) buffer
+  int64_t prev_calls = 0;
+  const bool has_top = !W.top_units.empty();
+  int k_first = has_top ? P.m - 1 : P.m - 2;
+  if (P.start_level > 0) {  // start below caller-provided temporaries T(start_level)
+    k_first = P.start_level - 1;
+    prev_suffix = P.start_suffixes;
+    prev_calls = (int64_t)(P.start_suffixes.size() / (P.m - P.start_level));
+    for (int64_t c = 0; c < prev_calls; ++c) prev_call.push_back((int)c);
+  } else if (!has_top) {  // the top level was computed by an earlier wave
+    for (size_t i = 0; i < W.units.size(); ++i) {
+      prev_suffix.push_back(W.units[i]);
+      prev_call.push_back(W.top_call[i]);
+    }
+    prev_calls = (int64_t)W.units.size();
+  }
+  for (int k = k_first; k >= P.stop_level; --k) {
+    LevelHost L;
+    L.k = k;
+    L.keys_out = keys_at(P, k);
+    L.keys_in = keys_at(P, k + 1);
+    L.blk_out = blk_at(P, k);
+    L.blk_in = blk_at(P, k + 1);
+    L.bAk = ipow(P.bA, k);
+    L.rest = L.bAk * ipow(P.bC, P.m - 1 - k);
+    const int sl = P.m - k;  // suffix length of this level's calls
+    std::vector<int4> parents;
+    if (k == P.m - 1 && P.start_level == 0) {
+      const std::vector<int>& tu = W.top_units;
+      for (size_t i = 0; i < tu.size(); ++i) {
+        L.suffixes.push_back(tu[i]);
+        L.child_call.push_back((int)i);
+      }
+      size_t s = 0;
+      while (s < tu.size()) {
+        size_t e = s + 1;
+        while (e < tu.size() && tu[e] == tu[e - 1] + 1) ++e;
+        parents.push_back(int4{0, (int)(tu[s] * P.bC), (int)((e - s) * P.bC), (int)s});
+        s = e;
+      }
+      L.n_calls = (int64_t)tu.size();
+      // the lower levels of this wave start from its own units
+      prev_call.assign(W.top_call.begin(), W.top_call.end());
+    } else {
+      int64_t running = 0;
+      std::vector<int64_t> full(P.m);
+      for (int64_t c = 0; c < prev_calls; ++c) {
+        const int32_t* sp = &prev_suffix[(size_t)(c * (sl - 1))];
+        const int J = sp[0];
+        parents.push_back(int4{prev_call[(size_t)c], 0, (int)((J + 1) * P.bC), (int)running});
+        for (int jb = 0; jb <= J; ++jb) {
+          L.suffixes.push_back(jb);
+          for (int q = 0; q < sl - 1; ++q) L.suffixes.push_back(sp[q]);
+          if (k == 0) {
+            full[0] = jb;
+            for (int q = 0; q < sl - 1; ++q) full[q + 1] = sp[q];
+            L.child_call.push_back((int)bcss::hypertriangle_rank(full.data(), P.m, P.pbar));
+          } else {
+            L.child_call.push_back((int)running);
+          }
+          ++running;
+        }
+      }
+      L.n_calls = running;
+    }
+    // group parents into launches by tile configuration
+    std::map<int, LaunchHost> by_cfg;
+    for (const int4& whole : parents) {
+      // a parent's rows may be split into pieces of different tile shapes; a
+      // piece is a parent with a later row0 (its child index follows from
+      // child_off + (jb - row0/b_c) in the epilogue)
+      std::vector<std::pair<int, int>> pieces;
+      if (fast) pieces = policy.split(whole.z, P.bA);
+      else pieces = {{-1, whole.z}};
+      int r0 = 0;
+      for (const auto& pc : pieces) {
+        const int cfg = fast ? fast_cfg(P.bA, pc.first) : CFG_GENERIC;
+        int4 par = whole;
+        par.y = whole.y + r0;
+        par.z = pc.second;
+        par.w = whole.w + r0 / (int)P.bC;
+        r0 += pc.second;
+        LaunchHost& X = by_cfg[cfg];
+        const KernelCfg& C = kernel_cfg(cfg);
+        if (X.parents.empty()) {
+          X.cfg = cfg;
+          X.n_tiles = (int)((L.rest + C.BN - 1) / C.BN);
+          X.item_off.push_back(0);
+        }
+        X.parents.push_back(par);
+        X.item_off.push_back(X.item_off.back() +
+                             (long long)L.keys_out * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
+        X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
+      }
+    }
+    for (auto& kv : by_cfg) {
+      // flat work list: parent-major, then key, n-tile, m-tile (adjacent CTAs
+      // share the B tile of one (key, n-tile))
+      LaunchHost& X = kv.second;
+      const int BM = kernel_cfg(X.cfg).BM;
+      X.items.reserve((size_t)X.item_off.back());
+      for (size_t pi = 0; pi < X.parents.size(); ++pi) {
+        const int mtiles = (X.parents[pi].z + BM - 1) / BM;
+        for (int64_t key = 0; key < L.keys_out; ++key)
+          for (int nt = 0; nt < X.n_tiles; ++nt)
+            for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});
+      }
+      L.flops += kv.second.flops;
+      L.launches.push_back(std::move(kv.second));
+    }
+    if (k == P.m - 1 && P.start_level == 0) {
+      prev_suffix.clear();
+      for (int u : W.units) prev_suffix.push_back(u);
+      prev_calls = (int64_t)W.units.size();
+    } else {
+      prev_suffix = L.suffixes;
+      prev_call.resize((size_t)L.n_calls);
+      for (int64_t c = 0; c < L.n_calls; ++c) prev_call[(size_t)c] = (int)c;
+      prev_calls = L.n_calls;
+    }
+    W.levels.push_back(std::move(L));
+  }
+}
+
+// Exact flops of top-level subtree u: sum over levels of (calls of the
+// subtree at level k) x 2*b_c*n*keys(k)*rest(k).
+double unit_cost(const bcss_plan& P, int u) {
+  double f = 0;
+  for (int k = P.m - 1; k >= 0; --k)
+    f += (double)calls_for(P, {u}, k) * 2.0 * P.bC * P.n * keys_at(P, k) *
+         (double)(ipow(P.bA, k) * ipow(P.bC, P.m - 1 - k));
+  return f;
+}
+
+int build_plan(bcss_plan& P) {
+  if (P.built) return BCSS_OK;
+  try {
+    std::vector<int> units = P.units;
+    if (!P.units_set)
+      for (int u = 0; u < P.pbar; ++u) units.push_back(u);
+    std::sort(units.begin(), units.end());
+    units.erase(std::unique(units.begin(), units.end()), units.end());
+    // pipeline groups: contiguous units with ~equal flops, largest units first
+    // (run_host downloads one group's C while later groups compute, so the
+    // last group - the one whose download is not overlapped - is the smallest)
+    std::vector<std::vector<int>> groups;
+    if (P.pipeline_waves > 1 && !P.keep_temps && units.size() > 1) {
+      double tot = 0;
+      for (int u : units) tot += unit_cost(P, u);
+      const double target = tot / P.pipeline_waves;
+      double acc = 0;
+      groups.emplace_back();
+      for (auto it = units.rbegin(); it != units.rend(); ++it) {
+        const double c = unit_cost(P, *it);
+        if (!groups.back().empty() && acc + c / 2 > target * groups.size() &&
+            (int)groups.size() < P.pipeline_waves)
+          groups.emplace_back();
+        groups.back().push_back(*it);
+        acc += c;
+      }
+      for (auto& g : groups) std::sort(g.begin(), g.end());
+    } else {
+      groups.push_back(units);
+    }
+    // waves: greedy groups of units whose live temporaries fit the limit
+    P.waves.clear();
+    for (const auto& grp : groups) {
+      std::vector<int> cur;
+      for (int u : grp) {
+        std::vector<int> trial = cur;
+        trial.push_back(u);
+        if (!cur.empty() && !P.keep_temps && P.ws_limit > 0 && peak_for(P, trial) > P.ws_limit) {
+          P.waves.push_back(WaveHost{cur, {}, {}, {}, {}});
+          cur = {u};
+        } else {
+          cur = trial;
+        }
+      }
+      if (!cur.empty()) P.waves.push_back(WaveHost{cur, {}, {}, {}, {}});
+    }
+    if (!P.keep_temps && P.ws_limit > 0) {
+      for (auto& W : P.waves)
+        if (peak_for(P, W.units) > P.ws_limit)
+          return fail(BCSS_ERR_NOMEM, "one top-level unit needs %zu workspace bytes > limit %zu",
+                      peak_for(P, W.units), P.ws_limit);
+    }
+    if (P.start_level > 0 || P.stop_level > 0) {
+      // partial runs (multi-GPU exchange points): one wave, regions from the built levels
+      P.waves.clear();
+      P.waves.push_back(WaveHost{units, {}, {}, {}, {}});
+      WaveHost& W = P.waves[0];
+      if (P.start_level == 0) {
+        W.top_units = units;
+        for (size_t i = 0; i < units.size(); ++i) W.top_call.push_back((int)i);
+      }
+      build_wave_levels(P, W);
+      auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+      size_t r[2] = {0, 0};
+      const int k_first = W.levels.empty() ? 0 : W.levels.front().k;
+      for (auto& L : W.levels)
+        if (L.k > P.stop_level && L.k >= 1)
+          r[(k_first - L.k) % 2] = std::max(r[(k_first - L.k) % 2],
+                                            al((size_t)L.n_calls * L.keys_out * L.blk_out * sizeof(double)));
+      W.level_off.assign(P.m + 1, 0);
+      for (auto& L : W.levels)
+        if (L.k > P.stop_level && L.k >= 1) W.level_off[L.k] = (k_first - L.k) % 2 == 0 ? 0 : r[0];
+      P.ws_bytes = r[0] + r[1];
+      P.top_first = false;
+    } else {
+    // Top level: with a pipeline, the first wave computes T(m-1) for every
+    // unit (it overlaps the chunked upload of A) and later waves only run the
+    // levels below; otherwise every wave computes its own units' top level.
+    P.top_first = P.pipeline_waves > 1 && P.waves.size() > 1 && !P.keep_temps;
+    {
+      std::vector<int> all;
+      for (auto& W : P.waves) all.insert(all.end(), W.units.begin(), W.units.end());
+      std::sort(all.begin(), all.end());
+      for (size_t wi = 0; wi < P.waves.size(); ++wi) {
+        WaveHost& W = P.waves[wi];
+        W.top_units = P.top_first ? (wi == 0 ? all : std::vector<int>{}) : W.units;
+        const std::vector<int>& ref = P.top_first ? all : W.units;
+        W.top_call.clear();
+        for (int u : W.units)
+          W.top_call.push_back((int)(std::lower_bound(ref.begin(), ref.end(), u) - ref.begin()));
+      }
+    }
+    // Workspace layout per wave: keep_temps gives every level its own region;
+    // otherwise levels alternate between two regions (T(k+1) is read while
+    // T(k) is written); with top_first, T(m-1) of all units has its own
+    // region and the lower levels alternate behind it.
+    P.ws_bytes = 0;
+    auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+    size_t top_bytes = 0;
+    if (P.top_first) top_bytes = al(level_bytes(P, P.waves[0].top_units)[P.m - 1]);
+    for (auto& W : P.waves) {
+      auto b = level_bytes(P, W.units);
+      W.level_off.assign(P.m + 1, 0);
+      size_t end = 0;
+      if (P.keep_temps) {
+        for (int k = 1; k < P.m; ++k) { W.level_off[k] = end; end += al(b[k]); }
+      } else if (P.top_first) {
+        size_t r[2] = {0, 0};
+        for (int k = 1; k < P.m - 1; ++k) r[(P.m - 2 - k) % 2] = std::max(r[(P.m - 2 - k) % 2], al(b[k]));
+        W.level_off[P.m - 1] = 0;
+        for (int k = 1; k < P.m - 1; ++k) W.level_off[k] = top_bytes + ((P.m - 2 - k) % 2 == 0 ? 0 : r[0]);
+        end = top_bytes + r[0] + r[1];
+      } else {
+        size_t r[2] = {0, 0};
+        for (int k = 1; k < P.m; ++k) r[(P.m - 1 - k) % 2] = std::max(r[(P.m - 1 - k) % 2], al(b[k]));
+        for (int k = 1; k < P.m; ++k) W.level_off[k] = (P.m - 1 - k) % 2 == 0 ? 0 : r[0];
+        end = r[0] + r[1];
+      }
+      P.ws_bytes = std::max(P.ws_bytes, end);
+    }
+    }  // full run
+    // tables
+    P.nbr.assign(P.m, {});
+    P.nbr_off.assign(P.m, 0);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+    for (int k = 0; k < P.m; ++k) {
+      build_nbr(P, k, P.nbr[k]);
+      P.nbr_off[k] = take(P.nbr[k].size() * sizeof(int2));
+    }
+    P.flops = 0;
+    P.c_blocks = 0;
+    const bool partial = P.start_level > 0 || P.stop_level > 0;
+    for (auto& W : P.waves) {
+      if (!partial) build_wave_levels(P, W);
+      for (auto& L : W.levels) {
+        for (auto& X : L.launches) {
+          X.off_parents = take(X.parents.size() * sizeof(int4));
+          X.off_items = take(X.items.size() * sizeof(int4));
+        }
+        L.off_child = take(L.child_call.size() * sizeof(int));
+        P.flops += L.flops;
+        if (L.k == 0) P.c_blocks += L.n_calls;
+      }
+    }
+    P.tables_bytes = off;
+    P.built = true;
+    return BCSS_OK;
+  } catch (const std::exception& e) {
+    return fail(BCSS_ERR_PARAMETER, "plan construction failed: %s", e.what());
+  }
+}
+
+// Upload the device tables once per plan.  The copy is stream-ordered on the
+// run's stream and synchronized: a plain cudaMemcpy from pageable memory can
+// return before its DMA lands, and kernels on a non-blocking stream would
+// then race it.
+int upload_tables(bcss_plan& P, cudaStream_t stream) {
+  int dev;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (P.d_tables && P.device == dev) return BCSS_OK;
+  if (P.d_tables) { cudaFree(P.d_tables); P.d_tables = nullptr; }
+  std::vector<char> host(P.tables_bytes, 0);
+  for (int k = 0; k < P.m; ++k)
+    if (!P.nbr[k].empty()) memcpy(&host[P.nbr_off[k]], P.nbr[k].data(), P.nbr[k].size() * sizeof(int2));
+  for (auto& W : P.waves)
+    for (auto& L : W.levels) {
+      for (auto& X : L.launches) {
+        memcpy(&host[X.off_parents], X.parents.data(), X.parents.size() * sizeof(int4));
+        memcpy(&host[X.off_items], X.items.data(), X.items.size() * sizeof(int4));
+      }
+      memcpy(&host[L.off_child], L.child_call.data(), L.child_call.size() * sizeof(int));
+    }
+  CUDA_TRY(cudaMalloc(&P.d_tables, std::max<size_t>(P.tables_bytes, 256)));
+  CUDA_TRY(cudaMemcpyAsync(P.d_tables, host.data(), P.tables_bytes, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaStreamSynchronize(stream));
+  P.device = dev;
+  static bool attr_done[64] = {false};
+  if (dev < 64 && !attr_done[dev]) {
+    for (int c = 0; c < N_CFGS; ++c) {
+      const KernelCfg& C = kernel_cfg(c);
+      CUDA_TRY(cudaFuncSetAttribute(C.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C.smem));
+    }
+    attr_done[dev] = true;
+  }
+  return BCSS_OK;
+}
+
+int ensure_workspace(bcss_plan& P) {
+  if (P.ws_bytes == 0) return BCSS_OK;
+  if (P.d_ws && P.ws_capacity >= P.ws_bytes) return BCSS_OK;
+  if (P.d_ws && !P.own_ws)
+    return fail(BCSS_ERR_STATE, "caller workspace of %zu bytes < required %zu", P.ws_capacity, P.ws_bytes);
+  if (P.d_ws) cudaFree(P.d_ws);
+  P.d_ws = nullptr;
+  cudaError_t e = cudaMalloc(&P.d_ws, P.ws_bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BCSS_ERR_NOMEM, "cudaMalloc of %zu workspace bytes failed: %s", P.ws_bytes, cudaGetErrorString(e));
+  }
+  P.ws_capacity = P.ws_bytes;
+  P.own_ws = true;
+  return BCSS_OK;
+}
+
+double* region_for(bcss_plan& P, const WaveHost& W, int k) {
+  return reinterpret_cast<double*>(static_cast<char*>(P.d_ws) + W.level_off[k]);
+}
+
+int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c) {
+  if (m < 2) return fail(BCSS_ERR_PARAMETER, "change of basis is defined for order >= 2");
+  if (m > 8) return fail(BCSS_ERR_PARAMETER, "order %d > 8 is not supported", m);
+  if (n < 1 || p < 1 || b_a < 1 || b_c < 1)
+    return fail(BCSS_ERR_PARAMETER, "dimensions and block dimensions must be positive");
+  if (n % b_a != 0) return fail(BCSS_ERR_BLOCK_DIVISIBILITY, "block dimension %lld does not divide %lld", (long long)b_a, (long long)n);
+  if (p % b_c != 0) return fail(BCSS_ERR_BLOCK_DIVISIBILITY, "output block dimension %lld does not divide %lld", (long long)b_c, (long long)p);
+  // int32 limits of the device tables and per-block offsets
+  const double blk = std::pow((double)std::max(b_a, b_c), m);
+  if (blk >= 2147483647.0) return fail(BCSS_ERR_PARAMETER, "block of %g elements exceeds the int32 block offset range", blk);
+  if (n > (1 << 30) || p > (1 << 30)) return fail(BCSS_ERR_PARAMETER, "dimension too large");
+  return BCSS_OK;
+}
+
+void invalidate(bcss_plan* P) {
+  P->built = false;
+  if (P->d_tables) { cudaFree(P->d_tables); P->d_tables = nullptr; }
+}
+
+
+}  // namespace bcss_host

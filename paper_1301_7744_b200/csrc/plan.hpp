@@ -1,0 +1,163 @@
+// Host-side plan of the BCSS sttsm C ABI: structures and helpers shared by
+// plan.cu (construction), run.cu (launch orchestration) and bcss_capi.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/bcss_sttsm.h"
+#include "combinatorics.hpp"
+#include "kernel_table.cuh"
+
+namespace bcss_host {
+
+extern thread_local std::string g_last_error;
+
+inline int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      return fail(BCSS_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(_e));        \
+  } while (0)
+
+inline bool is_pow2(int64_t v) { return v > 0 && (v & (v - 1)) == 0; }
+inline int ilog2(int64_t v) { int r = 0; while ((int64_t(1) << r) < v) ++r; return r; }
+inline int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; return r; }
+
+using bcss::KernelCfg;
+using bcss::N_SHAPES;
+constexpr int N_CFGS = 1 + 4 * N_SHAPES;
+enum { CFG_GENERIC = 0 };
+const KernelCfg& kernel_cfg(int cfg);
+int fast_cfg(int64_t bA, int shape);
+
+// ---- plan ----------------------------------------------------------------------
+// One kernel launch: the parents of a level that share a tile configuration.
+struct LaunchHost {
+  int cfg = 0;
+  int n_tiles = 0;
+  uint64_t flops = 0;
+  std::vector<int4> parents;       // {in_call, row0, rows, child_off}
+  std::vector<long long> item_off; // prefix sums of work items, size parents+1
+  std::vector<int4> items;         // per work item {parent, key, n-tile, m-tile}
+  size_t off_parents = 0, off_items = 0;  // into the device table buffer
+};
+
+struct LevelHost {
+  int k = 0;
+  int64_t keys_out = 0, keys_in = 0, blk_out = 0, blk_in = 0, rest = 0, bAk = 0;
+  int64_t n_calls = 0;
+  uint64_t flops = 0;
+  std::vector<LaunchHost> launches;
+  std::vector<int> child_call;
+  std::vector<int32_t> suffixes;  // n_calls x (m-k)
+  size_t off_child = 0;
+};
+
+struct WaveHost {
+  std::vector<int> units;          // top-level units whose lower levels this wave computes
+  std::vector<LevelHost> levels;   // k = m-1 (if top_units is non-empty) down to 0
+  std::vector<size_t> level_off;   // byte offset of T(k)'s region in the workspace
+  std::vector<int> top_units;      // units of the top level computed in this wave (may be a superset)
+  std::vector<int> top_call;       // per unit of `units`: its call index in the T(m-1) buffer
+};
+
+}  // namespace bcss_host
+
+using bcss_host::LaunchHost;
+using bcss_host::LevelHost;
+using bcss_host::WaveHost;
+
+struct bcss_plan {
+  int m = 0;
+  int64_t n = 0, p = 0, bA = 0, bC = 0, nbar = 0, pbar = 0;
+  bool reuse = true;
+  std::vector<int> units;
+  bool units_set = false;
+  size_t ws_limit = 0;
+  bool keep_temps = false;
+
+  bool built = false;
+  std::vector<WaveHost> waves;
+  std::vector<std::vector<int2>> nbr;  // per k
+  std::vector<size_t> nbr_off;         // per k, into the table buffer
+  size_t ws_bytes = 0;
+  uint64_t flops = 0;
+  int64_t c_blocks = 0;
+
+  int device = -1;
+  void* d_tables = nullptr;
+  size_t tables_bytes = 0;
+  void* d_ws = nullptr;
+  size_t ws_capacity = 0;
+  bool own_ws = false;
+  double *hA = nullptr, *hX = nullptr, *hC = nullptr;  // device buffers for run_host
+  size_t hA_bytes = 0, hX_bytes = 0, hC_bytes = 0;
+  cudaStream_t host_stream = nullptr;
+  int64_t last_launches = 0;
+  bool timing = false;
+  bool dynamic = false;             // dynamic work queues (kernels use the static stride today)
+  bool concurrent = true;           // concurrent launches per level (BCSS_SERIAL_LAUNCH=1 disables)
+  int pipeline_waves = 0;           // run_host: overlap H2D / compute / D2H over this many waves
+  bool top_first = false;           // first wave computes T(m-1) for all units
+  int start_level = 0;              // 0 = from A; else compute below caller-provided T(start_level)
+  std::vector<int32_t> start_suffixes;  // their calls (m - start_level entries each)
+  int stop_level = 0;               // last level computed; its T goes to the caller's output buffer
+  cudaStream_t copy_in = nullptr, copy_out = nullptr, copy_out2 = nullptr;
+  cudaEvent_t out2_done = nullptr;
+  std::vector<cudaEvent_t> chunk_ev;  // A chunk (first block index a) landed
+  std::vector<cudaEvent_t> wave_ev;   // a wave's C blocks are final
+  unsigned* d_counters = nullptr;
+  size_t counters_n = 0;
+  std::vector<cudaStream_t> side;   // concurrent launches of one level
+  std::vector<cudaEvent_t> join;
+  cudaEvent_t fork = nullptr;
+  std::vector<cudaEvent_t> events;  // 2 per timed level
+  std::vector<int> launch_level;
+  std::vector<uint64_t> launch_flops;
+  cudaStream_t timed_stream = nullptr;
+};
+
+
+namespace bcss_host {
+
+int64_t keys_at(const bcss_plan& P, int k);
+int64_t blk_at(const bcss_plan& P, int k);
+int build_plan(bcss_plan& P);
+int upload_tables(bcss_plan& P, cudaStream_t stream);
+int ensure_workspace(bcss_plan& P);
+double* region_for(bcss_plan& P, const WaveHost& W, int k);
+int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c);
+void invalidate(bcss_plan* P);
+int64_t first_rank_with(int64_t a, int m, int64_t extent);
+bool is_pinned(const void* p);
+
+// Host-transfer pipeline of run_host: A arrives in chunks (blocks whose first
+// index is a, a contiguous range of the packed payload), wave 0's top level
+// is split by key ranges that need only the chunks already landed, and each
+// wave's C blocks are downloaded while later waves compute.
+struct Pipe {
+  double* c_host = nullptr;
+  // BCSS_TRACE=1: completion events (name, event) polled after the run
+  std::vector<std::pair<std::string, cudaEvent_t>>* trace = nullptr;
+};
+void trace_mark(const Pipe* pipe, const std::string& name, cudaStream_t s);
+int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStream_t s, const Pipe* pipe);
+
+}  // namespace bcss_host

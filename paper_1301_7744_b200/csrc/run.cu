@@ -1,0 +1,216 @@
+// Run orchestration: per-level launches (concurrent per tile shape), the
+// host-transfer pipeline of bcss_sttsm_run_host, trace marks (plan.hpp).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+
+#include "plan.hpp"
+
+namespace bcss_host {
+
+// Host-transfer pipeline of run_host: A arrives in chunks (blocks whose first
+// index is a, a contiguous range of the packed payload), wave 0's top level
+// is split by key ranges that need only the chunks already landed, and each
+// wave's C blocks are downloaded while later waves compute.
+
+void trace_mark(const Pipe* pipe, const std::string& name, cudaStream_t s) {
+  if (!pipe || !pipe->trace) return;
+  cudaEvent_t ev;
+  cudaError_t e1 = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+  cudaError_t e2 = cudaEventRecord(ev, s);
+  if (e1 != cudaSuccess || e2 != cudaSuccess)
+    fprintf(stderr, "[bcss trace] %s: %s / %s\n", name.c_str(), cudaGetErrorString(e1), cudaGetErrorString(e2));
+  pipe->trace->emplace_back(name, ev);
+}
+
+int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const LaunchHost& X, const double* A,
+               const double* X_, double* C, long long item_lo, long long item_hi, unsigned* counter,
+               cudaStream_t ls, int sms) {
+  const long long total = item_hi - item_lo;
+  if (total <= 0) return BCSS_OK;
+  const KernelCfg& K = kernel_cfg(X.cfg);
+  char* tbl = static_cast<char*>(P->d_tables);
+  bcss::LevelArgs a;
+  memset(&a, 0, sizeof(a));
+  a.X = X_;
+  const bool from_input = (P->start_level == 0 && L.k == P->m - 1) || (P->start_level > 0 && L.k == P->start_level - 1);
+  a.Tin = from_input ? A : region_for(*P, W, L.k + 1);
+  a.Tout = (L.k == P->stop_level) ? C : region_for(*P, W, L.k);
+  a.parents = reinterpret_cast<const int4*>(tbl + X.off_parents);
+  a.items = reinterpret_cast<const int4*>(tbl + X.off_items) + item_lo;
+  a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
+  a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
+  a.counter = P->dynamic ? counter : nullptr;
+  a.total_items = total;
+  a.keys_in = L.keys_in; a.keys_out = L.keys_out;
+  a.blk_in = L.blk_in; a.blk_out = L.blk_out;
+  a.n_parents = (int)X.parents.size();
+  a.n = (int)P->n; a.ldx = (int)P->n; a.p_rows = (int)P->p;
+  a.nbar = (int)P->nbar; a.bA = (int)P->bA; a.bC = (int)P->bC;
+  a.lbA = is_pow2(P->bA) ? ilog2(P->bA) : -1;
+  a.k = L.k;
+  a.rest = (int)L.rest; a.bAk = (int)L.bAk;
+  a.n_tiles = X.n_tiles;
+  for (int i = 0; i < 10; ++i) a.pw[i] = (long long)std::min<double>(std::pow((double)P->bA, i), 9.0e18);
+  int occ = 1;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
+  const long long grid = std::min<long long>(total, (long long)sms * std::max(occ, 1));
+  K.fn<<<(unsigned)grid, K.NT, K.smem, ls>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return BCSS_OK;
+}
+
+int ensure_side(bcss_plan* P, int n) {
+  while ((int)P->side.size() < n) {
+    cudaStream_t ss;
+    CUDA_TRY(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    P->side.push_back(ss);
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    P->join.push_back(ev);
+  }
+  if (!P->fork) CUDA_TRY(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming));
+  return BCSS_OK;
+}
+
+// first packed rank of the m-tuples over `extent` whose first index is a
+int64_t first_rank_with(int64_t a, int m, int64_t extent) {
+  if (a >= extent) return bcss::simplex_count(extent, m);
+  std::vector<int64_t> t(m, a);
+  return bcss::hypertriangle_rank(t.data(), m, extent);
+}
+
+int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStream_t s, const Pipe* pipe) {
+  int st = build_plan(*P);
+  if (st) return st;
+  if ((st = upload_tables(*P, s))) return st;
+  if ((st = ensure_workspace(*P))) return st;
+  int dev, sms;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int64_t launches = 0;
+  if (P->timing) {
+    P->launch_level.clear();
+    P->launch_flops.clear();
+    P->timed_stream = s;
+  }
+  // Launches of one level (one per tile shape) are independent: they run
+  // concurrently on side streams, so one launch's tail overlaps the next
+  // launch's CTAs instead of idling SMs.
+  size_t n_launch_total = 0;
+  for (auto& W : P->waves)
+    for (auto& L : W.levels) n_launch_total += L.launches.size();
+  if (P->counters_n < n_launch_total) {
+    if (P->d_counters) cudaFree(P->d_counters);
+    P->d_counters = nullptr;
+    CUDA_TRY(cudaMalloc(&P->d_counters, n_launch_total * sizeof(unsigned)));
+    P->counters_n = n_launch_total;
+  }
+  CUDA_TRY(cudaMemsetAsync(P->d_counters, 0, n_launch_total * sizeof(unsigned), s));
+  size_t counter_idx = 0;
+  int level_idx = 0;
+  const size_t blk_c = (size_t)ipow(P->bC, P->m);
+  for (size_t wi = 0; wi < P->waves.size(); ++wi) {
+    const WaveHost& W = P->waves[wi];
+    for (const LevelHost& L : W.levels) {
+      const int nl = (int)L.launches.size();
+      // chunk-gated top level of the first wave (pipelined host run)
+      const bool gate = pipe && wi == 0 && L.k == P->m - 1;
+      const bool gate_split = gate && nl == 1 && L.launches[0].parents.size() == 1;
+      if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev.back(), 0));
+      const bool conc = (P->concurrent && nl > 1) || gate_split;
+      if (conc && (st = ensure_side(P, std::max(nl - 1, 1)))) return st;
+      if (P->timing) {
+        while (P->events.size() < (size_t)(2 * (level_idx + 1))) {
+          cudaEvent_t ev;
+          CUDA_TRY(cudaEventCreate(&ev));
+          P->events.push_back(ev);
+        }
+        CUDA_TRY(cudaEventRecord(P->events[2 * level_idx], s));
+      }
+      if (conc) {
+        CUDA_TRY(cudaEventRecord(P->fork, s));
+        for (int i = 1; i < std::max(nl, 2); ++i) CUDA_TRY(cudaStreamWaitEvent(P->side[i - 1], P->fork, 0));
+      }
+      if (gate_split) {
+        // keys with first index <= a need only A chunks 0..a; ~8 sub-launches
+        // alternate between two streams, each waiting for its last chunk
+        const LaunchHost& X = L.launches[0];
+        const int64_t per_key = X.item_off.back() / L.keys_out;
+        const int64_t nb = P->nbar;
+        const int groups = (int)std::min<int64_t>(8, nb);
+        int64_t a0 = 0;
+        unsigned* counter = P->d_counters + counter_idx++;
+        for (int g = 0; g < groups; ++g) {
+          int64_t a1 = (g == groups - 1) ? nb : std::max(a0 + 1, (nb * (g + 1)) / groups);
+          const int64_t k_lo = first_rank_with(a0, P->m - 1, nb), k_hi = first_rank_with(a1, P->m - 1, nb);
+          cudaStream_t ls = (g % 2 == 0) ? s : P->side[0];
+          CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[a1 - 1], 0));
+          if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, counter, ls, sms))) return st;
+          ++launches;
+          a0 = a1;
+        }
+      } else {
+        for (int li = 0; li < nl; ++li) {
+          const LaunchHost& X = L.launches[li];
+          cudaStream_t ls = (li == 0 || !conc) ? s : P->side[li - 1];
+          unsigned* counter = P->d_counters + counter_idx++;
+          if (X.item_off.back() == 0) continue;
+          if ((st = launch_one(P, W, L, X, A, X_, C, 0, X.item_off.back(), counter, ls, sms))) return st;
+          ++launches;
+        }
+      }
+      if (conc) {
+        for (int i = 1; i < std::max(nl, 2); ++i) {
+          CUDA_TRY(cudaEventRecord(P->join[i - 1], P->side[i - 1]));
+          CUDA_TRY(cudaStreamWaitEvent(s, P->join[i - 1], 0));
+        }
+      }
+      if (P->timing) {
+        CUDA_TRY(cudaEventRecord(P->events[2 * level_idx + 1], s));
+        P->launch_level.push_back(L.k);
+        P->launch_flops.push_back(L.flops);
+      }
+      ++level_idx;
+      trace_mark(pipe, "wave" + std::to_string(wi) + " level" + std::to_string(L.k) + " done", s);
+      if (pipe && L.k == 0) {
+        // this wave's C blocks are final: download them (runs of consecutive ranks)
+        CUDA_TRY(cudaEventRecord(P->wave_ev[wi], s));
+        CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->wave_ev[wi], 0));
+        CUDA_TRY(cudaStreamWaitEvent(P->copy_out2, P->wave_ev[wi], 0));
+        int which = 0;  // alternate two DMA streams so per-copy setup overlaps
+        std::vector<int> ranks(L.child_call.begin(), L.child_call.end());
+        std::sort(ranks.begin(), ranks.end());
+        size_t i = 0;
+        while (i < ranks.size()) {
+          size_t j = i + 1;
+          while (j < ranks.size() && ranks[j] == ranks[j - 1] + 1) ++j;
+          const size_t off = (size_t)ranks[i] * blk_c;
+          CUDA_TRY(cudaMemcpyAsync(pipe->c_host + off, C + off, (j - i) * blk_c * sizeof(double),
+                                   cudaMemcpyDeviceToHost, (which ^= 1) ? P->copy_out : P->copy_out2));
+          i = j;
+        }
+        trace_mark(pipe, "wave" + std::to_string(wi) + " C downloaded", P->copy_out);
+        // submit what is queued so far (the driver otherwise batches it until a sync)
+        cudaStreamQuery(s);
+        cudaStreamQuery(P->copy_out);
+        cudaStreamQuery(P->copy_out2);
+      }
+    }
+  }
+  P->last_launches = launches;
+  return BCSS_OK;
+}
+
+bool is_pinned(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+}  // namespace bcss_host
