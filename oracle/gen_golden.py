@@ -77,6 +77,11 @@ def main() -> None:
         (4, 4, 4, 2, 2), (4, 4, 4, 2, 1), (4, 6, 6, 2, 2), (4, 8, 8, 4, 4),
         (5, 4, 4, 2, 2), (5, 6, 6, 3, 3), (5, 8, 8, 4, 4), (3, 8, 12, 2, 4),
         (4, 8, 4, 4, 2), (2, 6, 9, 3, 3), (3, 5, 5, 1, 1),
+        # fast-path edge cases: b_C != b_A (both ways), b_C in {1, 2}, large b_C, p < n, p > n
+        (3, 16, 8, 4, 1), (3, 16, 16, 4, 2), (3, 16, 32, 4, 16), (3, 32, 16, 16, 4),
+        (4, 16, 16, 8, 4), (2, 64, 64, 32, 64), (3, 64, 32, 32, 8), (2, 32, 96, 8, 32),
+        # higher orders (the reference supports any m >= 2; this build m <= 8)
+        (6, 4, 4, 2, 2), (7, 4, 4, 2, 2), (8, 2, 2, 1, 1), (6, 8, 8, 4, 4),
     ]
     for i, (m, n, p, b_a, b_c) in enumerate(small):
         a = ref.random_symmetric(m, n, SEED + 100 + i)

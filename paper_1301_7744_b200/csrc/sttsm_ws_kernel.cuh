@@ -200,9 +200,9 @@ struct WsLevelKernel {
         if (a.bAk >= 2) {
           const long long off = (col & (a.bAk - 1)) + tstride * (col >> kl);
           *reinterpret_cast<double2*>(base + off) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
-        } else {  // level 0: columns are the tail modes, stride b_c
+        } else {  // level 0: columns are the tail modes, stride b_c (rest is odd iff b_c = 1)
           base[tstride * col] = acc[fm][fn][0];
-          base[tstride * (col + 1)] = acc[fm][fn][1];
+          if (col + 1 < a.rest) base[tstride * (col + 1)] = acc[fm][fn][1];
         }
       }
     }
