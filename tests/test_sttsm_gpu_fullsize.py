@@ -208,3 +208,36 @@ def test_s5_partial_plans_reassemble_c_bitwise(cfg_id, world):
         pl.close()
     torch.cuda.synchronize()
     assert torch.equal(c, want)
+
+
+@pytest.mark.parametrize("cfg_id", [3, 4])
+def test_unit_subsets_and_workspace_waves_are_bitwise_identical(cfg_id):
+    """Plans restricted to unit subsets write exactly their C blocks (others
+    untouched), and a workspace limit that forces several waves changes
+    nothing: every variant reproduces the single-plan C bit for bit."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 71 + cfg_id)
+    x = random_matrix_device(p, n, 72 + cfg_id)
+    want = run(CFG[cfg_id], a, x)
+    pbar = p // bc
+    halves = [list(range(0, pbar, 2)), list(range(1, pbar, 2))]
+    c = torch.full_like(want, float("nan"))
+    for units in halves:
+        pl = bs.SttsmPlan(m, n, p, ba, bc, units=units)
+        part = torch.full_like(want, float("nan"))
+        pl.run(a, x, part)
+        idx = torch.as_tensor(pl.c_block_ranks(), device="cuda")
+        mask = torch.zeros(want.numel() // bc**m, dtype=torch.bool, device="cuda")
+        mask[idx] = True
+        assert torch.isnan(part.view(-1, bc**m)[~mask]).all()  # nothing written outside its blocks
+        c.view(-1, bc**m)[idx] = part.view(-1, bc**m)[idx]
+        pl.close()
+    torch.cuda.synchronize()
+    assert torch.equal(c, want)
+    full_ws = bs.SttsmPlan(m, n, p, ba, bc).workspace_bytes
+    pl = bs.SttsmPlan(m, n, p, ba, bc, workspace_limit=full_ws // 3)
+    assert pl.stats()["waves"] > 1 and pl.workspace_bytes <= full_ws // 3
+    c2 = torch.empty_like(want)
+    pl.run(a, x, c2)
+    torch.cuda.synchronize()
+    assert torch.equal(c2, want)
