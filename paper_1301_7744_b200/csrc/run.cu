@@ -85,6 +85,16 @@ int64_t first_rank_with(int64_t a, int m, int64_t extent) {
 int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStream_t s, const Pipe* pipe) {
   int st = build_plan(*P);
   if (st) return st;
+  // Without a caller workspace or an explicit limit, fit the temporaries into
+  // the free HBM by splitting the units into more waves.
+  if (!P->d_ws && P->ws_limit == 0 && !P->keep_temps && P->start_level == 0 && P->stop_level == 0) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess && P->ws_bytes > free_b / 10 * 9) {
+      P->ws_limit = free_b / 20 * 17;
+      invalidate(P);
+      if ((st = build_plan(*P))) return st;
+    }
+  }
   if ((st = upload_tables(*P, s))) return st;
   if ((st = ensure_workspace(*P))) return st;
   int dev, sms;

@@ -152,6 +152,11 @@ class SttsmPlan:
         nbytes = self.workspace_bytes
         if nbytes == 0:
             return
+        free, _ = torch.cuda.mem_get_info(device)
+        if (self._ws is None or self._ws.numel() < nbytes) and nbytes > 0.9 * free:
+            # fit the temporaries into the free HBM: more waves, smaller workspace
+            _native.check(_native.lib().bcss_plan_set_workspace_limit(self._h, int(0.85 * free)))
+            nbytes = self.workspace_bytes
         if self._ws is None or self._ws.numel() < nbytes:
             self._ws = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
         _native.check(_native.lib().bcss_plan_set_workspace(

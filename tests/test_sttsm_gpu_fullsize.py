@@ -241,3 +241,28 @@ def test_unit_subsets_and_workspace_waves_are_bitwise_identical(cfg_id):
     pl.run(a, x, c2)
     torch.cuda.synchronize()
     assert torch.equal(c2, want)
+
+
+def test_workspace_fits_free_memory_automatically():
+    """With most of HBM taken, the config-5 plan splits its units into waves on
+    its own (torch-owned workspace path) and reproduces C bitwise."""
+    m, n, p, ba, bc = CFG[5]
+    a = random_bcss_device(m, n, ba, 81)
+    x = random_matrix_device(p, n, 82)
+    want = run(CFG[5], a, x)
+    need = bs.SttsmPlan(m, n, p, ba, bc).workspace_bytes
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    budget = 40 << 30                         # leave ~40 GB of the 96 GB the single wave wants
+    hog = torch.empty(int(free - budget), dtype=torch.uint8, device="cuda")
+    try:
+        plan = bs.SttsmPlan(m, n, p, ba, bc)
+        c = torch.empty_like(want)
+        plan.run(a, x, c)
+        torch.cuda.synchronize()
+        assert plan.stats()["waves"] > 1 and plan.workspace_bytes < budget < need
+        assert torch.equal(c, want)
+        plan.close()
+    finally:
+        del hog
+        torch.cuda.empty_cache()
