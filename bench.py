@@ -66,7 +66,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--schedule", default="auto", choices=["auto", "s1", "s5"],
                     help="multi-GPU schedule: s1 = top-level subtrees, no exchange; s5 = owners + "
-                         "T(m-2) exchange + balanced subtrees (auto: s5 for N>1, m>=3)")
+                         "T(m-2) exchange + balanced subtrees (auto: s5 when s1's balance < 0.9)")
     ap.add_argument("--dense", action="store_true",
                     help="also time the dense mode-product baseline (cuBLAS) when it fits")
     ap.add_argument("--pipeline", type=int, default=4,
@@ -238,7 +238,13 @@ def run_ours(args) -> None:
     total_flops = bs.bcss_flops(m, n, p, ba, bc)
     schedule = args.schedule
     if schedule == "auto":
-        schedule = "s5" if (world > 1 and m >= 3) else "s1"
+        # S1 needs no exchange; take S5 only when S1's LPT balance is poor
+        schedule = "s1"
+        if world > 1 and m >= 3:
+            costs = unit_flops(m, n, p, ba, bc)
+            loads = [sum(costs[u] for u in part) for part in partition_units(costs, world)]
+            if sum(costs) / world / max(loads) < 0.9:
+                schedule = "s5"
     runner = None
     if schedule == "s5":
         runner = S5Runner(m, n, p, ba, bc, rank, world, dev, group=None)
