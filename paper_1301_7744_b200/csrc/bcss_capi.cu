@@ -337,16 +337,16 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());
     // host-side polling timeline (first time each event is seen complete)
     std::vector<double> seen(trace.size(), -1.0);
-    const auto t0 = std::chrono::steady_clock::now();
+    const auto t0 = h0;  // times relative to the start of this call
     size_t left = trace.size();
     while (left) {
       const double now = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       for (size_t i = 0; i < trace.size(); ++i)
         if (seen[i] < 0 && cudaEventQuery(trace[i].second) == cudaSuccess) { seen[i] = now; --left; }
     }
-    fprintf(stderr, "[bcss trace] run_host pipeline timeline (host-polled ms, relative to upload start):\n");
+    fprintf(stderr, "[bcss trace] run_host pipeline timeline (host-polled ms since the call began):\n");
     for (size_t i = 0; i < trace.size(); ++i) {
-      fprintf(stderr, "  %-28s %8.3f\n", trace[i].first.c_str(), seen[i] - seen[0]);
+      fprintf(stderr, "  %-28s %8.3f\n", trace[i].first.c_str(), seen[i]);
       cudaEventDestroy(trace[i].second);
     }
   }

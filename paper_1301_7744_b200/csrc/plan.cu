@@ -40,8 +40,8 @@ int fast_cfg(int64_t bA, int shape) {
 }
 
 // Relative DMMA efficiency of each tile shape (larger tiles reuse operands
-// more); the plan picks, per parent, the shape minimizing padded work / eff.
-// BCSS_SHAPE_EFF="e128,e64,e32" overrides, BCSS_FORCE_SHAPE=i forces one.
+// more); the plan splits each parent's rows over shapes minimizing padded
+// work / eff.  BCSS_SHAPE_EFF="e0,...,e9" overrides, BCSS_FORCE_SHAPE=i forces one.
 struct ShapePolicy {
   // Measured full-tile FP64 TFLOP/s of each shape (BCSS_FAST_SHAPES order) per
   // b_a in {4, 8, 16, 32} on B200 (tools/calibrate_shapes.py: top level of configs 2/3/4, padding
@@ -102,8 +102,7 @@ struct ShapePolicy {
         const double c = cost[std::max(0, r - bm)] + bm / eff[bi][sidx];
         if (c < cost[r] - 1e-12) { cost[r] = c; choice[r] = sidx; }
       }
-    std::map<int, int, std::greater<int>> tiles_by_bm;  // bm -> (shape, count) via two maps
-    std::map<int, int> shape_of_bm, count_of_bm;
+    std::map<int, int> shape_of_bm, count_of_bm;  // tile rows -> shape index / tile count
     for (int r = rows; r > 0;) {
       const int sidx = choice[r];
       const int bm = shape_bm(sidx);
@@ -197,7 +196,11 @@ size_t peak_for(const bcss_plan& P, const std::vector<int>& units) {
 }
 
 void build_wave_levels(bcss_plan& P, WaveHost& W) {
-  const bool fast = P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0;
+  // The fast kernel needs power-of-two blocks and the insertion form of the
+  // redirection; with reuse=False the levels below the top read dense block
+  // tables with the identity mapping (contracted position k), which is that
+  // form too - only the top level (unsorted keys into A) needs the generic kernel.
+  const bool fast_shape = is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0;
   static const ShapePolicy policy;
   W.levels.clear();
   std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls
@@ -273,6 +276,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
       // piece is a parent with a later row0 (its child index follows from
       // child_off + (jb - row0/b_c) in the epilogue)
       std::vector<std::pair<int, int>> pieces;
+      const bool fast = fast_shape && (P.reuse || k < P.m - 1);
       if (fast) pieces = policy.split(whole.z, P.bA);
       else pieces = {{-1, whole.z}};
       int r0 = 0;
