@@ -352,19 +352,29 @@ int build_plan(bcss_plan& P) {
     // last group - the one whose download is not overlapped - is the smallest)
     std::vector<std::vector<int>> groups;
     if (P.pipeline_waves > 1 && !P.keep_temps && units.size() > 1) {
+      // the first group is a single unit so the first C download starts early
+      const bool solo_first = !getenv("BCSS_PIPE_BALANCED");
+      std::vector<int> rest_units(units.begin(), units.end());
+      if (solo_first) {
+        groups.push_back({rest_units.back()});
+        rest_units.pop_back();
+      }
+      const int nw = std::max(1, P.pipeline_waves - (solo_first ? 1 : 0));
       double tot = 0;
-      for (int u : units) tot += unit_cost(P, u);
-      const double target = tot / P.pipeline_waves;
+      for (int u : rest_units) tot += unit_cost(P, u);
+      const double target = tot / nw;
       double acc = 0;
+      const size_t g0 = groups.size();
       groups.emplace_back();
-      for (auto it = units.rbegin(); it != units.rend(); ++it) {
+      for (auto it = rest_units.rbegin(); it != rest_units.rend(); ++it) {
         const double c = unit_cost(P, *it);
-        if (!groups.back().empty() && acc + c / 2 > target * groups.size() &&
+        if (!groups.back().empty() && acc + c / 2 > target * (groups.size() - g0) &&
             (int)groups.size() < P.pipeline_waves)
           groups.emplace_back();
         groups.back().push_back(*it);
         acc += c;
       }
+      if (groups.back().empty()) groups.pop_back();
       for (auto& g : groups) std::sort(g.begin(), g.end());
     } else {
       groups.push_back(units);

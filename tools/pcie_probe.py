@@ -38,3 +38,16 @@ def both():
 bi = timeit(both)
 print(json.dumps({"bytes_GB": gb, "h2d_GBps": gb / h2d, "d2h_GBps": gb / d2h, "h2d_ms": h2d * 1e3,
                   "d2h_ms": d2h * 1e3, "concurrent_ms": bi * 1e3, "concurrent_GBps_total": 2 * gb / bi}))
+
+# many medium copies (the per-wave C download pattern)
+for chunk in (256 << 10, 768 << 10, 4 << 20):
+    k = chunk // 8
+    s2 = torch.cuda.Stream()
+
+    def many():
+        with torch.cuda.stream(s2):
+            for off in range(0, n - k + 1, k):
+                h2[off:off + k].copy_(d2[off:off + k], non_blocking=True)
+
+    t = timeit(many, reps=3)
+    print(json.dumps({"d2h_chunk_bytes": chunk, "copies": n // k, "ms": t * 1e3, "GBps": gb / t}))
