@@ -47,10 +47,10 @@ struct ShapePolicy {
   // b_a in {4, 8, 16, 32} on B200 (tools/calibrate_shapes.py: top level of configs 2/3/4, padding
   // corrected); b_a = 4 borrows the b_a = 8 row.
   double eff[4][N_SHAPES] = {
-      {32.52, 29.87, 29.28, 31.85, 31.28, 28.90, 19.83, 31.09, 31.91, 29.94},
-      {32.52, 29.87, 29.28, 31.85, 31.28, 28.90, 19.83, 31.09, 31.91, 29.94},
-      {32.80, 31.61, 30.58, 32.51, 31.64, 30.48, 23.06, 31.47, 32.96, 31.15},
-      {33.11, 32.26, 31.74, 32.62, 32.04, 30.95, 21.70, 31.99, 33.08, 31.32},
+      {32.56, 30.40, 30.06, 32.19, 32.12, 29.28, 22.25, 31.96, 32.26, 30.86},
+      {32.56, 30.40, 30.06, 32.19, 32.12, 29.28, 22.25, 31.96, 32.26, 30.86},
+      {33.12, 32.31, 31.93, 32.85, 32.96, 32.05, 25.62, 32.90, 33.51, 32.11},
+      {33.33, 32.79, 33.09, 33.15, 33.02, 32.54, 21.04, 33.00, 33.64, 32.01},
   };
   int force = -1;
   ShapePolicy() {

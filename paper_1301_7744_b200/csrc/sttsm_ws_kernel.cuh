@@ -15,6 +15,7 @@
 
 #include "sttsm_kernels.cuh"
 
+
 namespace bcss {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -28,6 +29,20 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* bar) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+// Bulk (TMA-engine) copy global -> shared of `bytes` (multiple of 16), which
+// completes on `bar`; the issuing thread must have raised the barrier's
+// expected transaction count (mbar_expect_tx) by the bytes it issues.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;\n" ::"r"(b), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_copy_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+               "l"(gmem), "r"(bytes), "r"(b)
+               : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
@@ -70,6 +85,9 @@ struct WsLevelKernel {
   static constexpr int A_STAGE = BM * LDA, B_STAGE = G * GR_SIZE;
   static constexpr int NA = (BM * BK / 2) / PT;  // X pairs per producer thread per stage
   static constexpr int GP = RG * BN / 2;         // B pairs per group
+  // column runs of at least 2^BULK_MIN_LG doubles go through bulk copies
+  // (measured: 256 B runs pay off for b_a >= 16; with b_a = 8 only >= 1 KB runs do)
+  static constexpr int BULK_MIN_LG = BA >= 16 ? 5 : 7;
   static constexpr int NB = (BK * BN / 2) / PT;  // B pairs per producer thread per stage
   static constexpr int GPAD = (G + 3) / 4 * 4;   // modes per slot, int4-aligned
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) +
@@ -86,7 +104,7 @@ struct WsLevelKernel {
 
   // ---- producer: one stage of cp.async (PT threads) ----------------------------
   static __device__ __forceinline__ void produce(const LevelArgs& a, const TileInfo& t, int kstep, double* As,
-                                                 double* Bs, int* modes, int ptid) {
+                                                 double* Bs, int* modes, int ptid, uint64_t* fullbar) {
     const int k0 = kstep * BK;
 #pragma unroll 4
     for (int u = 0; u < NA; ++u) {
@@ -118,6 +136,21 @@ struct WsLevelKernel {
           const bool ok = grp_ok && cg < a.rest;
           const double* src = ok ? base + (e0 + e2) + ((long long)cg << LBA) : a.X;
           cp_async16(dst + col * RG + (e2 ^ swz(col)), src, ok);
+        }
+      } else if (pos * LBA >= BULK_MIN_LG && grp_ok && n0 + BN <= a.rest) {
+        // long column runs: one bulk copy per run into the padded [e][col]
+        // layout (the copy engine does the addressing)
+        const int sh = pos * LBA;
+        const int L = (1 << sh) < BN ? (1 << sh) : BN;   // contiguous doubles per run
+        const int runs_per_row = BN / L;
+        const int mine = ptid < RG * runs_per_row ? (RG * runs_per_row - 1 - ptid) / PT + 1 : 0;
+        if (mine) mbar_expect_tx(fullbar, (unsigned)(mine * L * 8));
+        for (int r = ptid; r < RG * runs_per_row; r += PT) {
+          const int e = r / runs_per_row, c0 = (r % runs_per_row) * L;
+          const int cg = n0 + c0;
+          const long long off = (long long)(cg & ((1 << sh) - 1)) + ((long long)(cg >> sh) << (sh + LBA)) +
+                                ((long long)(e0 + e) << sh);
+          bulk_copy_g2s(dst + e * LDR + c0, base + off, (unsigned)L * 8u, fullbar);
         }
       } else {  // column-contiguous block: pairs along col, staged [e][col]
         const int sh = pos * LBA;
@@ -242,7 +275,7 @@ struct WsLevelKernel {
       unsigned phase = 0;
       for (long long step = 0; step < total_steps; ++step) {
         if (step >= STAGES) mbar_wait(empty + slot, phase ^ 1);
-        produce(a, t, k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * GPAD, ptid);
+        produce(a, t, k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * GPAD, ptid, full + slot);
         mbar_arrive_cp_async(full + slot);
         const bool last = (k == ksteps - 1);
         if (last && ptid < BM) rowoff[slot * BM + ptid] = my_roff;
