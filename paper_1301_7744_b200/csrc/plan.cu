@@ -4,12 +4,14 @@
 // by breadth-first levels over waves of top-level units.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
 
 #include "plan.hpp"
+#include "shape_costs.hpp"
 
 namespace bcss_host {
 
@@ -39,85 +41,54 @@ int fast_cfg(int64_t bA, int shape) {
   return 1 + shape * 4 + i;
 }
 
-// Relative DMMA efficiency of each tile shape (larger tiles reuse operands
-// more); the plan splits each parent's rows over shapes minimizing padded
-// work / eff.  BCSS_SHAPE_EFF="e0,...,e9" overrides, BCSS_FORCE_SHAPE=i forces one.
+// Tile-shape policy.  A parent's rows are cut into tiles of the fast shapes;
+// a tile with fewer valid rows than its height skips the empty 8-row
+// fragments, so its cost is the measured full-tile time scaled by
+// kFragFrac (shape_costs.hpp).  The split minimizes the summed tile cost
+// (knapsack over row counts).  BCSS_FORCE_SHAPE=i forces one shape.
 struct ShapePolicy {
-  // Measured full-tile FP64 TFLOP/s of each shape (BCSS_FAST_SHAPES order) per
-  // b_a in {4, 8, 16, 32} on B200 (tools/calibrate_shapes.py: top level of configs 2/3/4, padding
-  // corrected); b_a = 4 borrows the b_a = 8 row.
-  double eff[4][N_SHAPES] = {
-      {32.56, 30.40, 30.06, 32.19, 32.12, 29.28, 22.25, 31.96, 32.26, 30.86},
-      {32.56, 30.40, 30.06, 32.19, 32.12, 29.28, 22.25, 31.96, 32.26, 30.86},
-      {33.12, 32.31, 31.93, 32.85, 32.96, 32.05, 25.62, 32.90, 33.51, 32.11},
-      {33.33, 32.79, 33.09, 33.15, 33.02, 32.54, 21.04, 33.00, 33.64, 32.01},
-  };
   int force = -1;
   ShapePolicy() {
-    // BCSS_SHAPE_EFF="e0,e1,...,e5" overrides every b_a's row; BCSS_FORCE_SHAPE=i forces one
-    if (const char* e = getenv("BCSS_SHAPE_EFF")) {
-      double v[N_SHAPES];
-      int got = 0;
-      const char* q = e;
-      while (got < N_SHAPES) {
-        int used = 0;
-        if (sscanf(q, "%lf%n", &v[got], &used) != 1) break;
-        ++got;
-        q += used;
-        if (*q == ',') ++q;
-      }
-      if (got == N_SHAPES)
-        for (auto& row : eff)
-          for (int i = 0; i < N_SHAPES; ++i) row[i] = v[i];
-    }
     if (const char* f = getenv("BCSS_FORCE_SHAPE")) force = atoi(f);
   }
-  // shape minimizing padded rows / throughput for a parent with `rows` rows
-  int pick(int rows, int64_t bA) const {
-    if (force >= 0 && force < N_SHAPES) return force;
-    const int bi = bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3;
-    int best = 0;
-    double bt = 1e300;
-    for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
-      if (eff[bi][sidx] <= 0) continue;
-      const int bm = shape_bm(sidx);
-      const double t = (double)((rows + bm - 1) / bm * bm) / eff[bi][sidx];
-      if (t < bt - 1e-9) { bt = t; best = sidx; }
-    }
-    return best;
+  static int table(int64_t bA) { return bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3; }
+  // time (arbitrary units) of one tile of shape s holding v valid rows
+  static double tile_cost(int bi, int s, int v) {
+    const int bm = shape_bm(s);
+    const int nf = (std::min(v, bm) + 7) / 8;
+    return bm / bcss::kTileTflops[bi][s] * bcss::kFragFrac[bi][s][nf - 1];
   }
-  // Row decomposition of a parent with `rows` rows into contiguous pieces, one
-  // tile shape each (largest tiles first), minimizing padded rows / throughput
-  // (knapsack over row counts): e.g. 160 rows -> 128 + 32.
+  // Row decomposition of a parent with `rows` rows into contiguous pieces,
+  // each one tile shape: the full tiles of a shape form one piece, every
+  // partial tile is a piece of its own.
   std::vector<std::pair<int, int>> split(int rows, int64_t bA) const {
     if (force >= 0 && force < N_SHAPES) return {{force, rows}};
-    const int bi = bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3;
+    const int bi = table(bA);
     std::vector<double> cost(rows + 1, 1e300);
-    std::vector<int> choice(rows + 1, -1);
+    std::vector<int2> choice(rows + 1, int2{-1, 0});  // {shape, rows of the last tile}
     cost[0] = 0;
     for (int r = 1; r <= rows; ++r)
       for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
-        if (eff[bi][sidx] <= 0) continue;
         const int bm = shape_bm(sidx);
-        const double c = cost[std::max(0, r - bm)] + bm / eff[bi][sidx];
-        if (c < cost[r] - 1e-12) { cost[r] = c; choice[r] = sidx; }
+        const int vmax = std::min(bm, r);
+        for (int nf = 1; nf <= (vmax + 7) / 8; ++nf) {  // last tile: nf valid fragments
+          const int v = std::min(8 * nf, vmax);
+          const double c = cost[r - v] + tile_cost(bi, sidx, v);
+          if (c < cost[r] - 1e-12) { cost[r] = c; choice[r] = int2{sidx, v}; }
+        }
       }
-    std::map<int, int> shape_of_bm, count_of_bm;  // tile rows -> shape index / tile count
-    for (int r = rows; r > 0;) {
-      const int sidx = choice[r];
-      const int bm = shape_bm(sidx);
-      shape_of_bm[bm] = sidx;
-      count_of_bm[bm] += 1;
-      r = std::max(0, r - bm);
-    }
+    std::map<int, int> full_rows;            // shape -> rows in full tiles
     std::vector<std::pair<int, int>> out;
-    int left = rows;
-    for (auto it = count_of_bm.rbegin(); it != count_of_bm.rend(); ++it) {
-      const int take = std::min(left, it->first * it->second);
-      if (take > 0) out.push_back({shape_of_bm[it->first], take});
-      left -= take;
+    for (int r = rows; r > 0;) {
+      const int2 c = choice[r];
+      if (c.y == shape_bm(c.x)) full_rows[c.x] += c.y;
+      else out.push_back({c.x, c.y});
+      r -= c.y;
     }
-    return out;
+    std::vector<std::pair<int, int>> pieces;
+    for (auto it = full_rows.rbegin(); it != full_rows.rend(); ++it) pieces.push_back({it->first, it->second});
+    pieces.insert(pieces.end(), out.begin(), out.end());
+    return pieces;
   }
 };
 
@@ -324,6 +295,16 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
       prev_call.resize((size_t)L.n_calls);
       for (int64_t c = 0; c < L.n_calls; ++c) prev_call[(size_t)c] = (int)c;
       prev_calls = L.n_calls;
+    }
+    if (getenv("BCSS_PLAN_DUMP")) {  // diagnostics: one line per launch
+      for (const auto& X : L.launches) {
+        std::map<int, int> rows_hist;
+        for (const int4& par : X.parents) rows_hist[par.z] += 1;
+        fprintf(stderr, "[bcss plan] level %d %-18s parents %zu items %lld gflop %.2f rows:", L.k,
+                kernel_cfg(X.cfg).name, X.parents.size(), (long long)X.item_off.back(), X.flops / 1e9);
+        for (auto& kv : rows_hist) fprintf(stderr, " %dx%d", kv.first, kv.second);
+        fprintf(stderr, "\n");
+      }
     }
     W.levels.push_back(std::move(L));
   }

@@ -103,41 +103,74 @@ struct WsLevelKernel {
   static __device__ __forceinline__ int swz(int col) { return ((col >> SW_SHIFT) & SW_MASK) << 2; }
 
   // ---- producer: one stage of cp.async (PT threads) ----------------------------
-  static __device__ __forceinline__ void produce(const LevelArgs& a, const TileInfo& t, int kstep, double* As,
-                                                 double* Bs, int* modes, int ptid, uint64_t* fullbar) {
+  // Addressing is hoisted per thread: a thread's columns (and, for
+  // e-contiguous blocks, its e pair and swizzle) are fixed within a group, so
+  // every copy after the first is one add on each side.
+  static constexpr int HP = RG / 2;          // e pairs per column (e-contiguous blocks)
+  static constexpr int CSTEP = PT / HP;      // column stride of a thread (e-contiguous blocks)
+  static constexpr int CPR = BN / 2;         // column pairs per row (column-contiguous blocks)
+  static constexpr int ESTEP = PT >= CPR ? PT / CPR : 1;   // row stride of a thread
+  static constexpr int NCOL = PT >= CPR ? 1 : CPR / PT;    // column pairs per thread
+  static_assert(PT % HP == 0 && BN % CSTEP == 0 && CSTEP % 4 == 0, "e-contiguous loader");
+  static_assert((PT >= CPR ? PT % CPR == 0 && RG % ESTEP == 0 : CPR % PT == 0), "column loader");
+
+  static __device__ __forceinline__ void cp16(unsigned sdst, const double* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(src));
+  }
+  static __device__ __forceinline__ void cp16z(unsigned sdst, const double* src, bool ok) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(src), "r"(ok ? 16 : 0));
+  }
+
+  // neighbour entries of the G groups of stage `kstep` of tile t (loaded a stage ahead)
+  static __device__ __forceinline__ void load_nb(const LevelArgs& a, const TileInfo& t, int kstep, int2 (&nb)[G]) {
+    const int2* nrow = a.nbr + (long long)t.key * a.nbar;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const int i0 = kstep * BK + g * RG;
+      nb[g] = __ldg(nrow + (i0 < a.n ? (i0 >> LBA) : 0));
+    }
+  }
+
+  static __device__ __forceinline__ void produce(const LevelArgs& a, const TileInfo& t, int kstep,
+                                                 const int2 (&nb)[G], unsigned As_s, unsigned Bs_s, int* modes,
+                                                 int ptid, uint64_t* fullbar) {
     const int k0 = kstep * BK;
-#pragma unroll 4
+#pragma unroll
     for (int u = 0; u < NA; ++u) {
       const int idx = ptid + u * PT;
       const int r = idx / (BK / 2), c = (idx % (BK / 2)) * 2;
       const int rr = t.mt * BM + r;
       const bool ok = (rr < t.rows) && (k0 + c < a.n);
       const double* src = ok ? a.X + (long long)(t.row0 + rr) * a.ldx + k0 + c : a.X;
-      cp_async16(As + r * LDA + c, src, ok);
+      cp16z(As_s + (unsigned)(r * LDA + c) * 8u, src, ok);
     }
     const int n0 = t.nt * BN;
-    const int2* nrow = a.nbr + (long long)t.key * a.nbar;
+    const bool full_n = n0 + BN <= a.rest;
     const double* tin_call = a.Tin + (long long)t.in_call * a.keys_in * a.blk_in;
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int i0 = k0 + g * RG;
       const bool grp_ok = i0 < a.n;
-      const int2 nb = __ldg(nrow + (grp_ok ? (i0 >> LBA) : 0));
-      const int pos = code_p(nb.y);
-      const double* base = tin_call + (long long)nb.x * a.blk_in;
+      const int pos = code_p(nb[g].y);
+      const double* base = tin_call + (long long)nb[g].x * a.blk_in;
       const int e0 = i0 & (BA - 1);
-      double* dst = Bs + g * GR_SIZE;
+      const unsigned dst = Bs_s + (unsigned)(g * GR_SIZE) * 8u;
       if (ptid == 0) modes[g] = pos == 0;
       if (pos == 0) {  // e-contiguous block: pairs along e, staged [col][e ^ swz]
+        const int e2 = (ptid % HP) * 2, c = ptid / HP;
+        const double* src = base + (e0 + e2) + ((long long)(n0 + c) << LBA);
+        const unsigned d = dst + (unsigned)(c * RG + (e2 ^ swz(c))) * 8u;
+        if (full_n && grp_ok) {
+#pragma unroll 8
+          for (int i = 0; i < BN / CSTEP; ++i) cp16(d + (unsigned)(i * CSTEP * RG) * 8u, src + ((long long)(i * CSTEP) << LBA));
+        } else {
 #pragma unroll 4
-        for (int q = ptid; q < GP; q += PT) {
-          const int e2 = (q % (RG / 2)) * 2, col = q / (RG / 2);
-          const int cg = n0 + col;
-          const bool ok = grp_ok && cg < a.rest;
-          const double* src = ok ? base + (e0 + e2) + ((long long)cg << LBA) : a.X;
-          cp_async16(dst + col * RG + (e2 ^ swz(col)), src, ok);
+          for (int i = 0; i < BN / CSTEP; ++i) {
+            const bool ok = grp_ok && n0 + c + i * CSTEP < a.rest;
+            cp16z(d + (unsigned)(i * CSTEP * RG) * 8u, ok ? src + ((long long)(i * CSTEP) << LBA) : a.X, ok);
+          }
         }
-      } else if (pos * LBA >= BULK_MIN_LG && grp_ok && n0 + BN <= a.rest) {
+      } else if (pos * LBA >= BULK_MIN_LG && grp_ok && full_n) {
         // long column runs: one bulk copy per run into the padded [e][col]
         // layout (the copy engine does the addressing)
         const int sh = pos * LBA;
@@ -145,36 +178,53 @@ struct WsLevelKernel {
         const int runs_per_row = BN / L;
         const int mine = ptid < RG * runs_per_row ? (RG * runs_per_row - 1 - ptid) / PT + 1 : 0;
         if (mine) mbar_expect_tx(fullbar, (unsigned)(mine * L * 8));
+        const unsigned bar = (unsigned)__cvta_generic_to_shared(fullbar);
         for (int r = ptid; r < RG * runs_per_row; r += PT) {
           const int e = r / runs_per_row, c0 = (r % runs_per_row) * L;
           const int cg = n0 + c0;
           const long long off = (long long)(cg & ((1 << sh) - 1)) + ((long long)(cg >> sh) << (sh + LBA)) +
                                 ((long long)(e0 + e) << sh);
-          bulk_copy_g2s(dst + e * LDR + c0, base + off, (unsigned)L * 8u, fullbar);
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                  dst + (unsigned)(e * LDR + c0) * 8u),
+              "l"(base + off), "r"((unsigned)L * 8u), "r"(bar)
+              : "memory");
         }
       } else {  // column-contiguous block: pairs along col, staged [e][col]
         const int sh = pos * LBA;
         const int lomask = (1 << sh) - 1;
-#pragma unroll 4
-        for (int q = ptid; q < GP; q += PT) {
-          const int c2 = (q % (BN / 2)) * 2, e = q / (BN / 2);
+        const int et = PT >= CPR ? ptid / CPR : 0;
+#pragma unroll
+        for (int j = 0; j < NCOL; ++j) {
+          const int c2 = 2 * ((PT >= CPR ? ptid % CPR : ptid) + j * PT);
           const int cg = n0 + c2;
-          const bool ok = grp_ok && cg < a.rest;
-          const long long off = (long long)(cg & lomask) + ((long long)(cg >> sh) << (sh + LBA)) +
-                                ((long long)(e0 + e) << sh);
-          const double* src = ok ? base + off : a.X;
-          cp_async16(dst + e * LDR + c2, src, ok);
+          const bool ok = grp_ok && (full_n || cg < a.rest);
+          const double* src =
+              base + ((long long)(cg & lomask) + ((long long)(cg >> sh) << (sh + LBA)) + ((long long)(e0 + et) << sh));
+          const long long sstep = (long long)ESTEP << sh;
+          const unsigned d = dst + (unsigned)(et * LDR + c2) * 8u;
+          if (ok) {
+#pragma unroll 8
+            for (int i = 0; i < RG / ESTEP; ++i) cp16(d + (unsigned)(i * ESTEP * LDR) * 8u, src + i * sstep);
+          } else {
+#pragma unroll 4
+            for (int i = 0; i < RG / ESTEP; ++i) cp16z(d + (unsigned)(i * ESTEP * LDR) * 8u, a.X, false);
+          }
         }
       }
     }
   }
 
   // ---- consumer: DMMA over one staged slice -------------------------------------
+  // Warp wm owns the 8-row fragments fm*WM + wm of the tile (interleaved, so a
+  // partial tile's valid fragments spread evenly over the warps); only the
+  // first NF of its FM fragments hold valid rows, the rest are skipped.
+  template <int NF>
   static __device__ __forceinline__ void consume(const double* As, const double* Bs, const int* modes, int cw,
                                                  double (&acc)[FM][FN][2]) {
     const int lane = threadIdx.x & 31;
     const int wm = cw / WN, wn = cw % WN;
-    const double* ap = As + (wm * WTM + (lane >> 2)) * LDA + (lane & 3);
+    const double* ap = As + (wm * 8 + (lane >> 2)) * LDA + (lane & 3);
     const int colw = wn * WTN + (lane >> 2);
     const int sw = swz(colw);
     int md[GPAD];
@@ -191,16 +241,24 @@ struct WsLevelKernel {
 #pragma unroll
       for (int kk = 0; kk < RG / 4; ++kk) {
         const int ko = cm ? ((kk * 4) ^ sw) : kk * 4 * LDR;
-        double af[FM], bf[FN];
+        double af[NF], bf[FN];
 #pragma unroll
-        for (int fm = 0; fm < FM; ++fm) af[fm] = ap[fm * 8 * LDA + (g * RG + kk * 4)];
+        for (int fm = 0; fm < NF; ++fm) af[fm] = ap[fm * 8 * WM * LDA + (g * RG + kk * 4)];
 #pragma unroll
         for (int fn = 0; fn < FN; ++fn) bf[fn] = bp[ko + fn * sn];
 #pragma unroll
-        for (int fm = 0; fm < FM; ++fm)
+        for (int fm = 0; fm < NF; ++fm)
 #pragma unroll
           for (int fn = 0; fn < FN; ++fn) dmma(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
       }
+    }
+  }
+  template <int NF>
+  static __device__ __forceinline__ void consume_valid(int nf, const double* As, const double* Bs, const int* modes,
+                                                       int cw, double (&acc)[FM][FN][2]) {
+    if constexpr (NF > 0) {
+      if (nf >= NF) consume<NF>(As, Bs, modes, cw, acc);
+      else consume_valid<NF - 1>(nf, As, Bs, modes, cw, acc);
     }
   }
 
@@ -221,6 +279,9 @@ struct WsLevelKernel {
     const int lane = threadIdx.x & 31;
     const int wn = cw % WN;
     const int kl = a.k * LBA;
+#ifdef BCSS_NO_EPILOGUE  // timing experiments only: results are not written
+    if (a.k >= 0) return;
+#endif
     const long long tstride = (long long)a.bAk * a.bC;
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
@@ -271,24 +332,40 @@ struct WsLevelKernel {
       const int ptid = threadIdx.x - NCW * 32;
       TileInfo t = decode_item(a, first, BM);
       long long my_roff = ptid < BM ? row_offset(a, t, ptid) : -1;  // fetched a tile ahead of use
+      int2 nb[G];
+      load_nb(a, t, 0, nb);
+      const unsigned As_s = (unsigned)__cvta_generic_to_shared(As);
+      const unsigned Bs_s = (unsigned)__cvta_generic_to_shared(Bs);
       int k = 0, slot = 0;
       unsigned phase = 0;
       for (long long step = 0; step < total_steps; ++step) {
+        // next stage's position and neighbour entries, loaded before this stage's copies
+        TileInfo tn = t;
+        int kn = k + 1;
+        const bool more = step + 1 < total_steps;
+        if (kn == ksteps) {
+          kn = 0;
+          if (more) tn = decode_item(a, t.item + gridDim.x, BM);
+        }
+        int2 nbn[G];
+        if (more) load_nb(a, tn, kn, nbn);
         if (step >= STAGES) mbar_wait(empty + slot, phase ^ 1);
-        produce(a, t, k, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * GPAD, ptid, full + slot);
+        produce(a, t, k, nb, As_s + (unsigned)(slot * A_STAGE) * 8u, Bs_s + (unsigned)(slot * B_STAGE) * 8u,
+                modes + slot * GPAD, ptid, full + slot);
         mbar_arrive_cp_async(full + slot);
         const bool last = (k == ksteps - 1);
         if (last && ptid < BM) rowoff[slot * BM + ptid] = my_roff;
-        if (last && ptid == 0) tiles[slot] = make_int4(t.nt, 0, 0, 0);
+        if (ptid == 0) {
+          const int vrows = t.rows - t.mt * BM;
+          tiles[slot] = make_int4(t.nt, ((vrows < BM ? vrows : BM) + 7) >> 3, 0, 0);
+        }
         mbar_arrive(full + slot);  // release this thread's modes / rowoff / tiles writes
         if (++slot == STAGES) { slot = 0; phase ^= 1; }
-        if (++k == ksteps) {
-          k = 0;
-          if (step + 1 < total_steps) {
-            t = decode_item(a, t.item + gridDim.x, BM);
-            if (ptid < BM) my_roff = row_offset(a, t, ptid);
-          }
-        }
+        if (last && more && ptid < BM) my_roff = row_offset(a, tn, ptid);
+        t = tn;
+        k = kn;
+#pragma unroll
+        for (int g = 0; g < G; ++g) nb[g] = nbn[g];
       }
       asm volatile("cp.async.wait_all;\n" ::: "memory");
       return;
@@ -306,21 +383,21 @@ struct WsLevelKernel {
     unsigned phase = 0;
     for (long long step = 0; step < total_steps; ++step) {
       mbar_wait(full + slot, phase);
-      consume(As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * GPAD, warp, acc);
+      const int4 tl = tiles[slot];
+      const int nf = tl.y > wm ? (tl.y - wm + WM - 1) / WM : 0;  // this warp's valid fragments
+      consume_valid<FM>(nf, As + slot * A_STAGE, Bs + slot * B_STAGE, modes + slot * GPAD, warp, acc);
       const bool last = (++k == ksteps);
       long long roff[FM];
-      int nt = 0;
       if (last) {  // read the tile's output rows before the slot is released
 #pragma unroll
-        for (int fm = 0; fm < FM; ++fm) roff[fm] = rowoff[slot * BM + wm * WTM + fm * 8 + (lane >> 2)];
-        nt = tiles[slot].x;
+        for (int fm = 0; fm < FM; ++fm) roff[fm] = rowoff[slot * BM + (fm * WM + wm) * 8 + (lane >> 2)];
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
       if (++slot == STAGES) { slot = 0; phase ^= 1; }
       if (last) {
         k = 0;
-        epilogue(a, roff, nt, warp, acc);
+        epilogue(a, roff, tl.x, warp, acc);
 #pragma unroll
         for (int fm = 0; fm < FM; ++fm)
 #pragma unroll
