@@ -86,8 +86,13 @@ struct WsLevelKernel {
   static constexpr int NA = (BM * BK / 2) / PT;  // X pairs per producer thread per stage
   static constexpr int GP = RG * BN / 2;         // B pairs per group
   // column runs of at least 2^BULK_MIN_LG doubles go through bulk copies
-  // (measured: 256 B runs pay off for b_a >= 16; with b_a = 8 only >= 1 KB runs do)
-  static constexpr int BULK_MIN_LG = BA >= 16 ? 5 : 7;
+  // (measured after the producer's addressing was hoisted: >= 512 B runs pay
+  // off for b_a >= 16, >= 4 KB runs for b_a <= 8; shorter runs lose to cp.async)
+#ifdef BCSS_BULK_LG_SMALL  // experiments: thresholds for b_a <= 8 / b_a >= 16
+  static constexpr int BULK_MIN_LG = BA >= 16 ? BCSS_BULK_LG_LARGE : BCSS_BULK_LG_SMALL;
+#else
+  static constexpr int BULK_MIN_LG = BA >= 16 ? 6 : 9;
+#endif
   static constexpr int NB = (BK * BN / 2) / PT;  // B pairs per producer thread per stage
   static constexpr int GPAD = (G + 3) / 4 * 4;   // modes per slot, int4-aligned
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) +
