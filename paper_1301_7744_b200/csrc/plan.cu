@@ -328,35 +328,65 @@ int build_plan(bcss_plan& P) {
       for (int u = 0; u < P.pbar; ++u) units.push_back(u);
     std::sort(units.begin(), units.end());
     units.erase(std::unique(units.begin(), units.end()), units.end());
-    // pipeline groups: contiguous units with ~equal flops, largest units first
-    // (run_host downloads one group's C while later groups compute, so the
-    // last group - the one whose download is not overlapped - is the smallest)
+    // pipeline groups: run_host computes T(m-1) of every unit first (it
+    // overlaps the upload of A), then the groups' lower levels one after the
+    // other while the previous group's C blocks download.  Contiguous groups
+    // (in unit order, largest or smallest unit first) are chosen by a DP
+    // over a two-resource model (device compute, then D2H of the group's C
+    // blocks as runs of consecutive ranks) minimizing the last download's end.
     std::vector<std::vector<int>> groups;
     if (P.pipeline_waves > 1 && !P.keep_temps && units.size() > 1) {
-      // the first group is a single unit so the first C download starts early
-      const bool solo_first = !getenv("BCSS_PIPE_BALANCED");
-      std::vector<int> rest_units(units.begin(), units.end());
-      if (solo_first) {
-        groups.push_back({rest_units.back()});
-        rest_units.pop_back();
+      const double rate_c = 33e12, rate_d = 55e9, t_copy = 3e-6, t_wave = 20e-6;  // flop/s, B/s, s, s
+      const int U = (int)units.size();
+      const int W = std::min(P.pipeline_waves, U);
+      const double blk_bytes = (double)ipow(P.bC, P.m) * sizeof(double);
+      std::vector<std::vector<int>> best_groups;
+      double best_t = 1e300;
+      for (int dir = 0; dir < 2; ++dir) {
+        std::vector<int> order(units.begin(), units.end());
+        if (dir == 0) std::reverse(order.begin(), order.end());  // largest unit first
+        std::vector<double> fl(U + 1, 0.0), by(U + 1, 0.0);
+        for (int i = 0; i < U; ++i) {
+          const int u = order[i];
+          const double top = 2.0 * P.bC * P.n * keys_at(P, P.m - 1) * (double)ipow(P.bA, P.m - 1);
+          fl[i + 1] = fl[i] + unit_cost(P, u) - top;
+          by[i + 1] = by[i] + (double)bcss::simplex_count(u + 1, P.m - 1) * blk_bytes;
+        }
+        // copies of a group of units (in value range [lo, hi]): one run per
+        // sorted prefix of length m-1 whose last index is <= hi
+        auto d2h = [&](int i, int j) {
+          int lo = order[i], hi = order[i];
+          for (int q = i; q < j; ++q) { lo = std::min(lo, order[q]); hi = std::max(hi, order[q]); }
+          const double copies = (double)bcss::simplex_count(hi + 1, P.m - 1);
+          return (by[j] - by[i]) / rate_d + copies * t_copy;
+        };
+        // td[g][j]: earliest end of the g-th group's download covering order[0, j)
+        std::vector<std::vector<double>> td(W + 1, std::vector<double>(U + 1, 1e300));
+        std::vector<std::vector<int>> from(W + 1, std::vector<int>(U + 1, -1));
+        td[0][0] = 0;
+        for (int g = 1; g <= W; ++g)
+          for (int j = 1; j <= U; ++j)
+            for (int i = g - 1; i < j; ++i) {
+              if (td[g - 1][i] >= 1e299) continue;
+              const double tc = fl[j] / rate_c + g * t_wave;  // compute of groups 1..g done
+              const double t = std::max(td[g - 1][i], tc) + d2h(i, j);
+              if (t < td[g][j]) { td[g][j] = t; from[g][j] = i; }
+            }
+        for (int g = 1; g <= W; ++g) {
+          if (td[g][U] >= best_t) continue;
+          best_t = td[g][U];
+          best_groups.clear();
+          for (int j = U, gg = g; gg > 0; j = from[gg][j], --gg)
+            best_groups.insert(best_groups.begin(), std::vector<int>(order.begin() + from[gg][j], order.begin() + j));
+        }
       }
-      const int nw = std::max(1, P.pipeline_waves - (solo_first ? 1 : 0));
-      double tot = 0;
-      for (int u : rest_units) tot += unit_cost(P, u);
-      const double target = tot / nw;
-      double acc = 0;
-      const size_t g0 = groups.size();
-      groups.emplace_back();
-      for (auto it = rest_units.rbegin(); it != rest_units.rend(); ++it) {
-        const double c = unit_cost(P, *it);
-        if (!groups.back().empty() && acc + c / 2 > target * (groups.size() - g0) &&
-            (int)groups.size() < P.pipeline_waves)
-          groups.emplace_back();
-        groups.back().push_back(*it);
-        acc += c;
-      }
-      if (groups.back().empty()) groups.pop_back();
+      groups = best_groups;
       for (auto& g : groups) std::sort(g.begin(), g.end());
+      if (getenv("BCSS_PLAN_DUMP")) {
+        fprintf(stderr, "[bcss plan] pipeline groups (model end %.3f ms):", best_t * 1e3);
+        for (auto& g : groups) fprintf(stderr, " [%d..%d]", g.front(), g.back());
+        fprintf(stderr, "\n");
+      }
     } else {
       groups.push_back(units);
     }

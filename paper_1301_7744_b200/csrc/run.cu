@@ -128,7 +128,9 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       const int nl = (int)L.launches.size();
       // chunk-gated top level of the first wave (pipelined host run)
       const bool gate = pipe && wi == 0 && L.k == P->m - 1;
-      const bool gate_split = gate && nl == 1 && L.launches[0].parents.size() == 1;
+      // every launch of the top level holds one piece of the single top parent
+      bool gate_split = gate;
+      for (const LaunchHost& X : L.launches) gate_split = gate_split && X.parents.size() == 1;
       if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev.back(), 0));
       const bool conc = (P->concurrent && nl > 1) || gate_split;
       if (conc && (st = ensure_side(P, std::max(nl - 1, 1)))) return st;
@@ -145,21 +147,29 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         for (int i = 1; i < std::max(nl, 2); ++i) CUDA_TRY(cudaStreamWaitEvent(P->side[i - 1], P->fork, 0));
       }
       if (gate_split) {
-        // keys with first index <= a need only A chunks 0..a; ~8 sub-launches
-        // alternate between two streams, each waiting for its last chunk
-        const LaunchHost& X = L.launches[0];
-        const int64_t per_key = X.item_off.back() / L.keys_out;
+        // keys with first index <= a need only A chunks 0..a: ~8 key groups per
+        // launch (tile shape), issued group-major so every shape's early keys
+        // run first; sub-launches alternate between two streams, each waiting
+        // for its group's last chunk
         const int64_t nb = P->nbar;
         const int groups = (int)std::min<int64_t>(8, nb);
         int64_t a0 = 0;
-        unsigned* counter = P->d_counters + counter_idx++;
+        unsigned* counter0 = P->d_counters + counter_idx;
+        counter_idx += nl;
+        int sub = 0;
         for (int g = 0; g < groups; ++g) {
           int64_t a1 = (g == groups - 1) ? nb : std::max(a0 + 1, (nb * (g + 1)) / groups);
           const int64_t k_lo = first_rank_with(a0, P->m - 1, nb), k_hi = first_rank_with(a1, P->m - 1, nb);
-          cudaStream_t ls = (g % 2 == 0) ? s : P->side[0];
-          CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[a1 - 1], 0));
-          if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, counter, ls, sms))) return st;
-          ++launches;
+          for (int li = 0; li < nl; ++li) {
+            const LaunchHost& X = L.launches[li];
+            const int64_t per_key = X.item_off.back() / L.keys_out;
+            if (per_key == 0 || k_hi <= k_lo) continue;
+            cudaStream_t ls = (sub++ % 2 == 0) ? s : P->side[0];
+            CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[a1 - 1], 0));
+            if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, counter0 + li, ls, sms)))
+              return st;
+            ++launches;
+          }
           a0 = a1;
         }
       } else {
@@ -193,6 +203,14 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         int which = 0;  // alternate two DMA streams so per-copy setup overlaps
         std::vector<int> ranks(L.child_call.begin(), L.child_call.end());
         std::sort(ranks.begin(), ranks.end());
+#ifdef BCSS_FAKE_CONTIG_D2H  // timing experiment: the wave's blocks as one contiguous run
+        {
+          static size_t fake_off = 0;
+          if (wi == 0) fake_off = 0;
+          for (size_t q = 0; q < ranks.size(); ++q) ranks[q] = (int)(fake_off + q);
+          fake_off += ranks.size();
+        }
+#endif
         size_t i = 0;
         while (i < ranks.size()) {
           size_t j = i + 1;
