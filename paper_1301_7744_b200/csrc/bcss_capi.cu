@@ -101,6 +101,7 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->d_ws && P->own_ws) cudaFree(P->d_ws);
   if (P->hA) cudaFree(P->hA);
   if (P->hX) cudaFree(P->hX);
+  if (P->dXm) cudaFree(P->dXm);
   if (P->hC) cudaFree(P->hC);
   if (P->host_stream) cudaStreamDestroy(P->host_stream);
   for (auto ev : P->events) cudaEventDestroy(ev);

@@ -231,7 +231,13 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
           if (k == 0) {
             full[0] = jb;
             for (int q = 0; q < sl - 1; ++q) full[q + 1] = sp[q];
-            L.child_call.push_back((int)bcss::hypertriangle_rank(full.data(), P.m, P.pbar));
+            if (P.mirror) {  // block of the original C: sorted = reversed mirrored tuple
+              std::vector<int64_t> orig(P.m);
+              for (int d = 0; d < P.m; ++d) orig[d] = P.pbar - 1 - full[P.m - 1 - d];
+              L.child_call.push_back((int)bcss::hypertriangle_rank(orig.data(), P.m, P.pbar));
+            } else {
+              L.child_call.push_back((int)bcss::hypertriangle_rank(full.data(), P.m, P.pbar));
+            }
           } else {
             L.child_call.push_back((int)running);
           }
@@ -324,6 +330,10 @@ int build_plan(bcss_plan& P) {
   if (P.built) return BCSS_OK;
   try {
     std::vector<int> units = P.units;
+    // mirrored C order for pipelined full runs on the fast kernels
+    P.mirror = P.pipeline_waves > 1 && !P.keep_temps && !P.units_set && P.start_level == 0 &&
+               P.stop_level == 0 && P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0 &&
+               !getenv("BCSS_NO_MIRROR");
     if (!P.units_set)
       for (int u = 0; u < P.pbar; ++u) units.push_back(u);
     std::sort(units.begin(), units.end());
@@ -357,7 +367,7 @@ int build_plan(bcss_plan& P) {
         auto d2h = [&](int i, int j) {
           int lo = order[i], hi = order[i];
           for (int q = i; q < j; ++q) { lo = std::min(lo, order[q]); hi = std::max(hi, order[q]); }
-          const double copies = (double)bcss::simplex_count(hi + 1, P.m - 1);
+          const double copies = P.mirror ? 1.0 : (double)bcss::simplex_count(hi + 1, P.m - 1);
           return (by[j] - by[i]) / rate_d + copies * t_copy;
         };
         // td[g][j]: earliest end of the g-th group's download covering order[0, j)

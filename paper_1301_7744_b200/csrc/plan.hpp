@@ -116,6 +116,14 @@ struct bcss_plan {
   bool concurrent = true;           // concurrent launches per level (BCSS_SERIAL_LAUNCH=1 disables)
   int pipeline_waves = 0;           // run_host: overlap H2D / compute / D2H over this many waves
   bool top_first = false;           // first wave computes T(m-1) for all units
+  // Mirrored C-block order (pipelined plans): the plan contracts X' (row blocks
+  // reversed, jb -> p̄-1-jb), so its top-level unit u is the SMALLEST index
+  // p̄-1-u of the C blocks below it, whose ranks are then one contiguous range
+  // (one D2H per wave).  Level 0 writes each block through the inverse map
+  // (block rank of the reversed mirrored tuple, element digits reversed).
+  bool mirror = false;
+  double* dXm = nullptr;            // X' (device, p x n)
+  size_t dXm_bytes = 0;
   int start_level = 0;              // 0 = from A; else compute below caller-provided T(start_level)
   std::vector<int32_t> start_suffixes;  // their calls (m - start_level entries each)
   int stop_level = 0;               // last level computed; its T goes to the caller's output buffer

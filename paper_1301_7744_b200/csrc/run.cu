@@ -53,6 +53,13 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   a.k = L.k;
   a.rest = (int)L.rest; a.bAk = (int)L.bAk;
   a.n_tiles = X.n_tiles;
+  a.row_mul = L.bAk;
+  a.mirror_digits = 0;
+  a.lbc = is_pow2(P->bC) ? ilog2(P->bC) : 0;
+  if (P->mirror && L.k == 0) {
+    a.row_mul = ipow(P->bC, P->m - 1);
+    a.mirror_digits = (int)P->m - 1;
+  }
   for (int i = 0; i < 10; ++i) a.pw[i] = (long long)std::min<double>(std::pow((double)P->bA, i), 9.0e18);
   int occ = 1;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K.fn, K.NT, K.smem));
@@ -60,6 +67,17 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   K.fn<<<(unsigned)grid, K.NT, K.smem, ls>>>(a);
   CUDA_TRY(cudaGetLastError());
   return BCSS_OK;
+}
+
+// X' for mirrored plans: row block jb of X' is row block p̄-1-jb of X
+__global__ void reverse_row_blocks(const double* __restrict__ src, double* __restrict__ dst, long long p, long long n,
+                                   long long bc) {
+  const long long total = p * n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / n, c = i - r * n;
+    const long long pbar = p / bc, jb = r / bc;
+    dst[i] = src[((pbar - 1 - jb) * bc + (r - jb * bc)) * n + c];
+  }
 }
 
 int ensure_side(bcss_plan* P, int n) {
@@ -96,6 +114,21 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     }
   }
   if ((st = upload_tables(*P, s))) return st;
+  if (P->mirror) {  // the kernels contract X' (row blocks reversed)
+    const size_t xb = (size_t)(P->p * P->n) * sizeof(double);
+    if (P->dXm_bytes < xb) {
+      if (P->dXm) cudaFree(P->dXm);
+      P->dXm = nullptr;
+      P->dXm_bytes = 0;
+      CUDA_TRY(cudaMalloc(&P->dXm, xb));
+      P->dXm_bytes = xb;
+    }
+    // pipelined host run: X is uploaded on copy_in ahead of A chunk 0
+    if (pipe) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev[0], 0));
+    reverse_row_blocks<<<296, 256, 0, s>>>(X_, P->dXm, P->p, P->n, P->bC);
+    CUDA_TRY(cudaGetLastError());
+    X_ = P->dXm;
+  }
   if ((st = ensure_workspace(*P))) return st;
   int dev, sms;
   CUDA_TRY(cudaGetDevice(&dev));

@@ -44,6 +44,9 @@ struct LevelArgs {
   int k;
   int rest, bAk;
   int n_tiles;
+  long long row_mul;        // output offset of tile row c: bAk, or b_c^(m-1) (mirrored level 0)
+  int mirror_digits;        // mirrored level 0: reverse the m-1 column digits (lbc bits each), else 0
+  int lbc;
   long long pw[10];         // bA^i
 };
 

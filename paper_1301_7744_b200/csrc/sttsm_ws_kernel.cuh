@@ -94,11 +94,13 @@ struct WsLevelKernel {
   static constexpr int BULK_MIN_LG = BA >= 16 ? 6 : 9;
 #endif
   static constexpr int NB = (BK * BN / 2) / PT;  // B pairs per producer thread per stage
+  static constexpr int CSTEP_ = PT / (RG / 2);
   static constexpr int GPAD = (G + 3) / 4 * 4;   // modes per slot, int4-aligned
   static constexpr size_t SMEM_BYTES = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double) +
                                        (size_t)STAGES * BM * sizeof(long long) +  // output row offsets
                                        STAGES * sizeof(int4) + STAGES * 2 * sizeof(uint64_t) +
-                                       STAGES * GPAD * sizeof(int);
+                                       STAGES * GPAD * sizeof(int) +
+                                       (BN / CSTEP_) * sizeof(int);  // mirrored level 0: digit_rev(i * CSTEP)
   static_assert(BM <= PT, "one producer thread per output row");
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
   static_assert((BM * BK / 2) % PT == 0 && (BK * BN / 2) % PT == 0 && GP % 32 == 0, "loader balance");
@@ -106,6 +108,18 @@ struct WsLevelKernel {
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 
   static __device__ __forceinline__ int swz(int col) { return ((col >> SW_SHIFT) & SW_MASK) << 2; }
+
+  // reverse the order of `digits` base-2^lbc digits of v
+  static __device__ __forceinline__ long long digit_rev(int v, int digits, int lbc) {
+    long long r = 0;
+    const int mask = (1 << lbc) - 1;
+    for (int d = 0; d < digits; ++d) {
+      r = (r << lbc) | (v & mask);
+      v >>= lbc;
+    }
+    return r;
+  }
+
 
   // ---- producer: one stage of cp.async (PT threads) ----------------------------
   // Addressing is hoisted per thread: a thread's columns (and, for
@@ -138,7 +152,7 @@ struct WsLevelKernel {
 
   static __device__ __forceinline__ void produce(const LevelArgs& a, const TileInfo& t, int kstep,
                                                  const int2 (&nb)[G], unsigned As_s, unsigned Bs_s, int* modes,
-                                                 int ptid, uint64_t* fullbar) {
+                                                 const int* srev, int ptid, uint64_t* fullbar) {
     const int k0 = kstep * BK;
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
@@ -161,7 +175,21 @@ struct WsLevelKernel {
       const int e0 = i0 & (BA - 1);
       const unsigned dst = Bs_s + (unsigned)(g * GR_SIZE) * 8u;
       if (ptid == 0) modes[g] = pos == 0;
-      if (pos == 0) {  // e-contiguous block: pairs along e, staged [col][e ^ swz]
+      if (pos == 0 && a.mirror_digits) {
+        // mirrored level 0: GEMM column g reads T(1) column digit_rev(g), so the
+        // output (element digits reversed) is written in GEMM column order
+        const int e2 = (ptid % HP) * 2, c = ptid / HP;
+        const unsigned d = dst + (unsigned)(c * RG + (e2 ^ swz(c))) * 8u;
+        // digit reversal is a bit permutation and n0, c, i*CSTEP have disjoint bits
+        const long long rb = digit_rev(n0 + c, a.mirror_digits, a.lbc);
+        const double* src0 = base + (e0 + e2);
+#pragma unroll 4
+        for (int i = 0; i < BN / CSTEP; ++i) {
+          const bool ok = grp_ok && n0 + c + i * CSTEP < a.rest;
+          const double* src = src0 + ((rb | srev[i]) << LBA);
+          cp16z(d + (unsigned)(i * CSTEP * RG) * 8u, ok ? src : a.X, ok);
+        }
+      } else if (pos == 0) {  // e-contiguous block: pairs along e, staged [col][e ^ swz]
         const int e2 = (ptid % HP) * 2, c = ptid / HP;
         const double* src = base + (e0 + e2) + ((long long)(n0 + c) << LBA);
         const unsigned d = dst + (unsigned)(c * RG + (e2 ^ swz(c))) * 8u;
@@ -276,7 +304,7 @@ struct WsLevelKernel {
     const int xrow = t.row0 + r;
     const int jb = xrow / a.bC, c = xrow - jb * a.bC;
     const int call = __ldg(a.child_call + t.child_off + (jb - t.row0 / a.bC));
-    return ((long long)call * a.keys_out + t.key) * a.blk_out + (long long)a.bAk * c;
+    return ((long long)call * a.keys_out + t.key) * a.blk_out + a.row_mul * c;
   }
 
   static __device__ __forceinline__ void epilogue(const LevelArgs& a, const long long (&roff)[FM], int nt, int cw,
@@ -299,6 +327,9 @@ struct WsLevelKernel {
         if (a.bAk >= 2) {
           const long long off = (col & (a.bAk - 1)) + tstride * (col >> kl);
           *reinterpret_cast<double2*>(base + off) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+        } else if (a.mirror_digits) {  // mirrored level 0: GEMM column = element offset
+          if (col + 1 < a.rest) *reinterpret_cast<double2*>(base + col) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+          else base[col] = acc[fm][fn][0];
         } else {  // level 0: columns are the tail modes, stride b_c (rest is odd iff b_c = 1)
           base[tstride * col] = acc[fm][fn][0];
           if (col + 1 < a.rest) base[tstride * (col + 1)] = acc[fm][fn][1];
@@ -316,6 +347,7 @@ struct WsLevelKernel {
     uint64_t* full = reinterpret_cast<uint64_t*>(tiles + STAGES);
     uint64_t* empty = full + STAGES;
     int* modes = reinterpret_cast<int*>(empty + STAGES);
+    int* srev = modes + STAGES * GPAD;  // mirrored level 0: digit_rev(i * CSTEP), i < BN / CSTEP
     const long long first = blockIdx.x;
     if (first >= a.total_items) return;
     const long long my_items = (a.total_items - 1 - first) / gridDim.x + 1;
@@ -335,6 +367,10 @@ struct WsLevelKernel {
       // ---------------- producer warps ----------------
       regs_dec<PROD_REGS>();
       const int ptid = threadIdx.x - NCW * 32;
+      if (a.mirror_digits) {  // producers only: named barrier 1 over the PT producer threads
+        if (ptid < BN / CSTEP) srev[ptid] = (int)digit_rev(ptid * CSTEP, a.mirror_digits, a.lbc);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(PT) : "memory");
+      }
       TileInfo t = decode_item(a, first, BM);
       long long my_roff = ptid < BM ? row_offset(a, t, ptid) : -1;  // fetched a tile ahead of use
       int2 nb[G];
@@ -356,7 +392,7 @@ struct WsLevelKernel {
         if (more) load_nb(a, tn, kn, nbn);
         if (step >= STAGES) mbar_wait(empty + slot, phase ^ 1);
         produce(a, t, k, nb, As_s + (unsigned)(slot * A_STAGE) * 8u, Bs_s + (unsigned)(slot * B_STAGE) * 8u,
-                modes + slot * GPAD, ptid, full + slot);
+                modes + slot * GPAD, srev, ptid, full + slot);
         mbar_arrive_cp_async(full + slot);
         const bool last = (k == ksteps - 1);
         if (last && ptid < BM) rowoff[slot * BM + ptid] = my_roff;

@@ -1,5 +1,6 @@
 """Quick device-resident timing of SttsmPlan on BASELINE configs (dev tool)."""
 import json
+import os
 import sys
 import time
 
@@ -15,7 +16,8 @@ def main():
     which = [int(a) for a in sys.argv[1:]] or [2, 3, 4]
     for c in which:
         m, n, p, ba, bc = CFGS[c]
-        plan = bs.SttsmPlan(m, n, p, ba, bc)
+        # QB_PIPELINE=w: a pipelined (mirrored, waved) plan on the device path
+        plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=int(os.environ.get("QB_PIPELINE", "0")))
         g = torch.Generator(device="cuda").manual_seed(1)
         A = torch.rand(plan.a_elems, dtype=torch.float64, device="cuda", generator=g) * 2 - 1
         X = torch.randn(p, n, dtype=torch.float64, device="cuda", generator=g)

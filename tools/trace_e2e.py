@@ -1,4 +1,4 @@
-"""Time the pipelined host path (run_host) for config 2 at several wave counts."""
+"""Time the pipelined host path (run_host) for config $CFG (default 2) at several wave counts."""
 import sys
 import time
 
@@ -8,7 +8,9 @@ sys.path.insert(0, ".")
 import paper_1301_7744_b200 as bs
 from paper_1301_7744_b200.generate import random_bcss_device, random_matrix_device
 
-cfg = (3, 512, 512, 32, 32)
+import os
+CFGS = {2: (3, 512, 512, 32, 32), 3: (4, 192, 192, 16, 16), 4: (5, 96, 96, 8, 8), 5: (4, 512, 256, 32, 32)}
+cfg = CFGS[int(os.environ.get("CFG", "2"))]
 m, n, p, ba, bc = cfg
 a = random_bcss_device(m, n, ba, 1).cpu().pin_memory()
 x = random_matrix_device(p, n, 2).cpu().pin_memory()
