@@ -236,14 +236,6 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         int which = 0;  // alternate two DMA streams so per-copy setup overlaps
         std::vector<int> ranks(L.child_call.begin(), L.child_call.end());
         std::sort(ranks.begin(), ranks.end());
-#ifdef BCSS_FAKE_CONTIG_D2H  // timing experiment: the wave's blocks as one contiguous run
-        {
-          static size_t fake_off = 0;
-          if (wi == 0) fake_off = 0;
-          for (size_t q = 0; q < ranks.size(); ++q) ranks[q] = (int)(fake_off + q);
-          fake_off += ranks.size();
-        }
-#endif
         size_t i = 0;
         while (i < ranks.size()) {
           size_t j = i + 1;
