@@ -110,6 +110,9 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->fork) cudaEventDestroy(P->fork);
   for (auto ev : P->chunk_ev) cudaEventDestroy(ev);
   for (auto ev : P->wave_ev) cudaEventDestroy(ev);
+  for (auto ev : P->grp_ev) cudaEventDestroy(ev);
+  for (auto ss : P->lvl_stream) cudaStreamDestroy(ss);
+  if (P->cascade_start) cudaEventDestroy(P->cascade_start);
   if (P->copy_in) cudaStreamDestroy(P->copy_in);
   if (P->copy_out) cudaStreamDestroy(P->copy_out);
   if (P->copy_out2) cudaStreamDestroy(P->copy_out2);

@@ -166,7 +166,7 @@ size_t peak_for(const bcss_plan& P, const std::vector<int>& units) {
   return r[0] + r[1];
 }
 
-void build_wave_levels(bcss_plan& P, WaveHost& W) {
+void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
   // The fast kernel needs power-of-two blocks and the insertion form of the
   // redirection; with reuse=False the levels below the top read dense block
   // tables with the identity mapping (contracted position k), which is that
@@ -277,18 +277,27 @@ void build_wave_levels(bcss_plan& P, WaveHost& W) {
         X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
       }
     }
+    const bool grouped = cascade_wave && k >= 1;
     for (auto& kv : by_cfg) {
       // flat work list: parent-major, then key, n-tile, m-tile (adjacent CTAs
-      // share the B tile of one (key, n-tile))
+      // share the B tile of one (key, n-tile)); cascade levels first split the
+      // keys into first-index groups
       LaunchHost& X = kv.second;
       const int BM = kernel_cfg(X.cfg).BM;
       X.items.reserve((size_t)X.item_off.back());
-      for (size_t pi = 0; pi < X.parents.size(); ++pi) {
-        const int mtiles = (X.parents[pi].z + BM - 1) / BM;
-        for (int64_t key = 0; key < L.keys_out; ++key)
-          for (int nt = 0; nt < X.n_tiles; ++nt)
-            for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});
+      const int ng = grouped ? (int)P.group_a.size() - 1 : 1;
+      for (int g = 0; g < ng; ++g) {
+        const int64_t k_lo = grouped ? first_rank_with(P.group_a[g], k, P.nbar) : 0;
+        const int64_t k_hi = grouped ? first_rank_with(P.group_a[g + 1], k, P.nbar) : L.keys_out;
+        if (grouped) X.group_items.push_back((long long)X.items.size());
+        for (size_t pi = 0; pi < X.parents.size(); ++pi) {
+          const int mtiles = (X.parents[pi].z + BM - 1) / BM;
+          for (int64_t key = k_lo; key < k_hi; ++key)
+            for (int nt = 0; nt < X.n_tiles; ++nt)
+              for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});
+        }
       }
+      if (grouped) X.group_items.push_back((long long)X.items.size());
       L.flops += kv.second.flops;
       L.launches.push_back(std::move(kv.second));
     }
@@ -334,6 +343,16 @@ int build_plan(bcss_plan& P) {
     P.mirror = P.pipeline_waves > 1 && !P.keep_temps && !P.units_set && P.start_level == 0 &&
                P.stop_level == 0 && P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0 &&
                !getenv("BCSS_NO_MIRROR");
+    const bool cascade_ok = P.mirror && !getenv("BCSS_NO_CASCADE") && !P.cascade_nofit;
+    P.cascade = false;  // decided by the pipeline model below
+    P.group_a.clear();
+    if (P.pipeline_waves > 1) {  // first-index groups of keys (A chunk boundaries of the gated top level)
+      const int64_t nb = P.nbar;
+      const int groups = (int)std::min<int64_t>(8, nb);
+      P.group_a.push_back(0);
+      for (int g = 0; g < groups; ++g)
+        P.group_a.push_back(g == groups - 1 ? nb : std::max(P.group_a.back() + 1, (nb * (g + 1)) / groups));
+    }
     if (!P.units_set)
       for (int u = 0; u < P.pbar; ++u) units.push_back(u);
     std::sort(units.begin(), units.end());
@@ -346,54 +365,113 @@ int build_plan(bcss_plan& P) {
     // blocks as runs of consecutive ranks) minimizing the last download's end.
     std::vector<std::vector<int>> groups;
     if (P.pipeline_waves > 1 && !P.keep_temps && units.size() > 1) {
-      const double rate_c = 33e12, rate_d = 55e9, t_copy = 3e-6, t_wave = 20e-6;  // flop/s, B/s, s, s
+      const double rate_c = 33e12, rate_d = 55e9, rate_h = 55e9, t_copy = 3e-6, t_wave = 20e-6;  // flop/s, B/s, s
       const int U = (int)units.size();
       const int W = std::min(P.pipeline_waves, U);
       const double blk_bytes = (double)ipow(P.bC, P.m) * sizeof(double);
-      std::vector<std::vector<int>> best_groups;
-      double best_t = 1e300;
-      for (int dir = 0; dir < 2; ++dir) {
-        std::vector<int> order(units.begin(), units.end());
-        if (dir == 0) std::reverse(order.begin(), order.end());  // largest unit first
-        std::vector<double> fl(U + 1, 0.0), by(U + 1, 0.0);
-        for (int i = 0; i < U; ++i) {
-          const int u = order[i];
-          const double top = 2.0 * P.bC * P.n * keys_at(P, P.m - 1) * (double)ipow(P.bA, P.m - 1);
-          fl[i + 1] = fl[i] + unit_cost(P, u) - top;
-          by[i + 1] = by[i] + (double)bcss::simplex_count(u + 1, P.m - 1) * blk_bytes;
-        }
-        // copies of a group of units (in value range [lo, hi]): one run per
-        // sorted prefix of length m-1 whose last index is <= hi
-        auto d2h = [&](int i, int j) {
-          int lo = order[i], hi = order[i];
-          for (int q = i; q < j; ++q) { lo = std::min(lo, order[q]); hi = std::max(hi, order[q]); }
-          const double copies = P.mirror ? 1.0 : (double)bcss::simplex_count(hi + 1, P.m - 1);
-          return (by[j] - by[i]) / rate_d + copies * t_copy;
-        };
-        // td[g][j]: earliest end of the g-th group's download covering order[0, j)
-        std::vector<std::vector<double>> td(W + 1, std::vector<double>(U + 1, 1e300));
-        std::vector<std::vector<int>> from(W + 1, std::vector<int>(U + 1, -1));
-        td[0][0] = 0;
-        for (int g = 1; g <= W; ++g)
-          for (int j = 1; j <= U; ++j)
-            for (int i = g - 1; i < j; ++i) {
-              if (td[g - 1][i] >= 1e299) continue;
-              const double tc = fl[j] / rate_c + g * t_wave;  // compute of groups 1..g done
-              const double t = std::max(td[g - 1][i], tc) + d2h(i, j);
-              if (t < td[g][j]) { td[g][j] = t; from[g][j] = i; }
-            }
-        for (int g = 1; g <= W; ++g) {
-          if (td[g][U] >= best_t) continue;
-          best_t = td[g][U];
-          best_groups.clear();
-          for (int j = U, gg = g; gg > 0; j = from[gg][j], --gg)
-            best_groups.insert(best_groups.begin(), std::vector<int>(order.begin() + from[gg][j], order.begin() + j));
+      const int G = (int)P.group_a.size() - 1;
+      // A chunk a (blocks of first index a) lands at t_land[a] (seconds from the upload start)
+      std::vector<double> t_land(P.nbar);
+      {
+        double acc = 0;
+        for (int64_t a = 0; a < P.nbar; ++a) {
+          acc += (double)bcss::simplex_count(P.nbar - a, P.m - 1) * (double)ipow(P.bA, P.m) * sizeof(double);
+          t_land[a] = acc / rate_h;
         }
       }
+      const double t_up = t_land[P.nbar - 1];
+      // flops of level k, key group g, for the given units (top level: all units)
+      auto group_flops = [&](const std::vector<int>& us, int k, int g) {
+        const double keys = (double)(first_rank_with(P.group_a[g + 1], k, P.nbar) - first_rank_with(P.group_a[g], k, P.nbar));
+        return (double)calls_for(P, us, k) * 2.0 * P.bC * P.n * keys * (double)(ipow(P.bA, k) * ipow(P.bC, P.m - 1 - k));
+      };
+      // Compute of the first wave (units `us`) relative to the end of the upload:
+      // list-schedule the gated groups (top level of all units; with the
+      // cascade also the first wave's levels m-2..1) on one device at rate_c,
+      // higher levels first; then the remaining levels.
+      auto first_wave = [&](const std::vector<int>& us, bool cascade) {
+        const int kmin = cascade ? 1 : P.m - 1;
+        std::vector<std::vector<double>> done(P.m + 1, std::vector<double>(G, 0.0));
+        std::vector<std::vector<bool>> fin(P.m, std::vector<bool>(G, false));
+        double now = 0;
+        for (int left = (P.m - kmin) * G; left > 0; --left) {
+          int bk = -1, bg = -1;
+          double best_ready = 1e300;
+          for (int k = P.m - 1; k >= kmin; --k)
+            for (int g = 0; g < G; ++g) {
+              if (fin[k][g] || (g > 0 && !fin[k][g - 1])) continue;
+              if (k < P.m - 1 && !fin[k + 1][g]) continue;
+              const double ready = std::max(k == P.m - 1 ? t_land[P.group_a[g + 1] - 1] : done[k + 1][g],
+                                            g > 0 ? done[k][g - 1] : 0.0);
+              // earliest-ready job; ties (already ready) go to the higher level
+              const double key = std::max(ready, now);
+              if (key < best_ready - 1e-12) { best_ready = key; bk = k; bg = g; }
+              break;  // only the first unfinished group of each level is a candidate
+            }
+          const std::vector<int>& who = (bk == P.m - 1) ? units : us;
+          now = best_ready + group_flops(who, bk, bg) / rate_c;
+          done[bk][bg] = now;
+          fin[bk][bg] = true;
+        }
+        double rest = 0;  // levels not gated: k < kmin (incl. level 0), first wave only
+        for (int k = kmin - 1; k >= 0; --k)
+          rest += (double)calls_for(P, us, k) * 2.0 * P.bC * P.n * keys_at(P, k) *
+                  (double)(ipow(P.bA, k) * ipow(P.bC, P.m - 1 - k));
+        return std::max(now, t_up) - t_up + rest / rate_c + t_wave;
+      };
+      std::vector<std::vector<int>> best_groups;
+      double best_t = 1e300;
+      bool best_cascade = false;
+      for (int mode = 0; mode < (cascade_ok ? 2 : 1); ++mode)
+        for (int dir = 0; dir < 2; ++dir) {
+          std::vector<int> order(units.begin(), units.end());
+          if (dir == 0) std::reverse(order.begin(), order.end());  // largest unit first
+          std::vector<double> fl(U + 1, 0.0), by(U + 1, 0.0);
+          const double top = 2.0 * P.bC * P.n * keys_at(P, P.m - 1) * (double)ipow(P.bA, P.m - 1);
+          for (int i = 0; i < U; ++i) {
+            const int u = order[i];
+            fl[i + 1] = fl[i] + unit_cost(P, u) - top;
+            by[i + 1] = by[i] + (double)bcss::simplex_count(u + 1, P.m - 1) * blk_bytes;
+          }
+          // copies of a group of units (in value range [lo, hi]): one run per
+          // sorted prefix of length m-1 whose last index is <= hi (mirrored: one)
+          auto d2h = [&](int i, int j) {
+            int hi = order[i];
+            for (int q = i; q < j; ++q) hi = std::max(hi, order[q]);
+            const double copies = P.mirror ? 1.0 : (double)bcss::simplex_count(hi + 1, P.m - 1);
+            return (by[j] - by[i]) / rate_d + copies * t_copy;
+          };
+          for (int i1 = 1; i1 <= U; ++i1) {
+            const double tc1 = first_wave(std::vector<int>(order.begin(), order.begin() + i1), mode == 1);
+            // td[g][j]: earliest end of the g-th group's download covering order[0, j)
+            std::vector<std::vector<double>> td(W + 1, std::vector<double>(U + 1, 1e300));
+            std::vector<std::vector<int>> from(W + 1, std::vector<int>(U + 1, -1));
+            td[1][i1] = tc1 + d2h(0, i1);
+            from[1][i1] = 0;
+            for (int g = 2; g <= W; ++g)
+              for (int j = i1 + 1; j <= U; ++j)
+                for (int i = i1; i < j; ++i) {
+                  if (td[g - 1][i] >= 1e299) continue;
+                  const double tc = tc1 + (fl[j] - fl[i1]) / rate_c + (g - 1) * t_wave;  // groups 1..g computed
+                  const double t = std::max(td[g - 1][i], tc) + d2h(i, j);
+                  if (t < td[g][j]) { td[g][j] = t; from[g][j] = i; }
+                }
+            for (int g = 1; g <= W; ++g) {
+              if (td[g][U] >= best_t - 1e-9) continue;
+              best_t = td[g][U];
+              best_cascade = mode == 1;
+              best_groups.clear();
+              for (int j = U, gg = g; gg > 0; j = from[gg][j], --gg)
+                best_groups.insert(best_groups.begin(), std::vector<int>(order.begin() + from[gg][j], order.begin() + j));
+            }
+          }
+        }
       groups = best_groups;
+      P.cascade = best_cascade;
       for (auto& g : groups) std::sort(g.begin(), g.end());
       if (getenv("BCSS_PLAN_DUMP")) {
-        fprintf(stderr, "[bcss plan] pipeline groups (model end %.3f ms):", best_t * 1e3);
+        fprintf(stderr, "[bcss plan] pipeline groups (model: %.3f ms after the upload, cascade %d):", best_t * 1e3,
+                (int)P.cascade);
         for (auto& g : groups) fprintf(stderr, " [%d..%d]", g.front(), g.back());
         fprintf(stderr, "\n");
       }
@@ -431,7 +509,7 @@ int build_plan(bcss_plan& P) {
         W.top_units = units;
         for (size_t i = 0; i < units.size(); ++i) W.top_call.push_back((int)i);
       }
-      build_wave_levels(P, W);
+      build_wave_levels(P, W, false);
       auto al = [](size_t v) { return (v + 255) / 256 * 256; };
       size_t r[2] = {0, 0};
       const int k_first = W.levels.empty() ? 0 : W.levels.front().k;
@@ -474,8 +552,13 @@ int build_plan(bcss_plan& P) {
       auto b = level_bytes(P, W.units);
       W.level_off.assign(P.m + 1, 0);
       size_t end = 0;
-      if (P.keep_temps) {
+      const bool disjoint = P.cascade && &W == &P.waves[0];  // cascade: levels overlap in time
+      if (P.keep_temps || (disjoint && !P.top_first)) {
         for (int k = 1; k < P.m; ++k) { W.level_off[k] = end; end += al(b[k]); }
+      } else if (disjoint) {
+        W.level_off[P.m - 1] = 0;
+        end = top_bytes;
+        for (int k = P.m - 2; k >= 1; --k) { W.level_off[k] = end; end += al(b[k]); }
       } else if (P.top_first) {
         size_t r[2] = {0, 0};
         for (int k = 1; k < P.m - 1; ++k) r[(P.m - 2 - k) % 2] = std::max(r[(P.m - 2 - k) % 2], al(b[k]));
@@ -489,6 +572,11 @@ int build_plan(bcss_plan& P) {
         end = r[0] + r[1];
       }
       P.ws_bytes = std::max(P.ws_bytes, end);
+    }
+    if (P.cascade && P.ws_limit > 0 && P.ws_bytes > P.ws_limit) {
+      // the first wave's disjoint regions do not fit: run it level-synchronously
+      P.cascade_nofit = true;
+      return build_plan(P);
     }
     }  // full run
     // tables
@@ -504,7 +592,7 @@ int build_plan(bcss_plan& P) {
     P.c_blocks = 0;
     const bool partial = P.start_level > 0 || P.stop_level > 0;
     for (auto& W : P.waves) {
-      if (!partial) build_wave_levels(P, W);
+      if (!partial) build_wave_levels(P, W, P.cascade && &W == &P.waves[0]);
       for (auto& L : W.levels) {
         for (auto& X : L.launches) {
           X.off_parents = take(X.parents.size() * sizeof(int4));
@@ -595,6 +683,7 @@ int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c) {
 
 void invalidate(bcss_plan* P) {
   P->built = false;
+  P->cascade_nofit = false;
   if (P->d_tables) { cudaFree(P->d_tables); P->d_tables = nullptr; }
 }
 

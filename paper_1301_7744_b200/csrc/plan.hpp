@@ -56,6 +56,9 @@ struct LaunchHost {
   std::vector<int4> parents;       // {in_call, row0, rows, child_off}
   std::vector<long long> item_off; // prefix sums of work items, size parents+1
   std::vector<int4> items;         // per work item {parent, key, n-tile, m-tile}
+  // cascade levels: items are ordered by key group (first key index in
+  // [group_a[g], group_a[g+1])) first; group g is items [group_items[g], group_items[g+1])
+  std::vector<long long> group_items;
   size_t off_parents = 0, off_items = 0;  // into the device table buffer
 };
 
@@ -122,6 +125,13 @@ struct bcss_plan {
   // (one D2H per wave).  Level 0 writes each block through the inverse map
   // (block rank of the reversed mirrored tuple, element digits reversed).
   bool mirror = false;
+  // Cascade (pipelined host runs): the first wave's levels m-1..1 run as key
+  // groups of equal first index; group g of level k needs only A chunks /
+  // T(k+1) groups <= g, so the levels below the top proceed while A is still
+  // uploading.  The first wave's temporaries then get disjoint regions.
+  bool cascade = false;
+  bool cascade_nofit = false;       // the disjoint first-wave regions exceeded the workspace limit
+  std::vector<int64_t> group_a;     // first-index boundaries of the key groups
   double* dXm = nullptr;            // X' (device, p x n)
   size_t dXm_bytes = 0;
   int start_level = 0;              // 0 = from A; else compute below caller-provided T(start_level)
@@ -131,6 +141,9 @@ struct bcss_plan {
   cudaEvent_t out2_done = nullptr;
   std::vector<cudaEvent_t> chunk_ev;  // A chunk (first block index a) landed
   std::vector<cudaEvent_t> wave_ev;   // a wave's C blocks are final
+  std::vector<cudaStream_t> lvl_stream;  // cascade: one stream per level
+  std::vector<cudaEvent_t> grp_ev;       // cascade: [k * groups + g] = groups 0..g of level k done
+  cudaEvent_t cascade_start = nullptr;
   unsigned* d_counters = nullptr;
   size_t counters_n = 0;
   std::vector<cudaStream_t> side;   // concurrent launches of one level

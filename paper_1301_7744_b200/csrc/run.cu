@@ -157,7 +157,64 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
   const size_t blk_c = (size_t)ipow(P->bC, P->m);
   for (size_t wi = 0; wi < P->waves.size(); ++wi) {
     const WaveHost& W = P->waves[wi];
+    const bool cascade = pipe && P->cascade && wi == 0;
+    if (cascade) {
+      // Levels m-1..1 of the first wave as key-group sub-launches, one stream
+      // per level: group g of the top level waits for A chunks 0..a_{g+1}-1,
+      // group g of level k for groups 0..g of level k+1 (a key of first index a
+      // only reads blocks whose first index is <= a), so the lower levels run
+      // while A is still uploading.
+      const int G = (int)P->group_a.size() - 1;
+      if ((int)P->lvl_stream.size() < 2 * P->m) {
+        // two streams per level (groups alternate); higher levels get higher
+        // priority so the gated top level keeps pace with the upload and the
+        // levels below fill the idle SMs
+        int lo = 0, hi = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        while ((int)P->lvl_stream.size() < 2 * P->m) {
+          const int k = (int)P->lvl_stream.size() / 2;
+          const int prio = std::max(hi, lo - (k * (lo - hi) + P->m - 2) / std::max(1, P->m - 1));
+          cudaStream_t ss;
+          CUDA_TRY(cudaStreamCreateWithPriority(&ss, cudaStreamNonBlocking, prio));
+          P->lvl_stream.push_back(ss);
+        }
+      }
+      while (P->grp_ev.size() < (size_t)(P->m * G)) {
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        P->grp_ev.push_back(ev);
+      }
+      if (!P->cascade_start) CUDA_TRY(cudaEventCreateWithFlags(&P->cascade_start, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(P->cascade_start, s));  // tables, X' and counters are ready
+      for (const LevelHost& L : W.levels) {
+        if (L.k == 0) continue;
+        for (int q = 0; q < 2; ++q) CUDA_TRY(cudaStreamWaitEvent(P->lvl_stream[2 * L.k + q], P->cascade_start, 0));
+        unsigned* counter0 = P->d_counters + counter_idx;
+        counter_idx += L.launches.size();
+        for (int g = 0; g < G; ++g) {
+          cudaStream_t ls = P->lvl_stream[2 * L.k + (g & 1)];
+          if (L.k == P->m - 1) {
+            CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[P->group_a[g + 1] - 1], 0));
+          } else {  // groups <= g of level k+1: g on one stream, g-1 (and earlier) on the other
+            CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g], 0));
+            if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g - 1], 0));
+          }
+          for (size_t li = 0; li < L.launches.size(); ++li) {
+            const LaunchHost& X = L.launches[li];
+            const long long lo = X.group_items[g], hi = X.group_items[g + 1];
+            if (hi <= lo) continue;
+            if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, counter0 + li, ls, sms))) return st;
+            ++launches;
+          }
+          if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[L.k * G + g - 1], 0));  // groups <= g done
+          CUDA_TRY(cudaEventRecord(P->grp_ev[L.k * G + g], ls));
+        }
+        trace_mark(pipe, "wave0 level" + std::to_string(L.k) + " done", P->lvl_stream[2 * L.k + ((G - 1) & 1)]);
+      }
+      CUDA_TRY(cudaStreamWaitEvent(s, P->grp_ev[1 * G + G - 1], 0));
+    }
     for (const LevelHost& L : W.levels) {
+      if (cascade && L.k >= 1) continue;
       const int nl = (int)L.launches.size();
       // chunk-gated top level of the first wave (pipelined host run)
       const bool gate = pipe && wi == 0 && L.k == P->m - 1;
