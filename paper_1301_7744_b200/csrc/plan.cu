@@ -443,6 +443,9 @@ int build_plan(bcss_plan& P) {
           };
           for (int i1 = 1; i1 <= U; ++i1) {
             const double tc1 = first_wave(std::vector<int>(order.begin(), order.begin() + i1), mode == 1);
+            if (getenv("BCSS_PLAN_DUMP") && atoi(getenv("BCSS_PLAN_DUMP")) > 1)
+              fprintf(stderr, "[bcss plan]   mode %d dir %d first group %d units: compute %.3f ms after upload, d2h %.3f ms\n",
+                      mode, dir, i1, tc1 * 1e3, d2h(0, i1) * 1e3);
             // td[g][j]: earliest end of the g-th group's download covering order[0, j)
             std::vector<std::vector<double>> td(W + 1, std::vector<double>(U + 1, 1e300));
             std::vector<std::vector<int>> from(W + 1, std::vector<int>(U + 1, -1));
