@@ -471,6 +471,7 @@ int build_plan(bcss_plan& P) {
         }
       groups = best_groups;
       P.cascade = best_cascade;
+      if (cascade_ok && getenv("BCSS_FORCE_CASCADE")) P.cascade = true;  // tests / experiments
       for (auto& g : groups) std::sort(g.begin(), g.end());
       if (getenv("BCSS_PLAN_DUMP")) {
         fprintf(stderr, "[bcss plan] pipeline groups (model: %.3f ms after the upload, cascade %d):", best_t * 1e3,

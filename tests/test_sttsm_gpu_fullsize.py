@@ -290,3 +290,26 @@ def test_workspace_fits_free_memory_automatically():
     finally:
         del hog
         torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_cascade_is_bitwise_identical_to_level_synchronous(cfg_id, monkeypatch):
+    """The cascade (first wave's levels as first-index key groups gated on A
+    chunks and upstream groups) reorders launches, not arithmetic: forced on
+    and forced off, the pipelined host run returns the same bits."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 81 + cfg_id)
+    x = random_matrix_device(p, n, 82 + cfg_id)
+    a_h, x_h = a.cpu().pin_memory(), x.cpu().pin_memory()
+    outs = []
+    for env in ("BCSS_FORCE_CASCADE", "BCSS_NO_CASCADE"):
+        monkeypatch.setenv(env, "1")
+        plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=4)
+        plan.stats()  # build with the variable set
+        monkeypatch.delenv(env)
+        c_h = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+        plan.run_host(a_h.numpy(), x_h.numpy(), c_h.numpy())
+        outs.append(c_h.clone())
+        plan.close()
+    assert torch.equal(outs[0], outs[1])
+    assert not torch.isnan(outs[0]).any()
