@@ -123,9 +123,14 @@ int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X
                         double* C_packed);
 
 /* Overlap host transfers with compute in bcss_sttsm_run_host: A is uploaded
- * in chunks (blocks with first index a) that gate the first wave's top-level
- * work, and the top-level units are split into `waves` flop-balanced groups
- * whose C blocks download while later groups compute.  0 = off. */
+ * in chunks (blocks with first index a) that gate the top-level work (and, when
+ * the plan's model predicts a gain, the first wave's lower levels: key groups of
+ * equal first index), and the top-level units are split into at most `waves`
+ * groups whose C blocks download while later groups compute.  Such a plan
+ * contracts the C modes in mirrored order (X with reversed row blocks) so every
+ * group's C blocks form one contiguous range: its results equal the plain
+ * plan's to rounding (~1e-16 relative), not bit for bit, and are identical
+ * between bcss_sttsm_run and bcss_sttsm_run_host.  0 = off. */
 int bcss_plan_set_pipeline(bcss_plan* plan, int waves);
 
 /* Partial runs, the exchange points of the multi-GPU schedule:
