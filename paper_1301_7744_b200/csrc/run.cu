@@ -143,8 +143,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
   // concurrently on side streams, so one launch's tail overlaps the next
   // launch's CTAs instead of idling SMs.
   size_t n_launch_total = 0;
-  for (auto& W : P->waves)
-    for (auto& L : W.levels) n_launch_total += L.launches.size();
+  for (auto& W : P->waves)  // one zeroed queue counter per kernel launch (sub-launches included)
+    for (auto& L : W.levels) n_launch_total += L.launches.size() * 9;
   if (P->counters_n < n_launch_total) {
     if (P->d_counters) cudaFree(P->d_counters);
     P->d_counters = nullptr;
@@ -189,8 +189,6 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       for (const LevelHost& L : W.levels) {
         if (L.k == 0) continue;
         for (int q = 0; q < 2; ++q) CUDA_TRY(cudaStreamWaitEvent(P->lvl_stream[2 * L.k + q], P->cascade_start, 0));
-        unsigned* counter0 = P->d_counters + counter_idx;
-        counter_idx += L.launches.size();
         for (int g = 0; g < G; ++g) {
           cudaStream_t ls = P->lvl_stream[2 * L.k + (g & 1)];
           if (L.k == P->m - 1) {
@@ -203,7 +201,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
             const LaunchHost& X = L.launches[li];
             const long long lo = X.group_items[g], hi = X.group_items[g + 1];
             if (hi <= lo) continue;
-            if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, counter0 + li, ls, sms))) return st;
+            if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, P->d_counters + counter_idx++, ls, sms))) return st;
             ++launches;
           }
           if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[L.k * G + g - 1], 0));  // groups <= g done
@@ -244,8 +242,6 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         const int64_t nb = P->nbar;
         const int groups = (int)std::min<int64_t>(8, nb);
         int64_t a0 = 0;
-        unsigned* counter0 = P->d_counters + counter_idx;
-        counter_idx += nl;
         int sub = 0;
         for (int g = 0; g < groups; ++g) {
           int64_t a1 = (g == groups - 1) ? nb : std::max(a0 + 1, (nb * (g + 1)) / groups);
@@ -256,7 +252,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
             if (per_key == 0 || k_hi <= k_lo) continue;
             cudaStream_t ls = (sub++ % 2 == 0) ? s : P->side[0];
             CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[a1 - 1], 0));
-            if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, counter0 + li, ls, sms)))
+            if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, P->d_counters + counter_idx++,
+                                 ls, sms)))
               return st;
             ++launches;
           }
