@@ -252,6 +252,31 @@ struct WsLevelKernel {
   // Warp wm owns the 8-row fragments fm*WM + wm of the tile (interleaved, so a
   // partial tile's valid fragments spread evenly over the warps); only the
   // first NF of its FM fragments hold valid rows, the rest are skipped.
+  // one row group (one ib) of the slice, for a compile-time staging mode
+  // (CM: e-contiguous block staged [col][e ^ swz]; else [e][col])
+  // (MODE 1: e-contiguous, 0: column-contiguous, -1: select at run time from cm)
+  template <int NF, int MODE>
+  static __device__ __forceinline__ void consume_group(const double* ap, const double* Bg, int colw, int sw, int g,
+                                                       bool cm_rt, double (&acc)[FM][FN][2]) {
+    const int lane = threadIdx.x & 31;
+    const bool cm = MODE < 0 ? cm_rt : MODE == 1;
+    const double* bp = Bg + (cm ? colw * RG + (lane & 3) : (lane & 3) * LDR + colw);
+    const int SN = cm ? 8 * RG : 8;
+#pragma unroll
+    for (int kk = 0; kk < RG / 4; ++kk) {
+      const int ko = cm ? ((kk * 4) ^ sw) : kk * 4 * LDR;
+      double af[NF], bf[FN];
+#pragma unroll
+      for (int fm = 0; fm < NF; ++fm) af[fm] = ap[fm * 8 * WM * LDA + (g * RG + kk * 4)];
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) bf[fn] = bp[ko + fn * SN];
+#pragma unroll
+      for (int fm = 0; fm < NF; ++fm)
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) dmma(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+    }
+  }
+
   template <int NF>
   static __device__ __forceinline__ void consume(const double* As, const double* Bs, const int* modes, int cw,
                                                  double (&acc)[FM][FN][2]) {
@@ -268,21 +293,11 @@ struct WsLevelKernel {
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const bool cm = md[g] != 0;
-      const double* bp = Bs + g * GR_SIZE + (cm ? colw * RG + (lane & 3) : (lane & 3) * LDR + colw);
-      const int sn = cm ? 8 * RG : 8;
-#pragma unroll
-      for (int kk = 0; kk < RG / 4; ++kk) {
-        const int ko = cm ? ((kk * 4) ^ sw) : kk * 4 * LDR;
-        double af[NF], bf[FN];
-#pragma unroll
-        for (int fm = 0; fm < NF; ++fm) af[fm] = ap[fm * 8 * WM * LDA + (g * RG + kk * 4)];
-#pragma unroll
-        for (int fn = 0; fn < FN; ++fn) bf[fn] = bp[ko + fn * sn];
-#pragma unroll
-        for (int fm = 0; fm < NF; ++fm)
-#pragma unroll
-          for (int fn = 0; fn < FN; ++fn) dmma(acc[fm][fn][0], acc[fm][fn][1], af[fm], bf[fn]);
+      if constexpr (RG >= 16) {  // the mode is CTA-uniform per group: branch to a specialized body
+        if (md[g]) consume_group<NF, 1>(ap, Bs + g * GR_SIZE, colw, sw, g, true, acc);
+        else consume_group<NF, 0>(ap, Bs + g * GR_SIZE, colw, sw, g, false, acc);
+      } else {  // short groups (b_a <= 8): selects are cheaper than the branches (measured)
+        consume_group<NF, -1>(ap, Bs + g * GR_SIZE, colw, sw, g, md[g] != 0, acc);
       }
     }
   }
