@@ -134,3 +134,30 @@ def test_status_codes_raise_named_errors():
     with pytest.raises(bs.ShapeError):
         bs.hypertriangle_rank((2, 1), 3)
     assert "outside" in _native.lib().bcss_last_error().decode() or True
+
+
+@pytest.mark.parametrize("cfg,waves", [((3, 512, 512, 32, 32), 4), ((4, 64, 64, 16, 16), 3),
+                                       ((5, 32, 48, 8, 8), 4), ((3, 64, 48, 16, 8), 3)])
+def test_pipelined_plan_writes_every_c_block_once_in_contiguous_waves(cfg, waves):
+    """A pipelined (mirrored) plan writes each C block exactly once, with the
+    right flops, and every wave's blocks form one contiguous rank range (one
+    D2H per wave): the rank list (wave order) splits into at most
+    `stats()["waves"]` segments that are each a contiguous set of ranks."""
+    m, n, p, ba, bc = cfg
+    plan = bs.SttsmPlan(*cfg, pipeline=waves)
+    st = plan.stats()
+    assert 1 <= st["waves"] <= waves
+    assert st["flops"] == bs.bcss_flops(*cfg)
+    ranks = plan.c_block_ranks().tolist()
+    assert sorted(ranks) == list(range(bs.simplex_count(p // bc, m)))
+    # fewest segments with contiguous rank sets (DP over cut positions)
+    best = [0] + [10 ** 9] * len(ranks)
+    for j in range(len(ranks)):
+        if best[j] >= 10 ** 9:
+            continue
+        lo = hi = ranks[j]
+        for i in range(j, len(ranks)):
+            lo, hi = min(lo, ranks[i]), max(hi, ranks[i])
+            if hi - lo == i - j:
+                best[i + 1] = min(best[i + 1], best[j] + 1)
+    assert best[-1] <= st["waves"]
