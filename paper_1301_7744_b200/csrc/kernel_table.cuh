@@ -40,10 +40,24 @@ KernelCfg make_cfg(const char* name) {
 
 constexpr int N_SHAPES = 10;
 
+// General-redirection variants (reuse=False top level), a subset of the shapes
+// above; BCSS_GEN_OF[i] is the fast shape each one mirrors (its measured cost).
+#define BCSS_GEN_SHAPES(X, BA)                                                 \
+  X((WsLevelKernel<128, 128, 32, 4, 4, 3, BA, 4, true>), "gen128x128c16")     \
+  X((WsLevelKernel<64, 256, 16, 2, 8, 4, BA, 4, true>), "gen64x256c16")       \
+  X((WsLevelKernel<32, 256, 32, 1, 8, 3, BA, 4, true>), "gen32x256c8")
+
+constexpr int N_GEN = 3;
+constexpr int BCSS_GEN_OF[N_GEN] = {3, 4, 2};
+
 extern const KernelCfg kFast4[N_SHAPES];
 extern const KernelCfg kFast8[N_SHAPES];
 extern const KernelCfg kFast16[N_SHAPES];
 extern const KernelCfg kFast32[N_SHAPES];
+extern const KernelCfg kGen4[N_GEN];
+extern const KernelCfg kGen8[N_GEN];
+extern const KernelCfg kGen16[N_GEN];
+extern const KernelCfg kGen32[N_GEN];
 extern const KernelCfg kGeneric;
 
 }  // namespace bcss

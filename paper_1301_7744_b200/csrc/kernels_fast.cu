@@ -12,4 +12,5 @@
 
 namespace bcss {
 const KernelCfg BCSS_CAT(kFast, BCSS_BA)[N_SHAPES] = {BCSS_FAST_SHAPES(BCSS_ENTRY, BCSS_BA)};
+const KernelCfg BCSS_CAT(kGen, BCSS_BA)[N_GEN] = {BCSS_GEN_SHAPES(BCSS_ENTRY, BCSS_BA)};
 }  // namespace bcss

@@ -24,9 +24,22 @@ int shape_bm(int shape) { return bcss::kFast32[shape].BM; }
 
 const KernelCfg& kernel_cfg(int cfg) {
   if (cfg == 0) return bcss::kGeneric;
+  if (cfg > 4 * N_SHAPES) {  // general-redirection variants
+    const int g = (cfg - 1 - 4 * N_SHAPES) / 4, ba = (cfg - 1) % 4;
+    const KernelCfg* t = ba == 0 ? bcss::kGen4 : ba == 1 ? bcss::kGen8 : ba == 2 ? bcss::kGen16 : bcss::kGen32;
+    return t[g];
+  }
   const int shape = (cfg - 1) / 4, ba = (cfg - 1) % 4;
   const KernelCfg* t = ba == 0 ? bcss::kFast4 : ba == 1 ? bcss::kFast8 : ba == 2 ? bcss::kFast16 : bcss::kFast32;
   return t[shape];
+}
+// general-redirection configuration mirroring fast shape `shape` (one of BCSS_GEN_OF), else -1
+int gen_cfg(int64_t bA, int shape) {
+  const int f = fast_cfg(bA, 0);
+  if (f < 0) return -1;
+  for (int g = 0; g < N_GEN; ++g)
+    if (bcss::BCSS_GEN_OF[g] == shape) return 1 + 4 * N_SHAPES + g * 4 + (f - 1);
+  return -1;
 }
 // fast configuration of tile shape `shape` for power-of-two b_a in {4, 8, 16, 32}, else -1
 int fast_cfg(int64_t bA, int shape) {
@@ -61,14 +74,15 @@ struct ShapePolicy {
   // Row decomposition of a parent with `rows` rows into contiguous pieces,
   // each one tile shape: the full tiles of a shape form one piece, every
   // partial tile is a piece of its own.
-  std::vector<std::pair<int, int>> split(int rows, int64_t bA) const {
-    if (force >= 0 && force < N_SHAPES) return {{force, rows}};
+  std::vector<std::pair<int, int>> split(int rows, int64_t bA, unsigned allowed = ~0u) const {
+    if (force >= 0 && force < N_SHAPES && ((allowed >> force) & 1)) return {{force, rows}};
     const int bi = table(bA);
     std::vector<double> cost(rows + 1, 1e300);
     std::vector<int2> choice(rows + 1, int2{-1, 0});  // {shape, rows of the last tile}
     cost[0] = 0;
     for (int r = 1; r <= rows; ++r)
       for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
+        if (!((allowed >> sidx) & 1)) continue;
         const int bm = shape_bm(sidx);
         const int vmax = std::min(bm, r);
         for (int nf = 1; nf <= (vmax + 7) / 8; ++nf) {  // last tile: nf valid fragments
@@ -254,11 +268,16 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       // child_off + (jb - row0/b_c) in the epilogue)
       std::vector<std::pair<int, int>> pieces;
       const bool fast = fast_shape && (P.reuse || k < P.m - 1);
+      // reuse=False top level: unsorted keys, general redirection permutations
+      const bool gen = fast_shape && !fast && !getenv("BCSS_NO_GEN_TOP");
+      unsigned gen_mask = 0;
+      for (int g = 0; g < bcss::N_GEN; ++g) gen_mask |= 1u << bcss::BCSS_GEN_OF[g];
       if (fast) pieces = policy.split(whole.z, P.bA);
+      else if (gen) pieces = policy.split(whole.z, P.bA, gen_mask);
       else pieces = {{-1, whole.z}};
       int r0 = 0;
       for (const auto& pc : pieces) {
-        const int cfg = fast ? fast_cfg(P.bA, pc.first) : CFG_GENERIC;
+        const int cfg = fast ? fast_cfg(P.bA, pc.first) : gen ? gen_cfg(P.bA, pc.first) : CFG_GENERIC;
         int4 par = whole;
         par.y = whole.y + r0;
         par.z = pc.second;

@@ -59,7 +59,9 @@ __device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.a
 
 // NPROD producer warps form whole warpgroups (setmaxnreg acts per warpgroup):
 // they shrink to PROD_REGS registers and the consumers grow into the rest.
-template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, int BA, int NPROD = 4>
+// GEN = true: general redirection permutations (reuse=False top level, whose
+// unsorted keys map to A's canonical blocks by arbitrary mode permutations).
+template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, int BA, int NPROD = 4, bool GEN = false>
 struct WsLevelKernel {
   static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int NCW = WM * WN;               // consumer warps
@@ -136,6 +138,9 @@ struct WsLevelKernel {
   static __device__ __forceinline__ void cp16(unsigned sdst, const double* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sdst), "l"(src));
   }
+  static __device__ __forceinline__ void cp8z(unsigned sdst, const double* src, bool ok) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sdst), "l"(src), "r"(ok ? 8 : 0));
+  }
   static __device__ __forceinline__ void cp16z(unsigned sdst, const double* src, bool ok) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sdst), "l"(src), "r"(ok ? 16 : 0));
   }
@@ -147,6 +152,67 @@ struct WsLevelKernel {
     for (int g = 0; g < G; ++g) {
       const int i0 = kstep * BK + g * RG;
       nb[g] = __ldg(nrow + (i0 < a.n ? (i0 >> LBA) : 0));
+    }
+  }
+
+  // General redirection: logical mode d < k of the block (K, ib) sits at stored
+  // position code_map(code, d), the contracted mode k at code_map(code, k), the
+  // tail behind the b_a digits.  For power-of-two b_a the column -> stored
+  // offset map is a bit permutation, so it distributes over disjoint bit fields.
+  static __device__ __forceinline__ long long perm_col(int col, int code, int k) {
+    long long r = 0;
+    for (int d = 0; d < k; ++d) r |= (long long)((col >> (d * LBA)) & (BA - 1)) << (code_map(code, d) * LBA);
+    return r | ((long long)(col >> (k * LBA)) << ((k + 1) * LBA));
+  }
+  static constexpr int LOG_NI = (BN / CSTEP_ >= 64) ? 6 : (BN / CSTEP_ >= 32) ? 5 : (BN / CSTEP_ >= 16) ? 4
+                              : (BN / CSTEP_ >= 8) ? 3 : (BN / CSTEP_ >= 4) ? 2 : (BN / CSTEP_ >= 2) ? 1 : 0;
+  static __device__ __forceinline__ void produce_group_gen(const LevelArgs& a, int code, const double* base, int e0,
+                                                        bool grp_ok, bool full_n, int n0, unsigned dst, int* mode,
+                                                        int ptid) {
+    const int k = a.k;
+    const int se = code_map(code, k) * LBA;  // log2 of the e stride
+    if (ptid == 0) *mode = se == 0;
+    if (se == 0) {  // e-contiguous: pairs along e, staged [col][e ^ swz]
+      const int e2 = (ptid % HP) * 2, c = ptid / HP;
+      const unsigned d = dst + (unsigned)(c * RG + (e2 ^ swz(c))) * 8u;
+      const long long pb = perm_col(n0 + c, code, k);
+      long long basis[LOG_NI > 0 ? LOG_NI : 1];
+#pragma unroll
+      for (int j = 0; j < LOG_NI; ++j) basis[j] = perm_col(CSTEP << j, code, k);
+      const double* src0 = base + (e0 + e2);
+#pragma unroll 4
+      for (int i = 0; i < BN / CSTEP; ++i) {
+        long long off = pb;
+#pragma unroll
+        for (int j = 0; j < LOG_NI; ++j)
+          if ((i >> j) & 1) off |= basis[j];
+        const bool ok = grp_ok && (full_n || n0 + c + i * CSTEP < a.rest);
+        cp16z(d + (unsigned)(i * CSTEP * RG) * 8u, ok ? src0 + off : a.X, ok);
+      }
+    } else {  // column-contiguous or scattered columns: staged [e][col]
+      const bool pair = code_map(code, 0) == 0 || k == 0;  // columns c2, c2+1 adjacent
+      const int et = PT >= CPR ? ptid / CPR : 0;
+#pragma unroll
+      for (int j = 0; j < NCOL; ++j) {
+        const int c2 = 2 * ((PT >= CPR ? ptid % CPR : ptid) + j * PT);
+        const int cg = n0 + c2;
+        const bool ok = grp_ok && (full_n || cg < a.rest);
+        const bool ok1 = grp_ok && (full_n || cg + 1 < a.rest);
+        const long long sstep = (long long)ESTEP << se;
+        const double* src = base + perm_col(cg, code, k) + ((long long)(e0 + et) << se);
+        const double* src1 = base + perm_col(cg + 1, code, k) + ((long long)(e0 + et) << se);
+        const unsigned d = dst + (unsigned)(et * LDR + c2) * 8u;
+#pragma unroll 4
+        for (int i = 0; i < RG / ESTEP; ++i) {
+          const unsigned di = d + (unsigned)(i * ESTEP * LDR) * 8u;
+          if (pair) {
+            cp16z(di, ok ? src + i * sstep : a.X, ok);
+          } else {
+            cp8z(di, ok ? src + i * sstep : a.X, ok);
+            cp8z(di + 8u, ok1 ? src1 + i * sstep : a.X, ok1);
+          }
+        }
+      }
     }
   }
 
@@ -174,6 +240,10 @@ struct WsLevelKernel {
       const double* base = tin_call + (long long)nb[g].x * a.blk_in;
       const int e0 = i0 & (BA - 1);
       const unsigned dst = Bs_s + (unsigned)(g * GR_SIZE) * 8u;
+      if constexpr (GEN) {
+        produce_group_gen(a, nb[g].y, base, e0, grp_ok, full_n, n0, dst, modes + g, ptid);
+        continue;
+      }
       if (ptid == 0) modes[g] = pos == 0;
       if (pos == 0 && a.mirror_digits) {
         // mirrored level 0: GEMM column g reads T(1) column digit_rev(g), so the

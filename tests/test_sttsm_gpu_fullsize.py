@@ -313,3 +313,20 @@ def test_cascade_is_bitwise_identical_to_level_synchronous(cfg_id, monkeypatch):
         plan.close()
     assert torch.equal(outs[0], outs[1])
     assert not torch.isnan(outs[0]).any()
+
+
+@pytest.mark.parametrize("cfg_id", [2, 3, 4])
+def test_noreuse_full_size_matches_reuse(cfg_id):
+    """reuse=False (product-keyed temporaries; its top level reads A through
+    general mode permutations on the fast kernel) agrees with reuse=True at
+    full size to fp64 rounding."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 91 + cfg_id)
+    x = random_matrix_device(p, n, 92 + cfg_id)
+    want = run(CFG[cfg_id], a, x)
+    plan = bs.SttsmPlan(m, n, p, ba, bc, reuse=False)
+    c = torch.full_like(want, float("nan"))
+    plan.run(a, x, c)
+    torch.cuda.synchronize()
+    assert float((c - want).norm() / want.norm()) <= 1e-13
+    plan.close()
