@@ -69,6 +69,8 @@ def parse_args():
                          "T(m-2) exchange + balanced subtrees (auto: s5 when s1's balance < 0.9)")
     ap.add_argument("--dense", action="store_true",
                     help="also time the dense mode-product baseline (cuBLAS) when it fits")
+    ap.add_argument("--noreuse", action="store_true",
+                    help="also time reuse=False (the algorithm-by-blocks without partial-symmetry reuse)")
     ap.add_argument("--pipeline", type=int, default=4,
                     help="waves of the e2e transfer/compute pipeline (0 = serial copies)")
     return ap.parse_args()
@@ -218,6 +220,32 @@ def run_dense(args, A, X, m, n, p, ba, rank, world, dev, job_ms):
             "impl": "dense mode-product chain, cuBLAS DGEMM via torch.tensordot"}
 
 
+def run_noreuse(args, A, X, m, n, p, ba, bc, rank, world, job_ms):
+    """reuse=False on the same inputs: the paper's with/without-reuse comparison."""
+    import torch
+
+    import paper_1301_7744_b200 as bs
+
+    if rank != 0 or world != 1:
+        return None
+    plan = bs.SttsmPlan(m, n, p, ba, bc, reuse=False)
+    C = torch.empty(plan.c_elems, dtype=torch.float64, device=A.device)
+    for _ in range(2):
+        plan.run(A, X, C)
+    torch.cuda.synchronize()
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record()
+    for _ in range(args.steps):
+        plan.run(A, X, C)
+    s1.record()
+    s1.synchronize()
+    ms = s0.elapsed_time(s1) / args.steps
+    fl = bs.bcss_flops(m, n, p, ba, bc, reuse=False)
+    plan.close()
+    return {"ms_per_step": round(ms, 4), "flops_per_step": fl, "tflops": round(fl / ms / 1e9, 3),
+            "speedup_reuse_vs_noreuse": round(ms / (job_ms / args.steps), 3)}
+
+
 def run_ours(args) -> None:
     import numpy as np
     import torch
@@ -324,6 +352,7 @@ def run_ours(args) -> None:
         pl.set_timing(False)
 
     dense_line = run_dense(args, A, X, m, n, p, ba, rank, world, dev, job_ms) if args.dense else None
+    noreuse_line = run_noreuse(args, A, X, m, n, p, ba, bc, rank, world, job_ms) if args.noreuse else None
     a_np_cpu = x_np_cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         a_np_cpu, x_np_cpu = A.cpu().numpy(), X.cpu().numpy()
@@ -409,6 +438,7 @@ def run_ours(args) -> None:
             "e2e": e2e,
             "gpu_launches": launches,
             "dense_baseline": dense_line,
+            "noreuse_baseline": noreuse_line,
             "clocks": clocks,
             "flops_per_step": total_flops,
         }
