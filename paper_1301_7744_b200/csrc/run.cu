@@ -216,8 +216,10 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       const int nl = (int)L.launches.size();
       // chunk-gated top level of the first wave (pipelined host run)
       const bool gate = pipe && wi == 0 && L.k == P->m - 1;
-      // every launch of the top level holds one piece of the single top parent
-      bool gate_split = gate;
+      // every launch of the top level holds one piece of the single top parent;
+      // key ranges follow A's chunks only for sorted keys (reuse=True): a
+      // product key K reads blocks whose first index is min(K), not K[0]
+      bool gate_split = gate && P->reuse;
       for (const LaunchHost& X : L.launches) gate_split = gate_split && X.parents.size() == 1;
       if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev.back(), 0));
       const bool conc = (P->concurrent && nl > 1) || gate_split;

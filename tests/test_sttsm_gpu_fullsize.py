@@ -330,3 +330,21 @@ def test_noreuse_full_size_matches_reuse(cfg_id):
     torch.cuda.synchronize()
     assert float((c - want).norm() / want.norm()) <= 1e-13
     plan.close()
+
+
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_pipelined_host_run_noreuse(cfg_id):
+    """Pipelined host run with reuse=False (product keys: the top level waits
+    for all of A instead of key ranges) equals the device run bit for bit."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 95 + cfg_id)
+    x = random_matrix_device(p, n, 96 + cfg_id)
+    plan = bs.SttsmPlan(m, n, p, ba, bc, reuse=False, pipeline=3)
+    c_dev = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
+    plan.run(a, x, c_dev)
+    torch.cuda.synchronize()
+    a_h, x_h = a.cpu().pin_memory(), x.cpu().pin_memory()
+    c_h = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    plan.run_host(a_h.numpy(), x_h.numpy(), c_h.numpy())
+    assert torch.equal(c_h, c_dev.cpu())
+    plan.close()
