@@ -69,4 +69,8 @@ def test_pipelined_mirrored_plan_matches_reference(path):
     plan.run(a_h.cuda(), x_h.cuda(), c_d)
     torch.cuda.synchronize()
     assert torch.equal(c_d.cpu(), c_h)
+    # pageable host buffers: the same plan falls back to serial copies
+    c_p = np.full(plan.c_elems, np.nan)
+    plan.run_host(np.ascontiguousarray(d["A"]), np.ascontiguousarray(d["X"]), c_p)
+    assert np.array_equal(c_p, c_h.numpy())
     plan.close()
