@@ -113,6 +113,8 @@ int bcss_plan_destroy(bcss_plan* P) {
   for (auto ev : P->grp_ev) cudaEventDestroy(ev);
   for (auto ss : P->lvl_stream) cudaStreamDestroy(ss);
   if (P->cascade_start) cudaEventDestroy(P->cascade_start);
+  for (auto ev : P->bg_ev)
+    if (ev) cudaEventDestroy(ev);
   if (P->copy_in) cudaStreamDestroy(P->copy_in);
   if (P->copy_out) cudaStreamDestroy(P->copy_out);
   if (P->copy_out2) cudaStreamDestroy(P->copy_out2);

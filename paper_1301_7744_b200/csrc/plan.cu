@@ -216,19 +216,29 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
     L.rest = L.bAk * ipow(P.bC, P.m - 1 - k);
     const int sl = P.m - k;  // suffix length of this level's calls
     std::vector<int4> parents;
+    int n_w0_wholes = 0;  // cascade top level: leading parents of first-wave units
     if (k == P.m - 1 && P.start_level == 0) {
       const std::vector<int>& tu = W.top_units;
       for (size_t i = 0; i < tu.size(); ++i) {
         L.suffixes.push_back(tu[i]);
         L.child_call.push_back((int)i);
       }
+      // contiguous runs of units; with the cascade, runs never mix first-wave
+      // and later units, and the first wave's runs come first
+      const bool split_w0 = cascade_wave && P.top_first;
+      auto in_w0 = [&](int u) { return std::find(W.units.begin(), W.units.end(), u) != W.units.end(); };
+      std::vector<int4> later;
       size_t s = 0;
       while (s < tu.size()) {
         size_t e = s + 1;
-        while (e < tu.size() && tu[e] == tu[e - 1] + 1) ++e;
-        parents.push_back(int4{0, (int)(tu[s] * P.bC), (int)((e - s) * P.bC), (int)s});
+        while (e < tu.size() && tu[e] == tu[e - 1] + 1 && (!split_w0 || in_w0(tu[e]) == in_w0(tu[s]))) ++e;
+        const int4 par = int4{0, (int)(tu[s] * P.bC), (int)((e - s) * P.bC), (int)s};
+        if (split_w0 && !in_w0(tu[s])) later.push_back(par);
+        else parents.push_back(par);
         s = e;
       }
+      n_w0_wholes = (int)parents.size();  // without top_first every top row belongs to the first wave
+      parents.insert(parents.end(), later.begin(), later.end());
       L.n_calls = (int64_t)tu.size();
       // the lower levels of this wave start from its own units
       prev_call.assign(W.top_call.begin(), W.top_call.end());
@@ -262,7 +272,8 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
     }
     // group parents into launches by tile configuration
     std::map<int, LaunchHost> by_cfg;
-    for (const int4& whole : parents) {
+    for (size_t wi = 0; wi < parents.size(); ++wi) {
+      const int4& whole = parents[wi];
       // a parent's rows may be split into pieces of different tile shapes; a
       // piece is a parent with a later row0 (its child index follows from
       // child_off + (jb - row0/b_c) in the epilogue)
@@ -291,6 +302,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
           X.item_off.push_back(0);
         }
         X.parents.push_back(par);
+        if ((int)wi < n_w0_wholes) X.n_w0 = (int)X.parents.size();
         X.item_off.push_back(X.item_off.back() +
                              (long long)L.keys_out * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
         X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
@@ -310,11 +322,13 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
         const int64_t k_hi = grouped ? first_rank_with(P.group_a[g + 1], k, P.nbar) : L.keys_out;
         if (grouped) X.group_items.push_back((long long)X.items.size());
         for (size_t pi = 0; pi < X.parents.size(); ++pi) {
+          if (grouped && (int)pi == X.n_w0) X.group_w0.push_back((long long)X.items.size());
           const int mtiles = (X.parents[pi].z + BM - 1) / BM;
           for (int64_t key = k_lo; key < k_hi; ++key)
             for (int nt = 0; nt < X.n_tiles; ++nt)
               for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});
         }
+        if (grouped && X.n_w0 >= (int)X.parents.size()) X.group_w0.push_back((long long)X.items.size());
       }
       if (grouped) X.group_items.push_back((long long)X.items.size());
       L.flops += kv.second.flops;
@@ -384,7 +398,8 @@ int build_plan(bcss_plan& P) {
     // blocks as runs of consecutive ranks) minimizing the last download's end.
     std::vector<std::vector<int>> groups;
     if (P.pipeline_waves > 1 && !P.keep_temps && units.size() > 1) {
-      const double rate_c = 33e12, rate_d = 55e9, rate_h = 55e9, t_copy = 3e-6, t_wave = 20e-6;  // flop/s, B/s, s
+      // flop/s, B/s, B/s, s per D2H copy, s per wave, s per gated sub-launch group (ramp + tail)
+      const double rate_c = 33e12, rate_d = 55e9, rate_h = 55e9, t_copy = 3e-6, t_wave = 20e-6, t_sub = 25e-6;
       const int U = (int)units.size();
       const int W = std::min(P.pipeline_waves, U);
       const double blk_bytes = (double)ipow(P.bC, P.m) * sizeof(double);
@@ -408,39 +423,72 @@ int build_plan(bcss_plan& P) {
       // list-schedule the gated groups (top level of all units; with the
       // cascade also the first wave's levels m-2..1) on one device at rate_c,
       // higher levels first; then the remaining levels.
-      auto first_wave = [&](const std::vector<int>& us, bool cascade) {
+      // cascade: later units' top-level rows of groups >= defer run after the first wave's level 0
+      int defer = G;
+      while (defer > 0 && t_land[P.group_a[defer] - 1] >= 0.85 * t_up) --defer;
+      if (const char* e = getenv("BCSS_DEFER_GROUP")) defer = std::max(0, std::min(G, atoi(e)));
+      auto level_flops = [&](const std::vector<int>& us, int k) {
+        return (double)calls_for(P, us, k) * 2.0 * P.bC * P.n * keys_at(P, k) *
+               (double)(ipow(P.bA, k) * ipow(P.bC, P.m - 1 - k));
+      };
+      // {end of the first wave's compute, time later waves may start}, both
+      // relative to the end of the upload.  One device at rate_c list-schedules
+      // the gated jobs (earliest start; ties to the first wave's chain).
+      auto first_wave = [&](const std::vector<int>& us, bool cascade) -> std::pair<double, double> {
+        std::vector<int> others;
+        for (int u : units)
+          if (std::find(us.begin(), us.end(), u) == us.end()) others.push_back(u);
+        // chain jobs (k, g): cascade - the first wave's rows of levels m-1..1;
+        // non-cascade - the top level of all units.  bg jobs: cascade only.
         const int kmin = cascade ? 1 : P.m - 1;
+        const std::vector<int>& top_rows = cascade ? us : units;
         std::vector<std::vector<double>> done(P.m + 1, std::vector<double>(G, 0.0));
         std::vector<std::vector<bool>> fin(P.m, std::vector<bool>(G, false));
+        std::vector<bool> bg_fin(G, !cascade);
+        for (int g = defer; g < G; ++g) bg_fin[g] = true;  // deferred: after level 0
         double now = 0;
-        for (int left = (P.m - kmin) * G; left > 0; --left) {
-          int bk = -1, bg = -1;
-          double best_ready = 1e300;
+        for (;;) {
+          int bk = -1, bgi = -1;
+          double best = 1e300;
           for (int k = P.m - 1; k >= kmin; --k)
             for (int g = 0; g < G; ++g) {
               if (fin[k][g] || (g > 0 && !fin[k][g - 1])) continue;
-              if (k < P.m - 1 && !fin[k + 1][g]) continue;
+              if (k < P.m - 1 && !fin[k + 1][g]) break;
               const double ready = std::max(k == P.m - 1 ? t_land[P.group_a[g + 1] - 1] : done[k + 1][g],
                                             g > 0 ? done[k][g - 1] : 0.0);
-              // earliest-ready job; ties (already ready) go to the higher level
               const double key = std::max(ready, now);
-              if (key < best_ready - 1e-12) { best_ready = key; bk = k; bg = g; }
-              break;  // only the first unfinished group of each level is a candidate
+              if (key < best - 1e-12) { best = key; bk = k; bgi = g; }
+              break;
             }
-          const std::vector<int>& who = (bk == P.m - 1) ? units : us;
-          now = best_ready + group_flops(who, bk, bg) / rate_c;
-          done[bk][bg] = now;
-          fin[bk][bg] = true;
+          int bb = -1;
+          for (int g = 0; g < G; ++g)
+            if (!bg_fin[g]) {
+              if (fin[P.m - 1][g]) {
+                const double key = std::max(done[P.m - 1][g], now);
+                if (key < best - 1e-12) { best = key; bk = -1; bb = g; }
+              }
+              break;
+            }
+          if (bk < 0 && bb < 0) break;
+          if (bk >= 0) {
+            now = best + group_flops(bk == P.m - 1 ? top_rows : us, bk, bgi) / rate_c + t_sub;
+            done[bk][bgi] = now;
+            fin[bk][bgi] = true;
+          } else {
+            now = best + group_flops(others, P.m - 1, bb) / rate_c + t_sub;
+            bg_fin[bb] = true;
+          }
         }
-        double rest = 0;  // levels not gated: k < kmin (incl. level 0), first wave only
-        for (int k = kmin - 1; k >= 0; --k)
-          rest += (double)calls_for(P, us, k) * 2.0 * P.bC * P.n * keys_at(P, k) *
-                  (double)(ipow(P.bA, k) * ipow(P.bC, P.m - 1 - k));
-        return std::max(now, t_up) - t_up + rest / rate_c + t_wave;
+        double rest = 0;  // the first wave's levels below the gated ones (incl. level 0)
+        for (int k = kmin - 1; k >= 0; --k) rest += level_flops(us, k);
+        const double t1 = std::max(now, t_up) + rest / rate_c;
+        double deferred = 0;
+        if (cascade)
+          for (int g = defer; g < G; ++g) deferred += group_flops(others, P.m - 1, g) + t_sub * rate_c;
+        return {t1 - t_up + t_wave, t1 + deferred / rate_c - t_up + t_wave};
       };
-      std::vector<std::vector<int>> best_groups;
-      double best_t = 1e300;
-      bool best_cascade = false;
+      double mode_best[2] = {1e300, 1e300};
+      std::vector<std::vector<int>> mode_groups[2];
       for (int mode = 0; mode < (cascade_ok ? 2 : 1); ++mode)
         for (int dir = 0; dir < 2; ++dir) {
           std::vector<int> order(units.begin(), units.end());
@@ -461,8 +509,9 @@ int build_plan(bcss_plan& P) {
             return (by[j] - by[i]) / rate_d + copies * t_copy;
           };
           for (int i1 = 1; i1 <= U; ++i1) {
-            const double tc1 = first_wave(std::vector<int>(order.begin(), order.begin() + i1), mode == 1);
-            if (getenv("BCSS_PLAN_DUMP") && atoi(getenv("BCSS_PLAN_DUMP")) > 1)
+            const std::pair<double, double> fw = first_wave(std::vector<int>(order.begin(), order.begin() + i1), mode == 1);
+            const double tc1 = fw.first, tlater = std::max(fw.first, fw.second);
+            if (getenv("BCSS_PLAN_DUMP") && atoi(getenv("BCSS_PLAN_DUMP")) > 2)
               fprintf(stderr, "[bcss plan]   mode %d dir %d first group %d units: compute %.3f ms after upload, d2h %.3f ms\n",
                       mode, dir, i1, tc1 * 1e3, d2h(0, i1) * 1e3);
             // td[g][j]: earliest end of the g-th group's download covering order[0, j)
@@ -474,23 +523,31 @@ int build_plan(bcss_plan& P) {
               for (int j = i1 + 1; j <= U; ++j)
                 for (int i = i1; i < j; ++i) {
                   if (td[g - 1][i] >= 1e299) continue;
-                  const double tc = tc1 + (fl[j] - fl[i1]) / rate_c + (g - 1) * t_wave;  // groups 1..g computed
+                  const double tc = tlater + (fl[j] - fl[i1]) / rate_c + (g - 1) * t_wave;  // groups 1..g computed
                   const double t = std::max(td[g - 1][i], tc) + d2h(i, j);
                   if (t < td[g][j]) { td[g][j] = t; from[g][j] = i; }
                 }
             for (int g = 1; g <= W; ++g) {
-              if (td[g][U] >= best_t - 1e-9) continue;
-              best_t = td[g][U];
-              best_cascade = mode == 1;
-              best_groups.clear();
+              if (td[g][U] >= mode_best[mode] - 1e-9) continue;
+              mode_best[mode] = td[g][U];
+              mode_groups[mode].clear();
               for (int j = U, gg = g; gg > 0; j = from[gg][j], --gg)
-                best_groups.insert(best_groups.begin(), std::vector<int>(order.begin() + from[gg][j], order.begin() + j));
+                mode_groups[mode].insert(mode_groups[mode].begin(),
+                                         std::vector<int>(order.begin() + from[gg][j], order.begin() + j));
             }
           }
         }
-      groups = best_groups;
-      P.cascade = best_cascade;
-      if (cascade_ok && getenv("BCSS_FORCE_CASCADE")) P.cascade = true;  // tests / experiments
+      if (getenv("BCSS_PLAN_DUMP") && atoi(getenv("BCSS_PLAN_DUMP")) > 1)
+        fprintf(stderr, "[bcss plan] model best: level-synchronous %.3f ms, cascade %.3f ms (after the upload)\n",
+                mode_best[0] * 1e3, mode_best[1] * 1e3);
+      // the cascade's model is less certain (many small gated launches): it
+      // must promise a 5 % gain
+      P.cascade = cascade_ok && (mode_best[1] < 0.95 * mode_best[0] || getenv("BCSS_FORCE_CASCADE"));
+      groups = mode_groups[P.cascade ? 1 : 0];
+      const double best_t = mode_best[P.cascade ? 1 : 0];
+      // later units' top-level rows of the key groups whose chunks land in the
+      // last 15 % of the upload run after the first wave's level 0
+      P.defer_group = defer;
       for (auto& g : groups) std::sort(g.begin(), g.end());
       if (getenv("BCSS_PLAN_DUMP")) {
         fprintf(stderr, "[bcss plan] pipeline groups (model: %.3f ms after the upload, cascade %d):", best_t * 1e3,

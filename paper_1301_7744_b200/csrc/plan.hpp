@@ -61,6 +61,10 @@ struct LaunchHost {
   // cascade levels: items are ordered by key group (first key index in
   // [group_a[g], group_a[g+1])) first; group g is items [group_items[g], group_items[g+1])
   std::vector<long long> group_items;
+  // cascade top level: the first n_w0 parents hold the first wave's unit rows;
+  // within group g, items [group_items[g], group_w0[g]) are theirs
+  int n_w0 = 0;
+  std::vector<long long> group_w0;
   size_t off_parents = 0, off_items = 0;  // into the device table buffer
 };
 
@@ -134,6 +138,7 @@ struct bcss_plan {
   bool cascade = false;
   bool cascade_nofit = false;       // the disjoint first-wave regions exceeded the workspace limit
   std::vector<int64_t> group_a;     // first-index boundaries of the key groups
+  int defer_group = 0;              // cascade: top-level rows of later waves in groups >= this run after wave 0
   double* dXm = nullptr;            // X' (device, p x n)
   size_t dXm_bytes = 0;
   int start_level = 0;              // 0 = from A; else compute below caller-provided T(start_level)
@@ -146,6 +151,7 @@ struct bcss_plan {
   std::vector<cudaStream_t> lvl_stream;  // cascade: one stream per level
   std::vector<cudaEvent_t> grp_ev;       // cascade: [k * groups + g] = groups 0..g of level k done
   cudaEvent_t cascade_start = nullptr;
+  cudaEvent_t bg_ev[2] = {nullptr, nullptr};  // cascade: non-deferred top rows of later waves done
   unsigned* d_counters = nullptr;
   size_t counters_n = 0;
   std::vector<cudaStream_t> side;   // concurrent launches of one level

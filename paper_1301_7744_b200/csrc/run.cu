@@ -185,6 +185,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         P->grp_ev.push_back(ev);
       }
       if (!P->cascade_start) CUDA_TRY(cudaEventCreateWithFlags(&P->cascade_start, cudaEventDisableTiming));
+      for (int q = 0; q < 2; ++q)
+        if (!P->bg_ev[q]) CUDA_TRY(cudaEventCreateWithFlags(&P->bg_ev[q], cudaEventDisableTiming));
       CUDA_TRY(cudaEventRecord(P->cascade_start, s));  // tables, X' and counters are ready
       for (const LevelHost& L : W.levels) {
         if (L.k == 0) continue;
@@ -197,16 +199,31 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
             CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g], 0));
             if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g - 1], 0));
           }
+          // top level: the first wave's unit rows first (its lower levels only
+          // read those), the other units' rows after the group's event; their
+          // late groups (>= defer_group) wait until the first wave's level 0
+          const bool top = L.k == P->m - 1;
           for (size_t li = 0; li < L.launches.size(); ++li) {
             const LaunchHost& X = L.launches[li];
-            const long long lo = X.group_items[g], hi = X.group_items[g + 1];
+            const long long lo = X.group_items[g], hi = top ? X.group_w0[g] : X.group_items[g + 1];
             if (hi <= lo) continue;
             if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, P->d_counters + counter_idx++, ls, sms))) return st;
             ++launches;
           }
           if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[L.k * G + g - 1], 0));  // groups <= g done
           CUDA_TRY(cudaEventRecord(P->grp_ev[L.k * G + g], ls));
+          if (top && g < P->defer_group) {
+            for (size_t li = 0; li < L.launches.size(); ++li) {
+              const LaunchHost& X = L.launches[li];
+              const long long lo = X.group_w0[g], hi = X.group_items[g + 1];
+              if (hi <= lo) continue;
+              if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, P->d_counters + counter_idx++, ls, sms))) return st;
+              ++launches;
+            }
+          }
         }
+        if (L.k == P->m - 1)  // the non-deferred rows of later units: done when both streams are
+          for (int q = 0; q < 2; ++q) CUDA_TRY(cudaEventRecord(P->bg_ev[q], P->lvl_stream[2 * L.k + q]));
         trace_mark(pipe, "wave0 level" + std::to_string(L.k) + " done", P->lvl_stream[2 * L.k + ((G - 1) & 1)]);
       }
       CUDA_TRY(cudaStreamWaitEvent(s, P->grp_ev[1 * G + G - 1], 0));
@@ -302,6 +319,21 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
           i = j;
         }
         trace_mark(pipe, "wave" + std::to_string(wi) + " C downloaded", P->copy_out);
+        if (cascade) {
+          // deferred top-level rows of the later waves, then every later wave
+          // may read T(m-1)
+          const LevelHost& T = W.levels.front();
+          const int G = (int)P->group_a.size() - 1;
+          for (int g = P->defer_group; g < G; ++g)
+            for (size_t li = 0; li < T.launches.size(); ++li) {
+              const LaunchHost& X = T.launches[li];
+              const long long lo = X.group_w0[g], hi = X.group_items[g + 1];
+              if (hi <= lo) continue;
+              if ((st = launch_one(P, W, T, X, A, X_, C, lo, hi, P->d_counters + counter_idx++, s, sms))) return st;
+              ++launches;
+            }
+          for (int q = 0; q < 2; ++q) CUDA_TRY(cudaStreamWaitEvent(s, P->bg_ev[q], 0));
+        }
         // submit what is queued so far (the driver otherwise batches it until a sync)
         cudaStreamQuery(s);
         cudaStreamQuery(P->copy_out);
