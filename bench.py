@@ -64,6 +64,9 @@ def parse_args():
                     help="target CPU seconds of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
+                    help="S5 T(m-2) exchange: peer = the owner's kernel stores into the assignee's buffer "
+                         "(CUDA IPC over NVLink), nccl = send/recv, auto = peer if every rank can map it")
     ap.add_argument("--schedule", default="auto", choices=["auto", "s1", "s5"],
                     help="multi-GPU schedule: s1 = top-level subtrees, no exchange; s5 = owners + "
                          "T(m-2) exchange + balanced subtrees (auto: s5 when s1's balance < 0.9)")
@@ -275,7 +278,7 @@ def run_ours(args) -> None:
                 schedule = "s5"
     runner = None
     if schedule == "s5":
-        runner = S5Runner(m, n, p, ba, bc, rank, world, dev, group=None)
+        runner = S5Runner(m, n, p, ba, bc, rank, world, dev, group=None, exchange=args.exchange)
         plans = runner.plans()
         my_flops = runner.flops
         c_elems = runner.c_elems
@@ -447,6 +450,8 @@ def run_ours(args) -> None:
             line["rank0_flop_share"] = round(my_flops / total_flops, 4)
         if runner is not None:
             line["exchange_bytes_rank0"] = runner.exchange_bytes
+            line["exchange"] = ("fused: owner kernel stores into the assignee's buffer (CUDA IPC)"
+                                if runner.exchange == "peer" else "NCCL send/recv")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

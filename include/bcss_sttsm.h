@@ -141,6 +141,21 @@ int bcss_plan_set_pipeline(bcss_plan* plan, int waves);
  * (m-level suffix entries each), reading their T(level) from the run's input
  * buffer (in the given call order) instead of A.  level = m restores a full run. */
 int bcss_plan_set_stop_level(bcss_plan* plan, int stop_level);
+/* Fused exchange for a stop-level plan: the kernel computing T(stop_level)
+ * writes call i (bcss_plan_level_calls order, keys x block doubles) straight
+ * to ptrs[i] - e.g. a slot of another GPU's receive buffer opened with
+ * bcss_ipc_open_handle (NVLink peer stores) - instead of the output buffer;
+ * a NULL entry keeps the default slot.  n must equal the number of stop-level
+ * calls; n = 0 clears the table.  Replaces the owner -> assignee send/recv of
+ * the multi-GPU schedule S5. */
+int bcss_plan_set_call_outputs(bcss_plan* plan, const void* const* ptrs, int64_t n);
+/* Device memory for exchange buffers and its CUDA IPC handle (64 bytes), so
+ * the other ranks' kernels can address it. */
+int bcss_device_alloc(size_t bytes, void** out_ptr);
+int bcss_device_free(void* ptr);
+int bcss_ipc_get_handle(const void* dev_ptr, void* out_handle64);
+int bcss_ipc_open_handle(const void* handle64, void** out_ptr);
+int bcss_ipc_close_handle(void* ptr);
 int bcss_plan_set_start_calls(bcss_plan* plan, int level, const int32_t* suffixes, int n_calls);
 /* Suffixes (m-k entries each) of the plan's level-k calls, in buffer order. */
 int bcss_plan_level_calls(bcss_plan* plan, int k, int32_t* out, int64_t n_max, int64_t* out_n);

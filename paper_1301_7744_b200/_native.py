@@ -54,6 +54,12 @@ SIGNATURES = {
     "bcss_sttsm_run_host": (_c_int, [_vp, _vp, _vp, _vp]),
     "bcss_plan_set_pipeline": (_c_int, [_vp, _c_int]),
     "bcss_plan_set_stop_level": (_c_int, [_vp, _c_int]),
+    "bcss_plan_set_call_outputs": (_c_int, [_vp, _P(_vp), _i64]),
+    "bcss_device_alloc": (_c_int, [_sz, _P(_vp)]),
+    "bcss_device_free": (_c_int, [_vp]),
+    "bcss_ipc_get_handle": (_c_int, [_vp, _vp]),
+    "bcss_ipc_open_handle": (_c_int, [_vp, _P(_vp)]),
+    "bcss_ipc_close_handle": (_c_int, [_vp]),
     "bcss_plan_set_start_calls": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _c_int]),
     "bcss_plan_level_calls": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _i64, _P(_i64)]),
     "bcss_plan_io_elems": (_c_int, [_vp, _P(_i64), _P(_i64)]),

@@ -102,6 +102,7 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->hA) cudaFree(P->hA);
   if (P->hX) cudaFree(P->hX);
   if (P->dXm) cudaFree(P->dXm);
+  if (P->d_call_out) cudaFree(P->d_call_out);
   if (P->hC) cudaFree(P->hC);
   if (P->host_stream) cudaStreamDestroy(P->host_stream);
   for (auto ev : P->events) cudaEventDestroy(ev);
@@ -192,6 +193,65 @@ int bcss_plan_set_stop_level(bcss_plan* P, int stop_level) {
   if (stop_level < 0 || stop_level >= P->m) return fail(BCSS_ERR_RANGE, "stop level %d outside 0..%d", stop_level, P->m - 1);
   P->stop_level = stop_level;
   invalidate(P);
+  return BCSS_OK;
+}
+
+int bcss_plan_set_call_outputs(bcss_plan* P, const void* const* ptrs, int64_t n) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (n == 0) {
+    P->call_out.clear();
+    P->call_out_dirty = true;
+    return BCSS_OK;
+  }
+  if (!ptrs || n < 0) return fail(BCSS_ERR_PARAMETER, "bad pointer table");
+  if (P->stop_level <= 0) return fail(BCSS_ERR_STATE, "call outputs need a stop level > 0");
+  int st = build_plan(*P);
+  if (st) return st;
+  int64_t calls = 0;
+  for (auto& W : P->waves)
+    for (auto& L : W.levels)
+      if (L.k == P->stop_level) calls += L.n_calls;
+  if (n != calls) return fail(BCSS_ERR_SHAPE, "%lld pointers for %lld stop-level calls", (long long)n, (long long)calls);
+  P->call_out.assign(reinterpret_cast<const double* const*>(ptrs), reinterpret_cast<const double* const*>(ptrs) + n);
+  P->call_out_dirty = true;
+  return BCSS_OK;
+}
+
+int bcss_device_alloc(size_t bytes, void** out_ptr) {
+  if (!out_ptr) return fail(BCSS_ERR_PARAMETER, "null output");
+  *out_ptr = nullptr;
+  cudaError_t e = cudaMalloc(out_ptr, std::max<size_t>(bytes, 256));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BCSS_ERR_NOMEM, "cudaMalloc of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  }
+  return BCSS_OK;
+}
+
+int bcss_device_free(void* ptr) {
+  CUDA_TRY(cudaFree(ptr));
+  return BCSS_OK;
+}
+
+int bcss_ipc_get_handle(const void* dev_ptr, void* out_handle64) {
+  if (!dev_ptr || !out_handle64) return fail(BCSS_ERR_PARAMETER, "null argument");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(cudaIpcGetMemHandle(&h, const_cast<void*>(dev_ptr)));
+  static_assert(sizeof(h) == 64, "IPC handle size");
+  memcpy(out_handle64, &h, sizeof(h));
+  return BCSS_OK;
+}
+
+int bcss_ipc_open_handle(const void* handle64, void** out_ptr) {
+  if (!handle64 || !out_ptr) return fail(BCSS_ERR_PARAMETER, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(out_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return BCSS_OK;
+}
+
+int bcss_ipc_close_handle(void* ptr) {
+  CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return BCSS_OK;
 }
 

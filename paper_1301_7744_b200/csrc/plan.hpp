@@ -130,6 +130,10 @@ struct bcss_plan {
   // p̄-1-u of the C blocks below it, whose ranks are then one contiguous range
   // (one D2H per wave).  Level 0 writes each block through the inverse map
   // (block rank of the reversed mirrored tuple, element digits reversed).
+  std::vector<const double*> call_out;  // stop level: per-call destinations (bcss_plan_set_call_outputs)
+  const double** d_call_out = nullptr;   // device copy
+  size_t d_call_out_cap = 0;
+  bool call_out_dirty = false;
   bool mirror = false;
   // Cascade (pipelined host runs): the first wave's levels m-1..1 run as key
   // groups of equal first index; group g of level k needs only A chunks /

@@ -53,6 +53,7 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   a.k = L.k;
   a.rest = (int)L.rest; a.bAk = (int)L.bAk;
   a.n_tiles = X.n_tiles;
+  a.call_out = (P->stop_level > 0 && L.k == P->stop_level && !P->call_out.empty()) ? P->d_call_out : nullptr;
   a.row_mul = L.bAk;
   a.mirror_digits = 0;
   a.lbc = is_pow2(P->bC) ? ilog2(P->bC) : 0;
@@ -114,6 +115,21 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     }
   }
   if ((st = upload_tables(*P, s))) return st;
+  if (P->call_out_dirty) {  // per-call destinations of the stop level
+    if (!P->call_out.empty()) {
+      const size_t nb = P->call_out.size() * sizeof(double*);
+      if (P->d_call_out_cap < nb) {
+        if (P->d_call_out) cudaFree(P->d_call_out);
+        P->d_call_out = nullptr;
+        P->d_call_out_cap = 0;
+        CUDA_TRY(cudaMalloc(&P->d_call_out, nb));
+        P->d_call_out_cap = nb;
+      }
+      CUDA_TRY(cudaMemcpyAsync(P->d_call_out, P->call_out.data(), nb, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    P->call_out_dirty = false;
+  }
   if (P->mirror) {  // the kernels contract X' (row blocks reversed)
     const size_t xb = (size_t)(P->p * P->n) * sizeof(double);
     if (P->dXm_bytes < xb) {

@@ -44,6 +44,7 @@ struct LevelArgs {
   int k;
   int rest, bAk;
   int n_tiles;
+  const double* const* call_out;  // stop level: per-call output slice (e.g. a peer GPU's buffer) or null
   long long row_mul;        // output offset of tile row c: bAk, or b_c^(m-1) (mirrored level 0)
   int mirror_digits;        // mirrored level 0: reverse the m-1 column digits (lbc bits each), else 0
   int lbc;
@@ -187,7 +188,9 @@ struct GenericLevelKernel {
       const int xrow = t.row0 + r;
       const int jb = xrow / a.bC, c = xrow - jb * a.bC;
       const int call = __ldg(a.child_call + t.child_off + (jb - jb0));
-      double* base = a.Tout + ((long long)call * a.keys_out + t.key) * a.blk_out + (long long)a.bAk * c;
+      double* base = (a.call_out && a.call_out[call] ? const_cast<double*>(a.call_out[call])
+                                                     : a.Tout + (long long)call * a.keys_out * a.blk_out) +
+                     (long long)t.key * a.blk_out + (long long)a.bAk * c;
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) {
         const int col = t.nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);

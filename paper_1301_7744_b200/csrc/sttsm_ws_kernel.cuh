@@ -18,6 +18,8 @@
 
 namespace bcss {
 
+constexpr long long kNoRow = (long long)(~0ull >> 1) * -1 - 1;  // padding row (row offsets may be negative)
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
@@ -385,11 +387,16 @@ struct WsLevelKernel {
   // (call*keys_out + K)*blk_out + b_A^k*c (change_of_basis.py:231-235).
   static __device__ __forceinline__ long long row_offset(const LevelArgs& a, const TileInfo& t, int r_local) {
     const int r = t.mt * BM + r_local;
-    if (r >= t.rows) return -1;
+    if (r >= t.rows) return kNoRow;
     const int xrow = t.row0 + r;
     const int jb = xrow / a.bC, c = xrow - jb * a.bC;
     const int call = __ldg(a.child_call + t.child_off + (jb - t.row0 / a.bC));
-    return ((long long)call * a.keys_out + t.key) * a.blk_out + a.row_mul * c;
+    long long base = (long long)call * a.keys_out * a.blk_out;
+    if (a.call_out) {  // per-call destination (a peer GPU's receive slot): offset from Tout in the flat address space
+      const double* dst = a.call_out[call];
+      if (dst) base = (long long)(reinterpret_cast<uintptr_t>(dst) - reinterpret_cast<uintptr_t>(a.Tout)) / 8;
+    }
+    return base + (long long)t.key * a.blk_out + a.row_mul * c;
   }
 
   static __device__ __forceinline__ void epilogue(const LevelArgs& a, const long long (&roff)[FM], int nt, int cw,
@@ -403,7 +410,7 @@ struct WsLevelKernel {
     const long long tstride = (long long)a.bAk * a.bC;
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
-      if (roff[fm] < 0) continue;
+      if (roff[fm] == kNoRow) continue;
       double* base = a.Tout + roff[fm];
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) {
@@ -457,7 +464,7 @@ struct WsLevelKernel {
         asm volatile("bar.sync 1, %0;\n" ::"n"(PT) : "memory");
       }
       TileInfo t = decode_item(a, first, BM);
-      long long my_roff = ptid < BM ? row_offset(a, t, ptid) : -1;  // fetched a tile ahead of use
+      long long my_roff = ptid < BM ? row_offset(a, t, ptid) : kNoRow;  // fetched a tile ahead of use
       int2 nb[G];
       load_nb(a, t, 0, nb);
       const unsigned As_s = (unsigned)__cvta_generic_to_shared(As);

@@ -159,16 +159,67 @@ def _gpu_compute(plan: SttsmPlan, inp, x, out) -> None:
     plan.run(inp, x, out)
 
 
+class DeviceBuffer:
+    """Device memory from the library's own cudaMalloc (so its CUDA IPC handle
+    covers exactly this buffer), viewed as a float64 torch tensor."""
+
+    def __init__(self, elems: int, device):
+        import ctypes
+
+        import torch
+
+        from . import _native
+
+        self._lib = _native.lib()
+        ptr = ctypes.c_void_p()
+        _native.check(self._lib.bcss_device_alloc(ctypes.c_size_t(max(1, elems) * 8), ctypes.byref(ptr)))
+        self.ptr = int(ptr.value)
+        self.__cuda_array_interface__ = {"shape": (max(1, elems),), "typestr": "<f8", "data": (self.ptr, False),
+                                         "version": 3, "strides": None}
+        self.tensor = torch.as_tensor(self, device=device)
+
+    def ipc_handle(self) -> bytes:
+        import ctypes
+
+        from . import _native
+
+        buf = ctypes.create_string_buffer(64)
+        _native.check(self._lib.bcss_ipc_get_handle(ctypes.c_void_p(self.ptr), buf))
+        return buf.raw
+
+    def close(self) -> None:
+        import ctypes
+
+        if getattr(self, "ptr", 0):
+            self.tensor = None
+            self._lib.bcss_device_free(ctypes.c_void_p(self.ptr))
+            self.ptr = 0
+
+
+def open_peer(handle: bytes) -> int:
+    """Device address (valid in this process) of another rank's buffer."""
+    import ctypes
+
+    from . import _native
+
+    out = ctypes.c_void_p()
+    _native.check(_native.lib().bcss_ipc_open_handle(ctypes.create_string_buffer(handle, 64), ctypes.byref(out)))
+    return int(out.value)
+
+
 class S5Runner:
     """One rank's share of the scheme-S5 schedule, with its plans, buffers and
     exchange list built once; ``run`` executes one full step (phase 1,
     T(m-2) exchange, phase 2) asynchronously on the current stream / NCCL."""
 
     def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, rank: int, world: int, device,
-                 reuse: bool = True, group=None, compute=_gpu_compute):
+                 reuse: bool = True, group=None, compute=_gpu_compute, exchange: str = "nccl"):
         import torch
 
         self.m, self.rank, self.world, self.group, self.compute = m, rank, world, group, compute
+        if exchange not in ("nccl", "peer", "auto"):
+            raise ValueError(f"exchange must be 'nccl', 'peer' or 'auto', not {exchange!r}")
+        self.exchange = exchange
         owners, subs = s5_schedule(m, n, p, b_a, b_c, world, reuse)
         self.owners, self.subs = owners, subs
         owner_of = {u: r for r in range(world) for u in owners[r]}
@@ -186,9 +237,55 @@ class S5Runner:
                 pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=owners[r], stop_level=m - 2)
                 order[r] = {c: i for i, c in enumerate(pl.level_calls(m - 2))}
                 pl.close()
-        self.t2 = (torch.empty(self.plan_o.c_elems, dtype=torch.float64, device=device)
-                   if self.plan_o else None)
-        self.inp = torch.empty(max(1, len(subs[rank])) * self.slice, dtype=torch.float64, device=device)
+        self.t2 = None  # owner output buffer (NCCL exchange only; the fused exchange stores to the slots)
+        self._buf, self._peers = None, []
+        if exchange in ("peer", "auto"):
+            # fused exchange: every rank's receive buffer is opened by the others
+            # (CUDA IPC); the owner's level-(m-2) kernel stores each call's
+            # T(m-2) slice straight into its assignee's slot (NVLink peer stores).
+            # "auto" falls back to NCCL send/recv if any rank cannot map a peer.
+            import torch.distributed as dist
+
+            ok, err = True, ""
+            solo = world == 1 or not dist.is_initialized()
+            try:
+                self._buf = DeviceBuffer(max(1, len(subs[rank])) * self.slice, device)
+                handle = None if solo else self._buf.ipc_handle()
+            except Exception as e:  # noqa: BLE001 - reported below / fallback
+                ok, err, handle = False, str(e), None
+            handles = [handle] * world
+            if not solo:
+                dist.all_gather_object(handles, handle, group=group)
+            base = {}
+            if ok and (solo or all(h is not None for h in handles)):
+                try:
+                    for r in range(world):
+                        if r == rank:
+                            base[r] = self._buf.ptr
+                        elif subs[r]:
+                            base[r] = open_peer(handles[r])
+                            self._peers.append(base[r])
+                except Exception as e:  # noqa: BLE001
+                    ok, err = False, str(e)
+            else:
+                ok = False
+            flags = [ok] * world
+            if not solo:
+                dist.all_gather_object(flags, ok, group=group)
+            if all(flags):
+                self.exchange = "peer"
+                self.inp = self._buf.tensor
+                self.dest = self.peer_destinations(subs, rank)
+                if self.plan_o is not None:
+                    self.plan_o.set_call_outputs([base[r] + 8 * self.slice * j for r, j in self.dest])
+            elif exchange == "peer":
+                raise RuntimeError(f"fused peer exchange unavailable on some rank: {err}")
+            else:
+                self.exchange = "nccl"
+        if self.exchange != "peer":
+            self.inp = torch.empty(max(1, len(subs[rank])) * self.slice, dtype=torch.float64, device=device)
+            if self.plan_o is not None:
+                self.t2 = torch.empty(self.plan_o.c_elems, dtype=torch.float64, device=device)
         self.local, self.sends, self.recvs = [], [], []  # (dst slot, src slot) / (peer, slot)
         for r in range(world):
             for j, c in enumerate(subs[r]):
@@ -204,6 +301,14 @@ class S5Runner:
         self.c_elems = full.c_elems
         full.close()
 
+    def peer_destinations(self, subs, rank) -> list[tuple[int, int]]:
+        """(assignee rank, slot) of every call of this rank's owner plan, in the
+        plan's level-(m-2) call order (the fused exchange's pointer table)."""
+        if self.plan_o is None:
+            return []
+        where = {c: (r, j) for r in range(len(subs)) for j, c in enumerate(subs[r])}
+        return [where[tuple(c)] for c in self.plan_o.level_calls(self.m - 2)]
+
     def plans(self):
         return [pl for pl in (self.plan_o, self.plan_s) if pl is not None]
 
@@ -215,6 +320,21 @@ class S5Runner:
         import torch.distributed as dist
 
         s = self.slice
+        if self.exchange == "peer":
+            import torch
+
+            if self.plan_o is not None:  # writes every T(m-2) slice into its assignee's buffer
+                # every call has a destination, so the output buffer is never touched
+                if self.plan_o._ws is None:
+                    self.plan_o.attach_torch_workspace(x.device)
+                self.plan_o.run_ptr(a.data_ptr(), x.data_ptr(), self.inp.data_ptr(),
+                                    torch.cuda.current_stream(x.device).cuda_stream)
+            if self.world > 1:
+                torch.cuda.synchronize()
+                dist.barrier(group=self.group)  # all owners' peer stores have landed
+            if self.plan_s is not None:
+                self.compute(self.plan_s, self.inp, x, c)
+            return
         if self.plan_o is not None:
             self.compute(self.plan_o, a, x, self.t2)
         for j, i in self.local:
@@ -236,12 +356,14 @@ class S5Runner:
 
 
 def sttsm_bcss_s5(a, x, m: int, b_a: int, b_c: int, reuse: bool = True, dst: int | None = 0,
-                  group=None, compute=_gpu_compute):
+                  group=None, compute=_gpu_compute, exchange: str = "nccl"):
     """Scheme-S5 sharded sttsm (one rank per GPU).
 
     Phase 1: owned units down to level m-2 (T(m-2) of their calls into a
     local buffer).  Exchange: each level-(m-2) call's T(m-2) goes from its
-    owner to the rank its subtree was assigned to (NCCL send/recv; local
+    owner to the rank its subtree was assigned to (``exchange="nccl"``: NCCL
+    send/recv; ``"peer"``: fused - the owner's kernel stores the slice straight
+    into the assignee's receive buffer through a CUDA IPC mapping; local
     copies for self).  Phase 2: the assigned subtrees down to C.  With ``dst``
     set, C is gathered there.  ``compute(plan, inp, x, out)`` runs a plan
     (tests substitute a CPU stand-in).
@@ -254,7 +376,8 @@ def sttsm_bcss_s5(a, x, m: int, b_a: int, b_c: int, reuse: bool = True, dst: int
     p, n = x.shape
     if m < 3:
         return sttsm_bcss_distributed(a, x, m, b_a, b_c, reuse=reuse, dst=dst, group=group)
-    runner = S5Runner(m, n, p, b_a, b_c, rank, world, x.device, reuse=reuse, group=group, compute=compute)
+    runner = S5Runner(m, n, p, b_a, b_c, rank, world, x.device, reuse=reuse, group=group, compute=compute,
+                      exchange=exchange)
     c = torch.zeros(runner.c_elems, dtype=x.dtype, device=x.device)
     runner.run(a, x, c)
     if dst is None:

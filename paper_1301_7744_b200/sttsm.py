@@ -120,6 +120,13 @@ class SttsmPlan:
             self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n.value, ctypes.byref(n)))
         return out
 
+    def set_call_outputs(self, ptrs) -> None:
+        """Stop-level plans: write call i's T(stop_level) slice to device
+        address ptrs[i] (0 = the output buffer's slot) - e.g. a peer GPU's
+        receive slot, which fuses the multi-GPU exchange into the kernel."""
+        arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[ctypes.c_void_p(int(q) or None) for q in ptrs])
+        _native.check(_native.lib().bcss_plan_set_call_outputs(self._h, arr, len(ptrs)))
+
     def level_calls(self, k: int) -> list[tuple[int, ...]]:
         """Suffixes of the plan's level-k calls in buffer order."""
         n = ctypes.c_int64()
