@@ -89,7 +89,6 @@ int bcss_plan_create(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int 
   if (!P) return fail(BCSS_ERR_NOMEM, "out of host memory");
   P->m = m; P->n = n; P->p = p; P->bA = b_a; P->bC = b_c;
   P->nbar = n / b_a; P->pbar = p / b_c; P->reuse = reuse != 0;
-  if (const char* e = getenv("BCSS_DYNAMIC_SCHEDULE")) P->dynamic = atoi(e) != 0;
   if (const char* e = getenv("BCSS_SERIAL_LAUNCH")) P->concurrent = atoi(e) == 0;
   *out_plan = P;
   return BCSS_OK;
@@ -120,7 +119,6 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->copy_out) cudaStreamDestroy(P->copy_out);
   if (P->copy_out2) cudaStreamDestroy(P->copy_out2);
   if (P->out2_done) cudaEventDestroy(P->out2_done);
-  if (P->d_counters) cudaFree(P->d_counters);
   delete P;
   return BCSS_OK;
 }

@@ -121,7 +121,6 @@ struct bcss_plan {
   cudaStream_t host_stream = nullptr;
   int64_t last_launches = 0;
   bool timing = false;
-  bool dynamic = false;             // dynamic work queues (kernels use the static stride today)
   bool concurrent = true;           // concurrent launches per level (BCSS_SERIAL_LAUNCH=1 disables)
   int pipeline_waves = 0;           // run_host: overlap H2D / compute / D2H over this many waves
   bool top_first = false;           // first wave computes T(m-1) for all units
@@ -156,8 +155,6 @@ struct bcss_plan {
   std::vector<cudaEvent_t> grp_ev;       // cascade: [k * groups + g] = groups 0..g of level k done
   cudaEvent_t cascade_start = nullptr;
   cudaEvent_t bg_ev[2] = {nullptr, nullptr};  // cascade: non-deferred top rows of later waves done
-  unsigned* d_counters = nullptr;
-  size_t counters_n = 0;
   std::vector<cudaStream_t> side;   // concurrent launches of one level
   std::vector<cudaEvent_t> join;
   cudaEvent_t fork = nullptr;

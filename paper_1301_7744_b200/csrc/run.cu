@@ -26,7 +26,7 @@ void trace_mark(const Pipe* pipe, const std::string& name, cudaStream_t s) {
 }
 
 int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const LaunchHost& X, const double* A,
-               const double* X_, double* C, long long item_lo, long long item_hi, unsigned* counter,
+               const double* X_, double* C, long long item_lo, long long item_hi,
                cudaStream_t ls, int sms) {
   const long long total = item_hi - item_lo;
   if (total <= 0) return BCSS_OK;
@@ -42,7 +42,6 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   a.items = reinterpret_cast<const int4*>(tbl + X.off_items) + item_lo;
   a.child_call = reinterpret_cast<const int*>(tbl + L.off_child);
   a.nbr = reinterpret_cast<const int2*>(tbl + P->nbr_off[L.k]);
-  a.counter = P->dynamic ? counter : nullptr;
   a.total_items = total;
   a.keys_in = L.keys_in; a.keys_out = L.keys_out;
   a.blk_in = L.blk_in; a.blk_out = L.blk_out;
@@ -158,17 +157,6 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
   // Launches of one level (one per tile shape) are independent: they run
   // concurrently on side streams, so one launch's tail overlaps the next
   // launch's CTAs instead of idling SMs.
-  size_t n_launch_total = 0;
-  for (auto& W : P->waves)  // one zeroed queue counter per kernel launch (sub-launches included)
-    for (auto& L : W.levels) n_launch_total += L.launches.size() * 9;
-  if (P->counters_n < n_launch_total) {
-    if (P->d_counters) cudaFree(P->d_counters);
-    P->d_counters = nullptr;
-    CUDA_TRY(cudaMalloc(&P->d_counters, n_launch_total * sizeof(unsigned)));
-    P->counters_n = n_launch_total;
-  }
-  CUDA_TRY(cudaMemsetAsync(P->d_counters, 0, n_launch_total * sizeof(unsigned), s));
-  size_t counter_idx = 0;
   int level_idx = 0;
   const size_t blk_c = (size_t)ipow(P->bC, P->m);
   for (size_t wi = 0; wi < P->waves.size(); ++wi) {
@@ -203,7 +191,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       if (!P->cascade_start) CUDA_TRY(cudaEventCreateWithFlags(&P->cascade_start, cudaEventDisableTiming));
       for (int q = 0; q < 2; ++q)
         if (!P->bg_ev[q]) CUDA_TRY(cudaEventCreateWithFlags(&P->bg_ev[q], cudaEventDisableTiming));
-      CUDA_TRY(cudaEventRecord(P->cascade_start, s));  // tables, X' and counters are ready
+      CUDA_TRY(cudaEventRecord(P->cascade_start, s));  // tables and X' are ready
       for (const LevelHost& L : W.levels) {
         if (L.k == 0) continue;
         for (int q = 0; q < 2; ++q) CUDA_TRY(cudaStreamWaitEvent(P->lvl_stream[2 * L.k + q], P->cascade_start, 0));
@@ -223,7 +211,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
             const LaunchHost& X = L.launches[li];
             const long long lo = X.group_items[g], hi = top ? X.group_w0[g] : X.group_items[g + 1];
             if (hi <= lo) continue;
-            if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, P->d_counters + counter_idx++, ls, sms))) return st;
+            if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, ls, sms))) return st;
             ++launches;
           }
           if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[L.k * G + g - 1], 0));  // groups <= g done
@@ -233,7 +221,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
               const LaunchHost& X = L.launches[li];
               const long long lo = X.group_w0[g], hi = X.group_items[g + 1];
               if (hi <= lo) continue;
-              if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, P->d_counters + counter_idx++, ls, sms))) return st;
+              if ((st = launch_one(P, W, L, X, A, X_, C, lo, hi, ls, sms))) return st;
               ++launches;
             }
           }
@@ -287,8 +275,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
             if (per_key == 0 || k_hi <= k_lo) continue;
             cudaStream_t ls = (sub++ % 2 == 0) ? s : P->side[0];
             CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[a1 - 1], 0));
-            if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, P->d_counters + counter_idx++,
-                                 ls, sms)))
+            if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, ls, sms)))
               return st;
             ++launches;
           }
@@ -298,9 +285,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         for (int li = 0; li < nl; ++li) {
           const LaunchHost& X = L.launches[li];
           cudaStream_t ls = (li == 0 || !conc) ? s : P->side[li - 1];
-          unsigned* counter = P->d_counters + counter_idx++;
           if (X.item_off.back() == 0) continue;
-          if ((st = launch_one(P, W, L, X, A, X_, C, 0, X.item_off.back(), counter, ls, sms))) return st;
+          if ((st = launch_one(P, W, L, X, A, X_, C, 0, X.item_off.back(), ls, sms))) return st;
           ++launches;
         }
       }
@@ -345,7 +331,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
               const LaunchHost& X = T.launches[li];
               const long long lo = X.group_w0[g], hi = X.group_items[g + 1];
               if (hi <= lo) continue;
-              if ((st = launch_one(P, W, T, X, A, X_, C, lo, hi, P->d_counters + counter_idx++, s, sms))) return st;
+              if ((st = launch_one(P, W, T, X, A, X_, C, lo, hi, s, sms))) return st;
               ++launches;
             }
           for (int q = 0; q < 2; ++q) CUDA_TRY(cudaStreamWaitEvent(s, P->bg_ev[q], 0));

@@ -35,7 +35,6 @@ struct LevelArgs {
   const int4* items;        // per work item {parent, key, n-tile, m-tile}
   const int* child_call;    // output call index of (parent child_off + jb - row0/b_c)
   const int2* nbr;          // [keys_out * nbar] {rank in T(k+1) keys, code}
-  unsigned* counter;        // dynamic work queue (zeroed before the launch) or null = static stride
   long long total_items;
   long long keys_in, keys_out, blk_in, blk_out;
   int n_parents;
