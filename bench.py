@@ -401,7 +401,8 @@ def run_ours(args) -> None:
         e2e_s = float(t.item())
         e2e = {"value": round(total_flops * args.steps / e2e_s / 1e9, 3), "unit": "GFLOP/s",
                "h2d_bytes_per_step": int(a_h.numel() * 8 + x_h.numel() * 8),
-               "d2h_bytes_per_step": int(c_h.numel() * 8),
+               "d2h_bytes_per_step": int(8 * (c_h.numel() if runner is not None or world == 1 else
+                                               len(plan.c_block_ranks()) * bc**m)),
                "ms_per_step": round(e2e_s / args.steps * 1e3, 3),
                "api": ("torch H2D of A/X + S5Runner.run + D2H of C, pinned host buffers" if runner is not None
                        else "SttsmPlan.run_host (C ABI bcss_sttsm_run_host), pinned host buffers"),

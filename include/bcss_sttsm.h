@@ -118,7 +118,9 @@ int bcss_sttsm_run(bcss_plan* plan, const double* A_packed, const double* X, dou
 /* Host-buffer run (the reference's call shape): copies A and X to the device,
  * runs, copies C back and synchronizes.  Pinned host memory gives full
  * PCIe bandwidth; pageable memory works too.  With a pipeline set (below) and
- * pinned buffers, the A upload, the compute and the C download overlap. */
+ * pinned buffers, the A upload, the compute and the C download overlap.  A
+ * plan restricted to some units (bcss_plan_set_units) writes only its own C
+ * blocks into C_packed and leaves the others untouched. */
 int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X,
                         double* C_packed);
 

@@ -353,9 +353,27 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
   if (!pipelined) {
     CUDA_TRY(cudaMemcpyAsync(P->hA, A, a_bytes, cudaMemcpyHostToDevice, P->host_stream));
     CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->host_stream));
-    if (P->units_set) CUDA_TRY(cudaMemsetAsync(P->hC, 0, c_bytes, P->host_stream));
     if ((st = run_impl(P, P->hA, P->hX, P->hC, P->host_stream, nullptr))) return st;
-    CUDA_TRY(cudaMemcpyAsync(C, P->hC, c_bytes, cudaMemcpyDeviceToHost, P->host_stream));
+    if (P->units_set && P->stop_level == 0) {
+      // a shard: only this plan's C blocks come back (runs of consecutive
+      // ranks); the caller's other blocks are left as they are
+      std::vector<int> ranks;
+      for (auto& W : P->waves)
+        for (auto& L : W.levels)
+          if (L.k == 0) ranks.insert(ranks.end(), L.child_call.begin(), L.child_call.end());
+      std::sort(ranks.begin(), ranks.end());
+      const size_t blk_c = (size_t)ipow(P->bC, P->m);
+      for (size_t i = 0; i < ranks.size();) {
+        size_t j = i + 1;
+        while (j < ranks.size() && ranks[j] == ranks[j - 1] + 1) ++j;
+        const size_t off = (size_t)ranks[i] * blk_c;
+        CUDA_TRY(cudaMemcpyAsync(C + off, P->hC + off, (j - i) * blk_c * sizeof(double), cudaMemcpyDeviceToHost,
+                                 P->host_stream));
+        i = j;
+      }
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(C, P->hC, c_bytes, cudaMemcpyDeviceToHost, P->host_stream));
+    }
     CUDA_TRY(cudaStreamSynchronize(P->host_stream));
     return BCSS_OK;
   }

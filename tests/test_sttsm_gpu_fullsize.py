@@ -348,3 +348,22 @@ def test_pipelined_host_run_noreuse(cfg_id):
     plan.run_host(a_h.numpy(), x_h.numpy(), c_h.numpy())
     assert torch.equal(c_h, c_dev.cpu())
     plan.close()
+
+
+def test_units_run_host_writes_only_own_blocks():
+    """A shard plan's host run fills exactly its own C blocks (the rest of the
+    caller's buffer is untouched) with the device-path values."""
+    m, n, p, ba, bc = CFG[3]
+    a = random_bcss_device(m, n, ba, 101)
+    x = random_matrix_device(p, n, 102)
+    want = run(CFG[3], a, x).cpu().numpy()
+    plan = bs.SttsmPlan(m, n, p, ba, bc, units=[0, 5, 11])
+    c_h = np.full(plan.c_elems, np.nan)
+    plan.run_host(a.cpu().numpy(), x.cpu().numpy(), c_h)
+    blk = bc**m
+    own = np.zeros(plan.c_elems, dtype=bool)
+    for r in plan.c_block_ranks():
+        own[r * blk:(r + 1) * blk] = True
+    assert np.array_equal(c_h[own], want[own])
+    assert np.isnan(c_h[~own]).all()
+    plan.close()
