@@ -45,10 +45,11 @@ constexpr int N_SHAPES = 10;
 #define BCSS_GEN_SHAPES(X, BA)                                                 \
   X((WsLevelKernel<128, 128, 32, 4, 4, 3, BA, 4, true>), "gen128x128c16")     \
   X((WsLevelKernel<64, 256, 16, 2, 8, 4, BA, 4, true>), "gen64x256c16")       \
-  X((WsLevelKernel<32, 256, 32, 1, 8, 3, BA, 4, true>), "gen32x256c8")
+  X((WsLevelKernel<32, 256, 32, 1, 8, 3, BA, 4, true>), "gen32x256c8")       \
+  X((WsLevelKernel<96, 128, 32, 3, 4, 3, BA, 4, true>), "gen96x128c12")
 
-constexpr int N_GEN = 3;
-constexpr int BCSS_GEN_OF[N_GEN] = {3, 4, 2};
+constexpr int N_GEN = 4;
+constexpr int BCSS_GEN_OF[N_GEN] = {3, 4, 2, 8};
 
 extern const KernelCfg kFast4[N_SHAPES];
 extern const KernelCfg kFast8[N_SHAPES];
