@@ -558,14 +558,31 @@ int build_plan(bcss_plan& P) {
     } else {
       groups.push_back(units);
     }
-    // waves: greedy groups of units whose live temporaries fit the limit
+    // waves: greedy groups of units whose live temporaries fit the limit.  A
+    // pipelined plan keeps T(m-1) of every unit resident (top-first) next to
+    // the wave's lower levels, so that is what must fit.
+    auto al256 = [](size_t v) { return (v + 255) / 256 * 256; };
+    const size_t top_all = al256(level_bytes(P, units)[P.m - 1]);
+    auto lower_bytes = [&](const std::vector<int>& us) -> size_t {
+      const auto b = level_bytes(P, us);
+      size_t r[2] = {0, 0};
+      for (int k = 1; k < P.m - 1; ++k) r[(P.m - 2 - k) % 2] = std::max(r[(P.m - 2 - k) % 2], al256(b[k]));
+      return r[0] + r[1];
+    };
+    bool tf_fits = true;  // every single unit fits next to the resident T(m-1)
+    if (P.ws_limit > 0)
+      for (int u : units) tf_fits = tf_fits && top_all + lower_bytes({u}) <= P.ws_limit;
+    const bool tf_want = P.pipeline_waves > 1 && !P.keep_temps && tf_fits;
+    auto wave_bytes = [&](const std::vector<int>& us) -> size_t {
+      return tf_want ? top_all + lower_bytes(us) : peak_for(P, us);
+    };
     P.waves.clear();
     for (const auto& grp : groups) {
       std::vector<int> cur;
       for (int u : grp) {
         std::vector<int> trial = cur;
         trial.push_back(u);
-        if (!cur.empty() && !P.keep_temps && P.ws_limit > 0 && peak_for(P, trial) > P.ws_limit) {
+        if (!cur.empty() && !P.keep_temps && P.ws_limit > 0 && wave_bytes(trial) > P.ws_limit) {
           P.waves.push_back(WaveHost{cur, {}, {}, {}, {}});
           cur = {u};
         } else {
@@ -576,9 +593,9 @@ int build_plan(bcss_plan& P) {
     }
     if (!P.keep_temps && P.ws_limit > 0) {
       for (auto& W : P.waves)
-        if (peak_for(P, W.units) > P.ws_limit)
+        if (wave_bytes(W.units) > P.ws_limit)
           return fail(BCSS_ERR_NOMEM, "one top-level unit needs %zu workspace bytes > limit %zu",
-                      peak_for(P, W.units), P.ws_limit);
+                      wave_bytes(W.units), P.ws_limit);
     }
     if (P.start_level > 0 || P.stop_level > 0) {
       // partial runs (multi-GPU exchange points): one wave, regions from the built levels
@@ -606,7 +623,7 @@ int build_plan(bcss_plan& P) {
     // Top level: with a pipeline, the first wave computes T(m-1) for every
     // unit (it overlaps the chunked upload of A) and later waves only run the
     // levels below; otherwise every wave computes its own units' top level.
-    P.top_first = P.pipeline_waves > 1 && P.waves.size() > 1 && !P.keep_temps;
+    P.top_first = tf_want && P.waves.size() > 1;
     {
       std::vector<int> all;
       for (auto& W : P.waves) all.insert(all.end(), W.units.begin(), W.units.end());

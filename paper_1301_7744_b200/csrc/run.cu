@@ -144,7 +144,21 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     CUDA_TRY(cudaGetLastError());
     X_ = P->dXm;
   }
-  if ((st = ensure_workspace(*P))) return st;
+  if ((st = ensure_workspace(*P)) == BCSS_ERR_NOMEM && !P->d_ws && !P->keep_temps && P->start_level == 0 &&
+      P->stop_level == 0 && P->ws_bytes > 0) {
+    // the allocation failed although the plan looked like it fit (other
+    // allocations, fragmentation): split into more waves and retry once
+    cudaGetLastError();
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      P->ws_limit = std::min(P->ws_bytes / 2, free_b / 20 * 17);
+      invalidate(P);
+      if ((st = build_plan(*P))) return st;
+      if ((st = upload_tables(*P, s))) return st;
+      st = ensure_workspace(*P);
+    }
+  }
+  if (st) return st;
   int dev, sms;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -305,6 +319,11 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       trace_mark(pipe, "wave" + std::to_string(wi) + " level" + std::to_string(L.k) + " done", s);
       if (pipe && L.k == 0) {
         // this wave's C blocks are final: download them (runs of consecutive ranks)
+        while (P->wave_ev.size() <= wi) {  // the plan may have been rebuilt with more waves
+          cudaEvent_t ev;
+          CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+          P->wave_ev.push_back(ev);
+        }
         CUDA_TRY(cudaEventRecord(P->wave_ev[wi], s));
         CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->wave_ev[wi], 0));
         CUDA_TRY(cudaStreamWaitEvent(P->copy_out2, P->wave_ev[wi], 0));

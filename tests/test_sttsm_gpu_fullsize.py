@@ -367,3 +367,54 @@ def test_units_run_host_writes_only_own_blocks():
     assert np.array_equal(c_h[own], want[own])
     assert np.isnan(c_h[~own]).all()
     plan.close()
+
+
+@pytest.mark.parametrize("cfg", [(3, 1024, 1024, 32, 32), (6, 48, 48, 8, 8), (5, 128, 64, 16, 8),
+                                 (4, 256, 192, 32, 16), (3, 384, 256, 32, 32)])
+def test_beyond_baseline_shapes_checksum(cfg):
+    """Shapes outside the BASELINE list (bigger n, m = 6, b_a != b_c, p != n,
+    non-power-of-two block counts): multilinear checksum on the device path and
+    the pipelined host path."""
+    m, n, p, ba, bc = cfg
+    a = random_bcss_device(m, n, ba, 111)
+    x = random_matrix_device(p, n, 112)
+    c = run(cfg, a, x)
+    v = torch.randn(p, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(9))
+    rhs, rhs_abs = multilinear_form(a, m, n, ba, x.t() @ v)
+    lhs, lhs_abs = multilinear_form(c, m, p, bc, v)
+    assert abs(lhs - rhs) <= 1e-11 * max(lhs_abs, rhs_abs)
+    torch.cuda.empty_cache()
+    plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=4)
+    c_h = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    plan.run_host(a.cpu().pin_memory().numpy(), x.cpu().pin_memory().numpy(), c_h.numpy())
+    assert float((c_h.cuda() - c).norm() / c.norm()) <= 1e-13
+    plan.close()
+
+
+def test_pipelined_host_run_refits_workspace_when_hbm_is_short():
+    """With most of HBM taken, the pipelined host run re-plans its waves to fit
+    the free memory (more waves than modelled) and still returns the same C."""
+    m, n, p, ba, bc = CFG[3]
+    a = random_bcss_device(m, n, ba, 121)
+    x = random_matrix_device(p, n, 122)
+    plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=3)
+    c_dev = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
+    plan.run(a, x, c_dev)
+    torch.cuda.synchronize()
+    want = c_dev.cpu()
+    need = plan.workspace_bytes
+    waves0 = plan.stats()["waves"]
+    plan.close()
+    del c_dev
+    torch.cuda.empty_cache()
+    free, _ = torch.cuda.mem_get_info()
+    # leave room for A/X/C copies plus ~70 % of the workspace
+    keep = 3 * plan.c_elems * 8 + int(0.7 * need)
+    hog = torch.empty(max(0, free - keep) // 8, dtype=torch.float64, device="cuda")
+    plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=3)
+    c_h = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    plan.run_host(a.cpu().pin_memory().numpy(), x.cpu().pin_memory().numpy(), c_h.numpy())
+    assert plan.stats()["waves"] > waves0
+    assert torch.equal(c_h, want)
+    plan.close()
+    del hog
