@@ -120,7 +120,9 @@ int bcss_sttsm_run(bcss_plan* plan, const double* A_packed, const double* X, dou
  * PCIe bandwidth; pageable memory works too.  With a pipeline set (below) and
  * pinned buffers, the A upload, the compute and the C download overlap.  A
  * plan restricted to some units (bcss_plan_set_units) writes only its own C
- * blocks into C_packed and leaves the others untouched. */
+ * blocks into C_packed and leaves the others untouched.  A pipelined plan given
+ * pageable buffers stages them through plan-owned pinned memory (all host
+ * cores) and then runs the pipeline. */
 int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X,
                         double* C_packed);
 

@@ -118,6 +118,8 @@ struct bcss_plan {
   bool own_ws = false;
   double *hA = nullptr, *hX = nullptr, *hC = nullptr;  // device buffers for run_host
   size_t hA_bytes = 0, hX_bytes = 0, hC_bytes = 0;
+  double *pinA = nullptr, *pinX = nullptr, *pinC = nullptr;  // pinned staging for pageable host buffers
+  size_t pinA_bytes = 0, pinX_bytes = 0, pinC_bytes = 0;
   cudaStream_t host_stream = nullptr;
   int64_t last_launches = 0;
   bool timing = false;

@@ -314,7 +314,9 @@ def _cached_plan(m, n, p, b_a, b_c, reuse) -> SttsmPlan:
     key = (m, n, p, b_a, b_c, bool(reuse))
     plan = _PLAN_CACHE.pop(key, None)
     if plan is None:
-        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse)
+        # pipelined: the host run stages the caller's (pageable) arrays through
+        # pinned memory with all host cores and overlaps upload, compute, download
+        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, pipeline=4)
     _PLAN_CACHE[key] = plan
     while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
         _, old = _PLAN_CACHE.popitem(last=False)
@@ -373,7 +375,9 @@ def sttsm_bcss_device(a_packed, x, m: int, b_a: int, b_c: int, out=None, reuse: 
 
     p, n = x.shape
     if plan is None:
-        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse)
+        # pipelined: the host run stages the caller's (pageable) arrays through
+        # pinned memory with all host cores and overlaps upload, compute, download
+        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, pipeline=4)
     if out is None:
         out = torch.empty(plan.c_elems, dtype=torch.float64, device=x.device)
     plan.run(a_packed, x, out, stream=stream)
