@@ -161,3 +161,19 @@ def test_pipelined_plan_writes_every_c_block_once_in_contiguous_waves(cfg, waves
             if hi - lo == i - j:
                 best[i + 1] = min(best[i + 1], best[j] + 1)
     assert best[-1] <= st["waves"]
+
+
+def test_call_output_table_validation():
+    """bcss_plan_set_call_outputs: only for stop-level plans, one pointer per
+    stop-level call (the fused S5 exchange's destination table)."""
+    m, n, p, ba, bc = 4, 64, 64, 16, 16
+    plain = bs.SttsmPlan(m, n, p, ba, bc)
+    with pytest.raises(bs.NativeError):
+        plain.set_call_outputs([0x1000])
+    owner = bs.SttsmPlan(m, n, p, ba, bc, units=[1, 3], stop_level=m - 2)
+    calls = owner.level_calls(m - 2)
+    assert calls and all(c[-1] in (1, 3) for c in calls)
+    with pytest.raises(bs.ShapeError):
+        owner.set_call_outputs([0x1000] * (len(calls) + 1))
+    owner.set_call_outputs([0x1000 + 8 * i for i in range(len(calls))])
+    owner.set_call_outputs([])  # clears the table
