@@ -260,11 +260,18 @@ def run_ours(args) -> None:
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # (ranks beyond the visible GPUs wrap around: a dry run of the multi-rank
+    # path on one GPU uses BCSS_BENCH_BACKEND=gloo, whose ranks never wait on
+    # each other's kernels)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("BCSS_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     m, n, p, ba, bc = CONFIGS[args.config]
     total_flops = bs.bcss_flops(m, n, p, ba, bc)
     schedule = args.schedule
