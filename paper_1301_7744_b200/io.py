@@ -15,7 +15,6 @@ return / accept this package's ``BcssTensor``.
 from __future__ import annotations
 
 import struct
-from pathlib import Path
 
 import numpy as np
 
