@@ -1,0 +1,74 @@
+"""Randomized parity sweep (dev tool): random shapes through every execution
+mode - device run, pipelined host run (mirrored order, cascade when chosen),
+pageable staging, reuse=False, a workspace limit that forces waves - against
+the numpy oracle (rel. Frobenius <= 1e-12).
+
+usage: python tools/fuzz.py [cases] [seed]
+"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+import paper_1301_7744_b200 as bs
+from oracle import bcss_oracle as orc
+
+cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
+rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
+bad = 0
+done = 0
+while done < cases:
+    m = int(rng.integers(2, 7))
+    ba = int(rng.choice([1, 2, 3, 4, 8, 16, 32] if m <= 3 else [1, 2, 4, 8, 16]))
+    bc = int(rng.choice([1, 2, 3, 4, 8, 16] if m <= 4 else [1, 2, 4, 8]))
+    nbar = int(rng.integers(1, {2: 9, 3: 7, 4: 5, 5: 4, 6: 3}[m]))
+    pbar = int(rng.integers(1, {2: 9, 3: 7, 4: 5, 5: 4, 6: 3}[m]))
+    n, p = ba * nbar, bc * pbar
+    if orc.bcss_flops(m, n, p, ba, bc) > 2e9:  # keep the numpy oracle fast
+        continue
+    done += 1
+    a = orc.random_bcss_packed(m, n, ba, int(rng.integers(1 << 30)))
+    x = rng.standard_normal((p, n))
+    want = orc.sttsm_bcss_packed(a, x, m, n, ba, bc)
+    modes = {}
+    plan = bs.SttsmPlan(m, n, p, ba, bc)
+    c = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
+    plan.run(torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), c)
+    torch.cuda.synchronize()
+    modes["device"] = c.cpu().numpy()
+    plan.close()
+    waves = int(rng.integers(2, 5))
+    plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=waves)
+    ch = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    plan.run_host(torch.from_numpy(a).pin_memory().numpy(), torch.from_numpy(x).pin_memory().numpy(), ch.numpy())
+    modes["pipelined"] = ch.numpy().copy()
+    cp = np.full(plan.c_elems, np.nan)
+    plan.run_host(a, x, cp)
+    modes["pageable"] = cp
+    plan.close()
+    plan = bs.SttsmPlan(m, n, p, ba, bc, reuse=False)
+    c = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
+    plan.run(torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), c)
+    torch.cuda.synchronize()
+    modes["noreuse"] = c.cpu().numpy()
+    plan.close()
+    full = bs.SttsmPlan(m, n, p, ba, bc)
+    ws = full.workspace_bytes
+    full.close()
+    if ws > 0 and pbar > 1:
+        try:
+            plan = bs.SttsmPlan(m, n, p, ba, bc, workspace_limit=max(1, ws // 2))
+            c = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
+            plan.run(torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), c)
+            torch.cuda.synchronize()
+            modes["waves"] = c.cpu().numpy()
+            plan.close()
+        except MemoryError:
+            pass  # a single unit does not fit half the workspace
+    for k, v in modes.items():
+        err = orc.rel_frobenius(v, want)
+        if not (err <= 1e-12):
+            bad += 1
+            print(f"MISMATCH {k} m={m} n={n} p={p} ba={ba} bc={bc}: rel {err:.3e}", flush=True)
+print(f"fuzz: {done} cases, {bad} mismatches")
