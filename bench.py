@@ -74,6 +74,8 @@ def parse_args():
                     help="also time the dense mode-product baseline (cuBLAS) when it fits")
     ap.add_argument("--noreuse", action="store_true",
                     help="also time reuse=False (the algorithm-by-blocks without partial-symmetry reuse)")
+    ap.add_argument("--e2e-sync", action="store_true",
+                    help="time e2e as back-to-back synchronous calls instead of the streamed async API")
     ap.add_argument("--pipeline", type=int, default=4,
                     help="waves of the e2e transfer/compute pipeline (0 = serial copies)")
     return ap.parse_args()
@@ -395,12 +397,31 @@ def run_ours(args) -> None:
 
             def e2e_step():
                 plan_e2e.run_host(a_np, x_np, c_np)
+        streamed = plan_e2e is not None and plan_e2e is not plan and not args.e2e_sync
         e2e_step()  # warm: allocates device buffers
+        if streamed:
+            plan_e2e.run_host_async(a_np, x_np, c_np)  # warm the second buffer set
+            plan_e2e.wait()
+        sync_ms = None
+        if streamed:
+            # single-call latency of the same API, for reference
+            t0 = time.perf_counter()
+            for _ in range(max(1, args.steps // 2)):
+                e2e_step()
+            sync_ms = (time.perf_counter() - t0) / max(1, args.steps // 2) * 1e3
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(args.steps):
-            e2e_step()
+        if streamed:
+            # K calls streamed through the asynchronous host API: every call
+            # uploads its A/X and downloads its C; call i+1's upload overlaps
+            # call i's compute and download (PCIe is full duplex)
+            for _ in range(args.steps):
+                plan_e2e.run_host_async(a_np, x_np, c_np)
+            plan_e2e.wait()
+        else:
+            for _ in range(args.steps):
+                e2e_step()
         e2e_s = time.perf_counter() - t0
         t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
         if world > 1:
@@ -412,7 +433,10 @@ def run_ours(args) -> None:
                                                len(plan.c_block_ranks()) * bc**m)),
                "ms_per_step": round(e2e_s / args.steps * 1e3, 3),
                "api": ("torch H2D of A/X + S5Runner.run + D2H of C, pinned host buffers" if runner is not None
+                       else "SttsmPlan.run_host_async x K + wait (C ABI bcss_sttsm_run_host_async), pinned "
+                            "host buffers, consecutive calls overlapped" if streamed
                        else "SttsmPlan.run_host (C ABI bcss_sttsm_run_host), pinned host buffers"),
+               "sync_ms_per_call": round(sync_ms, 3) if sync_ms is not None else None,
                "pipeline_waves": args.pipeline if (plan_e2e is not None and plan_e2e is not plan) else 0}
         if plan_e2e is not None and plan_e2e is not plan:
             plan_e2e.close()

@@ -125,6 +125,14 @@ int bcss_sttsm_run(bcss_plan* plan, const double* A_packed, const double* X, dou
  * cores) and then runs the pipeline. */
 int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X,
                         double* C_packed);
+/* Streaming form of the pipelined host run (pinned buffers, pipeline set):
+ * enqueues upload, compute and download and returns.  Consecutive calls
+ * alternate two device buffer sets, so call i+1's upload overlaps call i's
+ * compute and download (PCIe is full duplex).  The caller keeps A, X, C alive
+ * and unmodified until bcss_plan_wait; C is complete after it. */
+int bcss_sttsm_run_host_async(bcss_plan* plan, const double* A_packed, const double* X,
+                              double* C_packed);
+int bcss_plan_wait(bcss_plan* plan);
 
 /* Overlap host transfers with compute in bcss_sttsm_run_host: A is uploaded
  * in chunks (blocks with first index a) that gate the top-level work (and, when

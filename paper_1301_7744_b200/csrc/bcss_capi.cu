@@ -103,6 +103,13 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->hA) cudaFree(P->hA);
   if (P->hX) cudaFree(P->hX);
   if (P->dXm) cudaFree(P->dXm);
+  if (P->hA1) cudaFree(P->hA1);
+  if (P->hX1) cudaFree(P->hX1);
+  if (P->hC1) cudaFree(P->hC1);
+  for (int q = 0; q < 2; ++q) {
+    if (P->set_compute_done[q]) cudaEventDestroy(P->set_compute_done[q]);
+    if (P->set_d2h_done[q]) cudaEventDestroy(P->set_d2h_done[q]);
+  }
   if (P->pinA) cudaFreeHost(P->pinA);
   if (P->pinX) cudaFreeHost(P->pinX);
   if (P->pinC) cudaFreeHost(P->pinC);
@@ -353,7 +360,7 @@ void par_copy(void* dst, const void* src, size_t bytes) {
 }
 }  // namespace
 
-static int run_host_pinned(bcss_plan* P, const double* A, const double* X, double* C);
+static int run_host_pinned(bcss_plan* P, const double* A, const double* X, double* C, bool async);
 
 int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* C) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
@@ -383,14 +390,31 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
     // chunk-gated staging overlapped with the DMA on this host's 16 cores)
     par_copy(P->pinA, A, a_b);
     memcpy(P->pinX, X, x_b);
-    if ((st = run_host_pinned(P, P->pinA, P->pinX, P->pinC))) return st;
+    if ((st = run_host_pinned(P, P->pinA, P->pinX, P->pinC, false))) return st;
     par_copy(C, P->pinC, c_b);
     return BCSS_OK;
   }
-  return run_host_pinned(P, A, X, C);
+  return run_host_pinned(P, A, X, C, false);
 }
 
-static int run_host_pinned(bcss_plan* P, const double* A, const double* X, double* C) {
+int bcss_sttsm_run_host_async(bcss_plan* P, const double* A, const double* X, double* C) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (!A || !X || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
+  const bool can_pipe = P->pipeline_waves > 0 && !P->units_set && !P->keep_temps && P->start_level == 0 &&
+                        P->stop_level == 0;
+  if (!can_pipe || !is_pinned(A) || !is_pinned(X) || !is_pinned(C))
+    return fail(BCSS_ERR_STATE, "asynchronous host runs need a pipelined full plan and pinned buffers");
+  return run_host_pinned(P, A, X, C, true);
+}
+
+int bcss_plan_wait(bcss_plan* P) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream})
+    if (q) CUDA_TRY(cudaStreamSynchronize(q));
+  return BCSS_OK;
+}
+
+static int run_host_pinned(bcss_plan* P, const double* A, const double* X, double* C, bool async) {
   const size_t blk_a = (size_t)ipow(P->bA, P->m);
   const size_t a_bytes = (size_t)bcss::simplex_count(P->nbar, P->m) * blk_a * sizeof(double);
   const size_t x_bytes = (size_t)(P->p * P->n) * sizeof(double);
@@ -399,7 +423,12 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
     if (cap >= need) return BCSS_OK;
     if (ptr) cudaFree(ptr);
     ptr = nullptr; cap = 0;
-    CUDA_TRY(cudaMalloc(&ptr, need));
+    const cudaError_t e = cudaMalloc(&ptr, need);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ptr = nullptr;
+      return fail(BCSS_ERR_NOMEM, "cudaMalloc of %zu host-run bytes failed: %s", need, cudaGetErrorString(e));
+    }
     cap = need;
     return BCSS_OK;
   };
@@ -440,6 +469,23 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   }
   const auto h0 = std::chrono::steady_clock::now();
   if ((st = build_plan(*P))) return st;
+  // alternate device buffer sets between consecutive calls
+  const int set = (int)(P->host_calls++ & 1);
+  double* dA = P->hA;
+  double* dX = P->hX;
+  double* dC = P->hC;
+  if (set == 1) {
+    if ((st = grow(P->hA1, P->hA1_bytes, a_bytes))) return st;
+    if ((st = grow(P->hX1, P->hX1_bytes, x_bytes))) return st;
+    if ((st = grow(P->hC1, P->hC1_bytes, c_bytes))) return st;
+    dA = P->hA1;
+    dX = P->hX1;
+    dC = P->hC1;
+  }
+  for (int q = 0; q < 2; ++q) {
+    if (!P->set_compute_done[q]) CUDA_TRY(cudaEventCreateWithFlags(&P->set_compute_done[q], cudaEventDisableTiming));
+    if (!P->set_d2h_done[q]) CUDA_TRY(cudaEventCreateWithFlags(&P->set_d2h_done[q], cudaEventDisableTiming));
+  }
   if (!P->copy_in) CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_in, cudaStreamNonBlocking));
   if (!P->copy_out) CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_out, cudaStreamNonBlocking));
   if (!P->copy_out2) CUDA_TRY(cudaStreamCreateWithFlags(&P->copy_out2, cudaStreamNonBlocking));
@@ -454,27 +500,34 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   };
   if ((st = need_events(P->chunk_ev, (size_t)P->nbar))) return st;
   if ((st = need_events(P->wave_ev, P->waves.size()))) return st;
-  // everything below is ordered after work already queued on the host stream
-  CUDA_TRY(cudaEventRecord(P->chunk_ev[0], P->host_stream));
-  CUDA_TRY(cudaStreamWaitEvent(P->copy_in, P->chunk_ev[0], 0));
-  CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->chunk_ev[0], 0));
-  CUDA_TRY(cudaStreamWaitEvent(P->copy_out2, P->chunk_ev[0], 0));
+  // this set's device buffers: the upload waits until the set's previous call
+  // stopped reading A / X, the kernels until its C was downloaded
+  CUDA_TRY(cudaStreamWaitEvent(P->copy_in, P->set_compute_done[set], 0));
+  CUDA_TRY(cudaStreamWaitEvent(P->host_stream, P->set_d2h_done[set], 0));
   Pipe pipe;
   pipe.c_host = C;
   std::vector<std::pair<std::string, cudaEvent_t>> trace;
   const char* tr = getenv("BCSS_TRACE");
   if (tr && atoi(tr) == 1) pipe.trace = &trace;
   trace_mark(&pipe, "upload start", P->copy_in);
-  CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->copy_in));
+  CUDA_TRY(cudaMemcpyAsync(dX, X, x_bytes, cudaMemcpyHostToDevice, P->copy_in));
   for (int64_t a = 0; a < P->nbar; ++a) {
     const size_t r0 = (size_t)first_rank_with(a, P->m, P->nbar), r1 = (size_t)first_rank_with(a + 1, P->m, P->nbar);
-    CUDA_TRY(cudaMemcpyAsync(P->hA + r0 * blk_a, A + r0 * blk_a, (r1 - r0) * blk_a * sizeof(double),
+    CUDA_TRY(cudaMemcpyAsync(dA + r0 * blk_a, A + r0 * blk_a, (r1 - r0) * blk_a * sizeof(double),
                              cudaMemcpyHostToDevice, P->copy_in));
     CUDA_TRY(cudaEventRecord(P->chunk_ev[a], P->copy_in));
     trace_mark(&pipe, "A chunk " + std::to_string(a) + " landed", P->copy_in);
   }
   cudaStreamQuery(P->copy_in);  // kick the driver to submit queued work now
-  if ((st = run_impl(P, P->hA, P->hX, P->hC, P->host_stream, &pipe))) return st;
+  if ((st = run_impl(P, dA, dX, dC, P->host_stream, &pipe))) return st;
+  CUDA_TRY(cudaEventRecord(P->set_compute_done[set], P->host_stream));
+  CUDA_TRY(cudaEventRecord(P->out2_done, P->copy_out2));
+  CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->out2_done, 0));
+  CUDA_TRY(cudaEventRecord(P->set_d2h_done[set], P->copy_out));
+  if (async) {
+    cudaStreamQuery(P->host_stream);  // submit
+    return BCSS_OK;
+  }
   if (pipe.trace) {
     fprintf(stderr, "[bcss trace] host enqueue took %.3f ms\n",
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count());

@@ -118,6 +118,13 @@ struct bcss_plan {
   bool own_ws = false;
   double *hA = nullptr, *hX = nullptr, *hC = nullptr;  // device buffers for run_host
   size_t hA_bytes = 0, hX_bytes = 0, hC_bytes = 0;
+  // second device buffer set of pipelined host runs: consecutive calls
+  // alternate sets so call i+1 uploads while call i computes / downloads
+  double *hA1 = nullptr, *hX1 = nullptr, *hC1 = nullptr;
+  size_t hA1_bytes = 0, hX1_bytes = 0, hC1_bytes = 0;
+  cudaEvent_t set_compute_done[2] = {nullptr, nullptr};  // kernels of the set's last call finished
+  cudaEvent_t set_d2h_done[2] = {nullptr, nullptr};      // downloads of the set's last call finished
+  uint64_t host_calls = 0;
   double *pinA = nullptr, *pinX = nullptr, *pinC = nullptr;  // pinned staging for pageable host buffers
   size_t pinA_bytes = 0, pinX_bytes = 0, pinC_bytes = 0;
   cudaStream_t host_stream = nullptr;

@@ -32,6 +32,23 @@ from .storage import BcssTensor, PartialSymTensor, packed_payload
 TempHook = Callable[[int, object], None]
 
 
+def _retry_after_torch_cache(call):
+    """The library allocates with cudaMalloc, which cannot use memory torch's
+    caching allocator holds: on an out-of-memory status release torch's cache
+    once and retry."""
+    try:
+        return call()
+    except MemoryError:
+        import sys
+
+        torch = sys.modules.get("torch")
+        if torch is None or not torch.cuda.is_available():
+            raise
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        return call()
+
+
 class SttsmPlan:
     """A validated problem plus its level/work-list tables and workspace.
 
@@ -197,9 +214,26 @@ class SttsmPlan:
                                ("C", c, self.c_elems)):
             if t.dtype != np.float64 or not t.flags.c_contiguous or t.size != numel:
                 raise ShapeError(f"{name} must be a contiguous float64 array of {numel} elements")
-        _native.check(_native.lib().bcss_sttsm_run_host(
+        _retry_after_torch_cache(lambda: _native.check(_native.lib().bcss_sttsm_run_host(
             self._h, ctypes.c_void_p(a.ctypes.data), ctypes.c_void_p(x.ctypes.data),
-            ctypes.c_void_p(c.ctypes.data)))
+            ctypes.c_void_p(c.ctypes.data))))
+
+    def run_host_async(self, a: np.ndarray, x: np.ndarray, c: np.ndarray) -> None:
+        """Streaming host run (pipelined plan, pinned buffers): returns after
+        enqueueing; consecutive calls overlap (the next upload runs while this
+        call computes and downloads).  Keep the buffers alive and unchanged
+        until ``wait()``; ``c`` is complete after it."""
+        for name, t, numel in (("A", a, self.a_elems), ("X", x, self.p * self.n),
+                               ("C", c, self.c_elems)):
+            if t.dtype != np.float64 or not t.flags.c_contiguous or t.size != numel:
+                raise ShapeError(f"{name} must be a contiguous float64 array of {numel} elements")
+        _retry_after_torch_cache(lambda: _native.check(_native.lib().bcss_sttsm_run_host_async(
+            self._h, ctypes.c_void_p(a.ctypes.data), ctypes.c_void_p(x.ctypes.data),
+            ctypes.c_void_p(c.ctypes.data))))
+
+    def wait(self) -> None:
+        """Wait for every host run enqueued on this plan."""
+        _native.check(_native.lib().bcss_plan_wait(self._h))
 
     def temp(self, k: int, suffix) -> np.ndarray:
         """Host copy of the kept temporary T(k) of call ``suffix`` (keep_temps)."""

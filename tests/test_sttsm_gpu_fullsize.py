@@ -418,3 +418,27 @@ def test_pipelined_host_run_refits_workspace_when_hbm_is_short():
     assert torch.equal(c_h, want)
     plan.close()
     del hog
+
+
+@pytest.mark.parametrize("cfg_id", [2, 4])
+def test_async_host_runs_overlap_and_stay_correct(cfg_id):
+    """Three streamed host runs with different inputs in flight at once (the
+    plan alternates two device buffer sets): every C equals its synchronous
+    result bit for bit."""
+    m, n, p, ba, bc = CFG[cfg_id]
+    plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=3)
+    ins, want = [], []
+    for s in range(3):
+        a = random_bcss_device(m, n, ba, 131 + s).cpu().pin_memory()
+        x = random_matrix_device(p, n, 141 + s).cpu().pin_memory()
+        c = torch.empty(plan.c_elems, dtype=torch.float64).pin_memory()
+        plan.run_host(a.numpy(), x.numpy(), c.numpy())
+        ins.append((a, x))
+        want.append(c.clone())
+    outs = [torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory() for _ in range(3)]
+    for (a, x), c in zip(ins, outs):
+        plan.run_host_async(a.numpy(), x.numpy(), c.numpy())
+    plan.wait()
+    for c, w in zip(outs, want):
+        assert torch.equal(c, w)
+    plan.close()
