@@ -227,12 +227,17 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       // and later units, and the first wave's runs come first
       const bool split_w0 = cascade_wave && P.top_first;
       auto in_w0 = [&](int u) { return std::find(W.units.begin(), W.units.end(), u) != W.units.end(); };
+      // X row block of unit u: u itself, or its position in the gathered X_top
+      auto pos = [&](int u) {
+        if (P.top_rows.empty()) return u;
+        return (int)(std::lower_bound(P.top_rows.begin(), P.top_rows.end(), u) - P.top_rows.begin());
+      };
       std::vector<int4> later;
       size_t s = 0;
       while (s < tu.size()) {
         size_t e = s + 1;
-        while (e < tu.size() && tu[e] == tu[e - 1] + 1 && (!split_w0 || in_w0(tu[e]) == in_w0(tu[s]))) ++e;
-        const int4 par = int4{0, (int)(tu[s] * P.bC), (int)((e - s) * P.bC), (int)s};
+        while (e < tu.size() && pos(tu[e]) == pos(tu[e - 1]) + 1 && (!split_w0 || in_w0(tu[e]) == in_w0(tu[s]))) ++e;
+        const int4 par = int4{0, (int)(pos(tu[s]) * P.bC), (int)((e - s) * P.bC), (int)s};
         if (split_w0 && !in_w0(tu[s])) later.push_back(par);
         else parents.push_back(par);
         s = e;
@@ -390,6 +395,11 @@ int build_plan(bcss_plan& P) {
       for (int u = 0; u < P.pbar; ++u) units.push_back(u);
     std::sort(units.begin(), units.end());
     units.erase(std::unique(units.begin(), units.end()), units.end());
+    // shard plans with scattered units: the top level reads gathered X rows
+    P.top_rows.clear();
+    if (P.units_set && !P.mirror && P.start_level == 0 && units.size() > 1 &&
+        units.back() - units.front() + 1 != (int)units.size() && !getenv("BCSS_NO_TOP_GATHER"))
+      P.top_rows = units;
     // pipeline groups: run_host computes T(m-1) of every unit first (it
     // overlaps the upload of A), then the groups' lower levels one after the
     // other while the previous group's C blocks download.  Contiguous groups
@@ -700,6 +710,7 @@ int build_plan(bcss_plan& P) {
         if (L.k == 0) P.c_blocks += L.n_calls;
       }
     }
+    P.off_top_rows = take(P.top_rows.size() * sizeof(int));
     P.tables_bytes = off;
     P.built = true;
     return BCSS_OK;
@@ -728,6 +739,7 @@ int upload_tables(bcss_plan& P, cudaStream_t stream) {
       }
       memcpy(&host[L.off_child], L.child_call.data(), L.child_call.size() * sizeof(int));
     }
+  if (!P.top_rows.empty()) memcpy(&host[P.off_top_rows], P.top_rows.data(), P.top_rows.size() * sizeof(int));
   CUDA_TRY(cudaMalloc(&P.d_tables, std::max<size_t>(P.tables_bytes, 256)));
   CUDA_TRY(cudaMemcpyAsync(P.d_tables, host.data(), P.tables_bytes, cudaMemcpyHostToDevice, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));

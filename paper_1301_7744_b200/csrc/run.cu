@@ -34,7 +34,8 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   char* tbl = static_cast<char*>(P->d_tables);
   bcss::LevelArgs a;
   memset(&a, 0, sizeof(a));
-  a.X = X_;
+  const bool top = P->start_level == 0 && L.k == P->m - 1;
+  a.X = (top && !P->top_rows.empty()) ? P->dXt : X_;
   const bool from_input = (P->start_level == 0 && L.k == P->m - 1) || (P->start_level > 0 && L.k == P->start_level - 1);
   a.Tin = from_input ? A : region_for(*P, W, L.k + 1);
   a.Tout = (L.k == P->stop_level) ? C : region_for(*P, W, L.k);
@@ -77,6 +78,17 @@ __global__ void reverse_row_blocks(const double* __restrict__ src, double* __res
     const long long r = i / n, c = i - r * n;
     const long long pbar = p / bc, jb = r / bc;
     dst[i] = src[((pbar - 1 - jb) * bc + (r - jb * bc)) * n + c];
+  }
+}
+
+// X_top for shard plans: row block i of dst is row block rows[i] of src
+__global__ void gather_row_blocks(const double* __restrict__ src, double* __restrict__ dst,
+                                  const int* __restrict__ rows, long long nblk, long long n, long long bc) {
+  const long long per = bc * n;  // doubles per row block (contiguous in both)
+  const long long total = nblk * per;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long b = i / per;
+    dst[i] = src[(long long)__ldg(rows + b) * per + (i - b * per)];
   }
 }
 
@@ -143,6 +155,20 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     reverse_row_blocks<<<296, 256, 0, s>>>(X_, P->dXm, P->p, P->n, P->bC);
     CUDA_TRY(cudaGetLastError());
     X_ = P->dXm;
+  }
+  if (!P->top_rows.empty()) {  // gathered top-level X rows (shard plans)
+    const size_t xb = P->top_rows.size() * (size_t)(P->bC * P->n) * sizeof(double);
+    if (P->dXt_bytes < xb) {
+      if (P->dXt) cudaFree(P->dXt);
+      P->dXt = nullptr;
+      P->dXt_bytes = 0;
+      CUDA_TRY(cudaMalloc(&P->dXt, xb));
+      P->dXt_bytes = xb;
+    }
+    if (pipe) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev[0], 0));  // X was uploaded ahead of A chunk 0
+    const int* rows = reinterpret_cast<const int*>(static_cast<char*>(P->d_tables) + P->off_top_rows);
+    gather_row_blocks<<<296, 256, 0, s>>>(X_, P->dXt, rows, (long long)P->top_rows.size(), P->n, P->bC);
+    CUDA_TRY(cudaGetLastError());
   }
   if ((st = ensure_workspace(*P)) == BCSS_ERR_NOMEM && !P->d_ws && !P->keep_temps && P->start_level == 0 &&
       P->stop_level == 0 && P->ws_bytes > 0) {
