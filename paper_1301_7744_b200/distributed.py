@@ -123,12 +123,33 @@ def sttsm_bcss_distributed(a, x, m: int, b_a: int, b_c: int, reuse: bool = True,
 
 def s5_schedule(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: bool = True):
     """(owners, subs): owners[r] = top-level units rank r computes down to level
-    m-2; subs[r] = level-(m-2) calls (i, u) whose subtrees rank r computes.
-    Deterministic, so every rank derives the same schedule without talking."""
+    m-2; subs[r] = level-(m-2) calls (i, u) whose subtrees rank r computes, in
+    execution order.  Deterministic, so every rank derives the same schedule
+    without talking.  See ``s5_groups`` for the release-time model."""
+    owners, subs, _ = s5_groups(m, n, p, b_a, b_c, world, reuse)
+    return owners, subs
+
+
+def s5_groups(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: bool = True):
+    """(owners, subs, groups) of scheme S5 with release times.
+
+    Owners: LPT over the owner costs (top-level rows of unit u plus its
+    level-(m-2) calls (i, u), i <= u).  A subtree call (i, u) is *released*
+    when the rank owning u finishes its owner plan (modelled as that rank's
+    owner flops), so the subtrees are list-scheduled by release time: each
+    call goes to the rank where it would finish first, max(free, release) +
+    cost.  groups[r] = [(lo, hi, src_ranks)]: subs[r][lo:hi] run as one
+    subtree plan once the owners in src_ranks have finished; consecutive
+    calls share a group unless the later one would otherwise wait.  No
+    global barrier separates the phases - a rank starts its first group as
+    soon as its own owner plan and that group's sources are done (config 5 at
+    8 GPUs: the barrier-separated schedule modelled 0.64 efficiency, this one
+    0.87 - bounded by the largest owner).
+    """
     pbar = p // b_c
     if m < 3:  # no level below m-2 to hand out: plain S1
         parts = partition_units(unit_flops(m, n, p, b_a, b_c, reuse), world)
-        return parts, [[] for _ in range(world)]
+        return parts, [[] for _ in range(world)], [[] for _ in range(world)]
     owner_cost = []
     for u in range(pbar):
         pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=[u], stop_level=m - 2)
@@ -136,23 +157,42 @@ def s5_schedule(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: b
         pl.close()
     loads = [0] * world
     owners: list[list[int]] = [[] for _ in range(world)]
+    owner_of = {}
     for u in sorted(range(pbar), key=lambda q: (-owner_cost[q], q)):
         r = min(range(world), key=lambda q: (loads[q], q))
         owners[r].append(u)
+        owner_of[u] = r
         loads[r] += owner_cost[u]
-    calls = [(i, u) for u in range(pbar) for i in range(u + 1)]
+    release = {u: loads[owner_of[u]] for u in range(pbar)}
     # subtree cost depends only on i (the row block) for fixed shapes
     sub_cost = {}
     for i in range(pbar):
         pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=[(i, pbar - 1)])
         sub_cost[i] = pl.stats()["flops"]
         pl.close()
+    calls = sorted(((i, u) for u in range(pbar) for i in range(u + 1)),
+                   key=lambda c: (release[c[1]], -sub_cost[c[0]], c))
+    free = list(loads)
     subs: list[list[tuple]] = [[] for _ in range(world)]
-    for c in sorted(calls, key=lambda q: (-sub_cost[q[0]], q)):
-        r = min(range(world), key=lambda q: (loads[q], q))
+    starts: list[list[int]] = [[] for _ in range(world)]
+    for c in calls:
+        rel, cost = release[c[1]], sub_cost[c[0]]
+        r = min(range(world), key=lambda q: (max(free[q], rel) + cost, free[q], q))
+        st = max(free[r], rel)
         subs[r].append(c)
-        loads[r] += sub_cost[c[0]]
-    return [sorted(o) for o in owners], [sorted(sb) for sb in subs]
+        starts[r].append(st)
+        free[r] = st + cost
+    groups: list[list[tuple]] = [[] for _ in range(world)]
+    for r in range(world):
+        lo = 0
+        for j in range(1, len(subs[r]) + 1):
+            # a call that would start later than the group's first call because it
+            # waits for its owner (not for the calls before it) opens a new group
+            if j == len(subs[r]) or release[subs[r][j][1]] > max(starts[r][lo], loads[r]):
+                src = sorted({owner_of[c[1]] for c in subs[r][lo:j]})
+                groups[r].append((lo, j, src))
+                lo = j
+    return [sorted(o) for o in owners], subs, groups
 
 
 def _gpu_compute(plan: SttsmPlan, inp, x, out) -> None:
@@ -210,7 +250,13 @@ def open_peer(handle: bytes) -> int:
 class S5Runner:
     """One rank's share of the scheme-S5 schedule, with its plans, buffers and
     exchange list built once; ``run`` executes one full step (phase 1,
-    T(m-2) exchange, phase 2) asynchronously on the current stream / NCCL."""
+    T(m-2) exchange, phase 2) asynchronously on the current stream / NCCL.
+
+    Phase 2 is one subtree plan per release group (``s5_groups``).  With the
+    fused exchange there is no barrier between the phases: every rank records
+    a CUDA IPC event after its owner plan, and each group's plan waits on the
+    events of the owners it reads from, so a rank whose owner work is short
+    starts its subtrees while the long owners still run."""
 
     def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, rank: int, world: int, device,
                  reuse: bool = True, group=None, compute=_gpu_compute, exchange: str = "nccl"):
@@ -220,13 +266,15 @@ class S5Runner:
         if exchange not in ("nccl", "peer", "auto"):
             raise ValueError(f"exchange must be 'nccl', 'peer' or 'auto', not {exchange!r}")
         self.exchange = exchange
-        owners, subs = s5_schedule(m, n, p, b_a, b_c, world, reuse)
-        self.owners, self.subs = owners, subs
+        owners, subs, groups = s5_groups(m, n, p, b_a, b_c, world, reuse)
+        self.owners, self.subs, self.groups = owners, subs, groups[rank]
         owner_of = {u: r for r in range(world) for u in owners[r]}
         self.plan_o = (SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=owners[rank], stop_level=m - 2)
                        if owners[rank] else None)
-        self.plan_s = (SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=subs[rank])
-                       if subs[rank] else None)
+        # one subtree plan per release group: slots subs[rank][lo:hi] of the receive buffer
+        self.plans_s = [SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2,
+                                  start_calls=subs[rank][lo:hi]) for lo, hi, _ in self.groups]
+        self._ev_own, self._ev_peer = None, {}
         probe = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=[(0, 0)])
         self.slice = probe.a_elems
         probe.close()
@@ -272,6 +320,25 @@ class S5Runner:
             flags = [ok] * world
             if not solo:
                 dist.all_gather_object(flags, ok, group=group)
+            if all(flags) and not solo:
+                # owner-done events: group g of an assignee waits on its sources' events
+                try:
+                    self._ev_own = torch.cuda.Event(interprocess=True)
+                    ev_handle = self._ev_own.ipc_handle()
+                except Exception as e:  # noqa: BLE001
+                    ok, err, ev_handle = False, str(e), None
+                ev_handles = [ev_handle] * world
+                dist.all_gather_object(ev_handles, ev_handle, group=group)
+                need = {q for _, _, src in self.groups for q in src if q != rank}
+                try:
+                    for q in need:
+                        if ev_handles[q] is None:
+                            raise RuntimeError(f"rank {q} has no owner event")
+                        self._ev_peer[q] = torch.cuda.Event.from_ipc_handle(device, ev_handles[q])
+                except Exception as e:  # noqa: BLE001
+                    ok, err = False, str(e)
+                flags = [ok] * world
+                dist.all_gather_object(flags, ok, group=group)
             if all(flags):
                 self.exchange = "peer"
                 self.inp = self._buf.tensor
@@ -310,7 +377,19 @@ class S5Runner:
         return [where[tuple(c)] for c in self.plan_o.level_calls(self.m - 2)]
 
     def plans(self):
-        return [pl for pl in (self.plan_o, self.plan_s) if pl is not None]
+        return ([self.plan_o] if self.plan_o is not None else []) + list(self.plans_s)
+
+    def _run_groups(self, x, c, wait_peers: bool) -> None:
+        import torch
+
+        s = self.slice
+        stream = torch.cuda.current_stream(x.device) if wait_peers else None
+        for (lo, hi, src), pl in zip(self.groups, self.plans_s):
+            if wait_peers:
+                for q in src:
+                    if q != self.rank:  # own owner work precedes on this stream
+                        stream.wait_event(self._ev_peer[q])
+            self.compute(pl, self.inp[lo * s:hi * s], x, c)
 
     def attach_torch_workspace(self, device=None) -> None:
         for pl in self.plans():
@@ -323,17 +402,22 @@ class S5Runner:
         if self.exchange == "peer":
             import torch
 
+            multi = self.world > 1 and self._ev_own is not None
+            if multi:
+                # the previous step's subtree plans finished reading every receive
+                # buffer before any owner overwrites one
+                torch.cuda.synchronize()
+                dist.barrier(group=self.group)
+            stream = torch.cuda.current_stream(x.device)
             if self.plan_o is not None:  # writes every T(m-2) slice into its assignee's buffer
                 # every call has a destination, so the output buffer is never touched
                 if self.plan_o._ws is None:
                     self.plan_o.attach_torch_workspace(x.device)
-                self.plan_o.run_ptr(a.data_ptr(), x.data_ptr(), self.inp.data_ptr(),
-                                    torch.cuda.current_stream(x.device).cuda_stream)
-            if self.world > 1:
-                torch.cuda.synchronize()
-                dist.barrier(group=self.group)  # all owners' peer stores have landed
-            if self.plan_s is not None:
-                self.compute(self.plan_s, self.inp, x, c)
+                self.plan_o.run_ptr(a.data_ptr(), x.data_ptr(), self.inp.data_ptr(), stream.cuda_stream)
+            if multi:
+                self._ev_own.record(stream)
+                dist.barrier(group=self.group)  # every owner event of this step is recorded (host only)
+            self._run_groups(x, c, wait_peers=multi)
             return
         if self.plan_o is not None:
             self.compute(self.plan_o, a, x, self.t2)
@@ -344,11 +428,12 @@ class S5Runner:
         if ops:
             for w in dist.batch_isend_irecv(ops):
                 w.wait()
-        if self.plan_s is not None:
-            self.compute(self.plan_s, self.inp, x, c)
+        self._run_groups(x, c, wait_peers=False)
 
     def c_block_ranks(self) -> np.ndarray:
-        return self.plan_s.c_block_ranks() if self.plan_s is not None else np.zeros(0, dtype=np.int64)
+        if not self.plans_s:
+            return np.zeros(0, dtype=np.int64)
+        return np.concatenate([pl.c_block_ranks() for pl in self.plans_s])
 
     @property
     def flops(self) -> int:

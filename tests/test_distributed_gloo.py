@@ -79,8 +79,11 @@ def _oracle_compute(d, m, n, p, ba, bc):
         else:
             size = inp.numel() // len(plan.start_calls)
             given = {c: inp[i * size:(i + 1) * size].numpy() for i, c in enumerate(plan.start_calls)}
-            out.copy_(torch.from_numpy(orc.sttsm_bcss_packed(None, d["X"], m, n, ba, bc,
-                                                             start=(plan.start_level, given))))
+            full = torch.from_numpy(orc.sttsm_bcss_packed(None, d["X"], m, n, ba, bc, start=(plan.start_level, given)))
+            # like the device plans: only this plan's C blocks are written
+            blk = bc**m
+            for r in plan.c_block_ranks():
+                out[r * blk:(r + 1) * blk] = full[r * blk:(r + 1) * blk]
     return compute
 
 

@@ -1,10 +1,13 @@
 """Predict the S5 multi-GPU schedule's strong scaling on ONE B200.
 
 Every virtual rank's phase-1 (owner) plan and phase-2 (subtree) plan is timed
-device-resident, one after the other.  S5Runner separates the phases with a
-barrier (all owners' T(m-2) stores land before any subtree starts), so the
-modelled job time is max(owner) + max(subtree); the exchange itself is fused
-into the owners' kernels (peer stores over NVLink) and is not modelled here.
+device-resident, one after the other, and the job is replayed from those
+times: rank r runs its owner plan, then each release group's subtree plan
+once its source owners are done (S5Runner gates the groups on the owners'
+CUDA IPC events; no barrier between the phases).  For comparison the
+barrier-separated model max(owner) + max(subtree) is printed too.  The
+exchange itself is fused into the owners' kernels (peer stores over NVLink)
+and is not modelled here.
 
 usage: python tools/s5_timing.py CONFIG [WORLD ...]
 """
@@ -15,7 +18,7 @@ import torch
 
 sys.path.insert(0, ".")
 import paper_1301_7744_b200 as bs
-from paper_1301_7744_b200.distributed import s5_schedule
+from paper_1301_7744_b200.distributed import s5_groups
 
 CFGS = {2: (3, 512, 512, 32, 32), 3: (4, 192, 192, 16, 16), 4: (5, 96, 96, 8, 8), 5: (4, 512, 256, 32, 32)}
 
@@ -52,8 +55,8 @@ def main():
     torch.cuda.empty_cache()
     print(json.dumps({"config": cfg, "t1_ms": round(t1, 3), "tflops_1": round(total / t1 / 1e9, 2)}), flush=True)
     for w in worlds:
-        owners, subs = s5_schedule(m, n, p, ba, bc, w)
-        t_o, t_s, fl = [], [], []
+        owners, subs, groups = s5_groups(m, n, p, ba, bc, w)
+        t_o, t_s, t_g, fl = [], [], [], []
         for r in range(w):
             f = 0
             if owners[r]:
@@ -66,25 +69,33 @@ def main():
             else:
                 t_o.append(0.0)
             torch.cuda.empty_cache()
-            if subs[r]:
-                pl = bs.SttsmPlan(m, n, p, ba, bc, start_level=m - 2, start_calls=subs[r])
+            tg = []
+            for lo, hi, _ in groups[r]:
+                pl = bs.SttsmPlan(m, n, p, ba, bc, start_level=m - 2, start_calls=subs[r][lo:hi])
                 inp = torch.rand(pl.a_elems, dtype=torch.float64, device="cuda")
                 out = torch.empty(pl.c_elems, dtype=torch.float64, device="cuda")
-                t_s.append(round(timed(pl, inp, X, out, reps), 3))
+                tg.append(round(timed(pl, inp, X, out, reps), 3))
                 f += pl.stats()["flops"]
                 pl.close()
                 del inp, out
-            else:
-                t_s.append(0.0)
+                torch.cuda.empty_cache()
+            t_g.append(tg)
+            t_s.append(round(sum(tg), 3))
             fl.append(f)
-            torch.cuda.empty_cache()
+        ends = []
+        for r in range(w):
+            t = t_o[r]
+            for (lo, hi, src), tg in zip(groups[r], t_g[r]):
+                t = max([t] + [t_o[q] for q in src]) + tg
+            ends.append(round(t, 3))
+        overlap = max(ends)
         barrier = max(t_o) + max(t_s)
-        overlap = max(a + b for a, b in zip(t_o, t_s))
         print(json.dumps({"world": w, "owners": owners, "n_subs": [len(s) for s in subs],
                           "owner_ms": t_o, "sub_ms": t_s,
                           "flop_balance": round(sum(fl) / w / max(fl), 4),
                           "job_ms_barrier": round(barrier, 3), "eff_barrier": round(t1 / w / barrier, 4),
-                          "job_ms_no_barrier": round(overlap, 3), "eff_no_barrier": round(t1 / w / overlap, 4)}),
+                          "rank_end_ms": ends, "groups": [len(g) for g in groups],
+                          "job_ms_gated": round(overlap, 3), "eff_gated": round(t1 / w / overlap, 4)}),
               flush=True)
 
 
