@@ -168,7 +168,17 @@ int bcss_device_free(void* ptr);
 int bcss_ipc_get_handle(const void* dev_ptr, void* out_handle64);
 int bcss_ipc_open_handle(const void* handle64, void** out_ptr);
 int bcss_ipc_close_handle(void* ptr);
+/* Stream-ordered copy between any two device addresses of this process,
+ * including peer buffers opened with bcss_ipc_open_handle (NVLink DMA): the
+ * T(m-1) hand-over from an owner GPU to its helper in the S5 schedule. */
+int bcss_copy_async(void* dst, const void* src, size_t bytes, void* stream);
 int bcss_plan_set_start_calls(bcss_plan* plan, int level, const int32_t* suffixes, int n_calls);
+/* With exactly one start call (J, ...): its first computed level produces only
+ * the children (jb, J, ...) for jb in `jbs` (strictly increasing, each <= J)
+ * instead of all jb <= J - a slice of the owner's level work handed to a
+ * helper GPU that received the start temporary.  Bit-identical to the same
+ * calls of the full plan.  n = 0 clears. */
+int bcss_plan_set_start_children(bcss_plan* plan, const int32_t* jbs, int n);
 /* Suffixes (m-k entries each) of the plan's level-k calls, in buffer order. */
 int bcss_plan_level_calls(bcss_plan* plan, int k, int32_t* out, int64_t n_max, int64_t* out_n);
 /* Element counts of the run's input (A or start temporaries) and output

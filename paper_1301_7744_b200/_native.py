@@ -62,7 +62,9 @@ SIGNATURES = {
     "bcss_ipc_get_handle": (_c_int, [_vp, _vp]),
     "bcss_ipc_open_handle": (_c_int, [_vp, _P(_vp)]),
     "bcss_ipc_close_handle": (_c_int, [_vp]),
+    "bcss_copy_async": (_c_int, [_vp, _vp, ctypes.c_size_t, _vp]),
     "bcss_plan_set_start_calls": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _c_int]),
+    "bcss_plan_set_start_children": (_c_int, [_vp, _P(ctypes.c_int32), _c_int]),
     "bcss_plan_level_calls": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _i64, _P(_i64)]),
     "bcss_plan_io_elems": (_c_int, [_vp, _P(_i64), _P(_i64)]),
     "bcss_plan_temp": (_c_int, [_vp, _c_int, _P(ctypes.c_int32), _P(_vp), _P(_i64)]),

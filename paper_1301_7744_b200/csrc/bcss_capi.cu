@@ -261,6 +261,12 @@ int bcss_ipc_open_handle(const void* handle64, void** out_ptr) {
   return BCSS_OK;
 }
 
+int bcss_copy_async(void* dst, const void* src, size_t bytes, void* stream) {
+  if ((!dst || !src) && bytes) return fail(BCSS_ERR_PARAMETER, "null buffer");
+  CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, static_cast<cudaStream_t>(stream)));
+  return BCSS_OK;
+}
+
 int bcss_ipc_close_handle(void* ptr) {
   CUDA_TRY(cudaIpcCloseMemHandle(ptr));
   return BCSS_OK;
@@ -285,6 +291,18 @@ int bcss_plan_set_start_calls(bcss_plan* P, int level, const int32_t* suffixes, 
     }
   P->start_level = level;
   P->start_suffixes.assign(suffixes, suffixes + (size_t)n_calls * sl);
+  invalidate(P);
+  return BCSS_OK;
+}
+
+int bcss_plan_set_start_children(bcss_plan* P, const int32_t* jbs, int n) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (n < 0 || (n > 0 && !jbs)) return fail(BCSS_ERR_PARAMETER, "bad child list");
+  for (int i = 0; i < n; ++i) {
+    if (jbs[i] < 0 || jbs[i] >= P->pbar) return fail(BCSS_ERR_RANGE, "child %d outside 0..%lld", jbs[i], (long long)P->pbar - 1);
+    if (i > 0 && jbs[i] <= jbs[i - 1]) return fail(BCSS_ERR_SHAPE, "children must be strictly increasing");
+  }
+  P->start_children.assign(jbs, jbs + n);
   invalidate(P);
   return BCSS_OK;
 }

@@ -229,8 +229,8 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       auto in_w0 = [&](int u) { return std::find(W.units.begin(), W.units.end(), u) != W.units.end(); };
       // X row block of unit u: u itself, or its position in the gathered X_top
       auto pos = [&](int u) {
-        if (P.top_rows.empty()) return u;
-        return (int)(std::lower_bound(P.top_rows.begin(), P.top_rows.end(), u) - P.top_rows.begin());
+        if (P.gather_rows.empty() || P.gather_level != k) return u;
+        return (int)(std::lower_bound(P.gather_rows.begin(), P.gather_rows.end(), u) - P.gather_rows.begin());
       };
       std::vector<int4> later;
       size_t s = 0;
@@ -250,11 +250,17 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
     } else {
       int64_t running = 0;
       std::vector<int64_t> full(P.m);
+      // start plan restricted to some children of its (single) start call:
+      // one parent over the gathered X rows of those children
+      const bool subset = k == k_first && P.start_level > 0 && !P.start_children.empty();
       for (int64_t c = 0; c < prev_calls; ++c) {
         const int32_t* sp = &prev_suffix[(size_t)(c * (sl - 1))];
         const int J = sp[0];
-        parents.push_back(int4{prev_call[(size_t)c], 0, (int)((J + 1) * P.bC), (int)running});
-        for (int jb = 0; jb <= J; ++jb) {
+        std::vector<int> kids;
+        if (subset) kids = P.start_children;
+        else for (int jb = 0; jb <= J; ++jb) kids.push_back(jb);
+        parents.push_back(int4{prev_call[(size_t)c], 0, (int)(kids.size() * P.bC), (int)running});
+        for (int jb : kids) {
           L.suffixes.push_back(jb);
           for (int q = 0; q < sl - 1; ++q) L.suffixes.push_back(sp[q]);
           if (k == 0) {
@@ -395,11 +401,25 @@ int build_plan(bcss_plan& P) {
       for (int u = 0; u < P.pbar; ++u) units.push_back(u);
     std::sort(units.begin(), units.end());
     units.erase(std::unique(units.begin(), units.end()), units.end());
-    // shard plans with scattered units: the top level reads gathered X rows
-    P.top_rows.clear();
+    // shard plans with scattered units: the top level reads gathered X rows;
+    // start plans with a child subset: their first level does
+    P.gather_rows.clear();
+    P.gather_level = -1;
     if (P.units_set && !P.mirror && P.start_level == 0 && units.size() > 1 &&
-        units.back() - units.front() + 1 != (int)units.size() && !getenv("BCSS_NO_TOP_GATHER"))
-      P.top_rows = units;
+        units.back() - units.front() + 1 != (int)units.size() && !getenv("BCSS_NO_TOP_GATHER")) {
+      P.gather_rows = units;
+      P.gather_level = P.m - 1;
+    }
+    if (P.start_level > 0 && !P.start_children.empty()) {
+      const int sl = P.m - P.start_level;
+      if (P.start_suffixes.size() != (size_t)sl)
+        return fail(BCSS_ERR_STATE, "start children need exactly one start call");
+      for (int jb : P.start_children)
+        if (jb > P.start_suffixes[0])
+          return fail(BCSS_ERR_RANGE, "start child %d > first suffix index %d", jb, (int)P.start_suffixes[0]);
+      P.gather_rows = P.start_children;
+      P.gather_level = P.start_level - 1;
+    }
     // pipeline groups: run_host computes T(m-1) of every unit first (it
     // overlaps the upload of A), then the groups' lower levels one after the
     // other while the previous group's C blocks download.  Contiguous groups
@@ -710,7 +730,7 @@ int build_plan(bcss_plan& P) {
         if (L.k == 0) P.c_blocks += L.n_calls;
       }
     }
-    P.off_top_rows = take(P.top_rows.size() * sizeof(int));
+    P.off_gather_rows = take(P.gather_rows.size() * sizeof(int));
     P.tables_bytes = off;
     P.built = true;
     return BCSS_OK;
@@ -739,7 +759,8 @@ int upload_tables(bcss_plan& P, cudaStream_t stream) {
       }
       memcpy(&host[L.off_child], L.child_call.data(), L.child_call.size() * sizeof(int));
     }
-  if (!P.top_rows.empty()) memcpy(&host[P.off_top_rows], P.top_rows.data(), P.top_rows.size() * sizeof(int));
+  if (!P.gather_rows.empty())
+    memcpy(&host[P.off_gather_rows], P.gather_rows.data(), P.gather_rows.size() * sizeof(int));
   CUDA_TRY(cudaMalloc(&P.d_tables, std::max<size_t>(P.tables_bytes, 256)));
   CUDA_TRY(cudaMemcpyAsync(P.d_tables, host.data(), P.tables_bytes, cudaMemcpyHostToDevice, stream));
   CUDA_TRY(cudaStreamSynchronize(stream));

@@ -153,14 +153,18 @@ struct bcss_plan {
   int defer_group = 0;              // cascade: top-level rows of later waves in groups >= this run after wave 0
   double* dXm = nullptr;            // X' (device, p x n)
   size_t dXm_bytes = 0;
-  // Gathered top-level rows (shard plans whose units are not one contiguous
-  // range, e.g. LPT pairs {j, p̄-1-j}): row block i of X_top is row block
-  // top_rows[i] of X, so the top level runs as ONE parent of |units|·b_C rows
-  // (taller tiles, each A tile read once per rank) instead of one short
-  // parent per run of units.  Empty: the top level reads X itself.
-  std::vector<int> top_rows;
-  size_t off_top_rows = 0;          // into the device table buffer
-  double* dXt = nullptr;            // X_top (device, |top_rows|·b_C x n)
+  // Gathered X rows for one level (gather_level): row block i of X_g is row
+  // block gather_rows[i] of X.  Shard plans whose units are not one contiguous
+  // range (e.g. LPT pairs {j, p̄-1-j}) run their top level as ONE parent of
+  // |units|·b_C rows (taller tiles, each A tile read once per rank) instead of
+  // one short parent per run of units; start plans restricted to a subset of
+  // the first level's children (start_children) contract only those rows.
+  // Empty: every level reads X itself.
+  std::vector<int> start_children;  // first computed level of a start plan: these jb only
+  std::vector<int> gather_rows;
+  int gather_level = -1;
+  size_t off_gather_rows = 0;       // into the device table buffer
+  double* dXt = nullptr;            // X_g (device, |gather_rows|·b_C x n)
   size_t dXt_bytes = 0;
   int start_level = 0;              // 0 = from A; else compute below caller-provided T(start_level)
   std::vector<int32_t> start_suffixes;  // their calls (m - start_level entries each)

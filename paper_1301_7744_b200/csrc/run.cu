@@ -34,8 +34,7 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   char* tbl = static_cast<char*>(P->d_tables);
   bcss::LevelArgs a;
   memset(&a, 0, sizeof(a));
-  const bool top = P->start_level == 0 && L.k == P->m - 1;
-  a.X = (top && !P->top_rows.empty()) ? P->dXt : X_;
+  a.X = (L.k == P->gather_level && !P->gather_rows.empty()) ? P->dXt : X_;
   const bool from_input = (P->start_level == 0 && L.k == P->m - 1) || (P->start_level > 0 && L.k == P->start_level - 1);
   a.Tin = from_input ? A : region_for(*P, W, L.k + 1);
   a.Tout = (L.k == P->stop_level) ? C : region_for(*P, W, L.k);
@@ -81,7 +80,7 @@ __global__ void reverse_row_blocks(const double* __restrict__ src, double* __res
   }
 }
 
-// X_top for shard plans: row block i of dst is row block rows[i] of src
+// gathered X rows (plan.hpp gather_rows): row block i of dst is row block rows[i] of src
 __global__ void gather_row_blocks(const double* __restrict__ src, double* __restrict__ dst,
                                   const int* __restrict__ rows, long long nblk, long long n, long long bc) {
   const long long per = bc * n;  // doubles per row block (contiguous in both)
@@ -156,8 +155,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     CUDA_TRY(cudaGetLastError());
     X_ = P->dXm;
   }
-  if (!P->top_rows.empty()) {  // gathered top-level X rows (shard plans)
-    const size_t xb = P->top_rows.size() * (size_t)(P->bC * P->n) * sizeof(double);
+  if (!P->gather_rows.empty()) {  // gathered X rows of one level (shard / child-subset plans)
+    const size_t xb = P->gather_rows.size() * (size_t)(P->bC * P->n) * sizeof(double);
     if (P->dXt_bytes < xb) {
       if (P->dXt) cudaFree(P->dXt);
       P->dXt = nullptr;
@@ -166,8 +165,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       P->dXt_bytes = xb;
     }
     if (pipe) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev[0], 0));  // X was uploaded ahead of A chunk 0
-    const int* rows = reinterpret_cast<const int*>(static_cast<char*>(P->d_tables) + P->off_top_rows);
-    gather_row_blocks<<<296, 256, 0, s>>>(X_, P->dXt, rows, (long long)P->top_rows.size(), P->n, P->bC);
+    const int* rows = reinterpret_cast<const int*>(static_cast<char*>(P->d_tables) + P->off_gather_rows);
+    gather_row_blocks<<<296, 256, 0, s>>>(X_, P->dXt, rows, (long long)P->gather_rows.size(), P->n, P->bC);
     CUDA_TRY(cudaGetLastError());
   }
   if ((st = ensure_workspace(*P)) == BCSS_ERR_NOMEM && !P->d_ws && !P->keep_temps && P->start_level == 0 &&

@@ -131,31 +131,57 @@ def s5_schedule(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: b
 
 
 def s5_groups(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: bool = True):
-    """(owners, subs, groups) of scheme S5 with release times.
+    """(owners, subs, groups) of scheme S5 without helpers; groups[r] =
+    [(lo, hi, source ranks)] (see ``s5_tasks``)."""
+    sc = s5_tasks(m, n, p, b_a, b_c, world, reuse, helpers=False)
+    groups = [[(lo, hi, sorted({q for q, _ in src})) for lo, hi, src in g] for g in sc["groups"]]
+    return sc["owners"], sc["subs"], groups
+
+
+# modelled rates of the schedule (flop/s of the level kernels, B/s of an
+# NVLink peer copy) - only their ratio matters: the T(m-1) transfer delay
+RATE_FLOPS = 34e12
+RATE_NVLINK = 600e9
+
+
+def s5_tasks(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: bool = True,
+             helpers: bool = True, force_helper: bool = False) -> dict:
+    """Task schedule of scheme S5 (release times, optional helpers).
 
     Owners: LPT over the owner costs (top-level rows of unit u plus its
-    level-(m-2) calls (i, u), i <= u).  A subtree call (i, u) is *released*
-    when the rank owning u finishes its owner plan (modelled as that rank's
-    owner flops), so the subtrees are list-scheduled by release time: each
-    call goes to the rank where it would finish first, max(free, release) +
-    cost.  groups[r] = [(lo, hi, src_ranks)]: subs[r][lo:hi] run as one
-    subtree plan once the owners in src_ranks have finished; consecutive
-    calls share a group unless the later one would otherwise wait.  No
-    global barrier separates the phases - a rank starts its first group as
-    soon as its own owner plan and that group's sources are done (config 5 at
-    8 GPUs: the barrier-separated schedule modelled 0.64 efficiency, this one
-    0.87 - bounded by the largest owner).
+    level-(m-2) calls (i, u), i <= u).  **Helpers**: an owner of a single unit
+    whose load exceeds the ideal share hands some of its level-(m-2) children
+    to the least-loaded rank, which receives T(m-1)[u] by an NVLink peer copy
+    after the owner's top level and computes those children from it (a start
+    plan with a child subset); the owner computes the rest.  A subtree call
+    (i, u) is *released* when the task producing its T(m-2) ends; the calls
+    are list-scheduled by release time (each to the rank where it would
+    finish first), and a rank's calls form release groups, one subtree plan
+    each, which wait only on their sources' completion events.
+
+    Times are modelled in flops (transfer = bytes x RATE_FLOPS / RATE_NVLINK).
+    Returns {owners, helper: {u: (h, children)}, own_children: {u: children},
+    help_of: {h: u}, subs, groups: [[(lo, hi, [(rank, "own"|"help")])]],
+    model_end: per-rank modelled end}.  ``force_helper`` hands one child of
+    the largest multi-child unit to another rank even when it does not pay
+    (tests).
     """
     pbar = p // b_c
     if m < 3:  # no level below m-2 to hand out: plain S1
         parts = partition_units(unit_flops(m, n, p, b_a, b_c, reuse), world)
-        return parts, [[] for _ in range(world)], [[] for _ in range(world)]
-    owner_cost = []
+        return {"owners": parts, "helper": {}, "own_children": {}, "help_of": {},
+                "subs": [[] for _ in range(world)], "groups": [[] for _ in range(world)], "model_end": None}
+    owner_cost, top_cost = [], []
     for u in range(pbar):
         pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=[u], stop_level=m - 2)
         owner_cost.append(pl.stats()["flops"])
         pl.close()
-    loads = [0] * world
+    pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=[0], stop_level=m - 1)
+    top = pl.stats()["flops"]  # every unit's top-level rows cost the same
+    t_bytes = pl.c_elems * 8   # T(m-1) of one unit
+    pl.close()
+    lvl = [(owner_cost[u] - top) / (u + 1) for u in range(pbar)]  # per level-(m-2) call of unit u
+    loads = [0.0] * world
     owners: list[list[int]] = [[] for _ in range(world)]
     owner_of = {}
     for u in sorted(range(pbar), key=lambda q: (-owner_cost[q], q)):
@@ -163,20 +189,66 @@ def s5_groups(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: boo
         owners[r].append(u)
         owner_of[u] = r
         loads[r] += owner_cost[u]
-    release = {u: loads[owner_of[u]] for u in range(pbar)}
-    # subtree cost depends only on i (the row block) for fixed shapes
     sub_cost = {}
     for i in range(pbar):
         pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=[(i, pbar - 1)])
         sub_cost[i] = pl.stats()["flops"]
         pl.close()
+    total = sum(owner_cost) + sum(sub_cost[i] for u in range(pbar) for i in range(u + 1))
+    ideal = total / world
+    transfer = t_bytes * RATE_FLOPS / RATE_NVLINK
+    own_end = list(loads)                       # end of each rank's owner task
+    help_end: dict[int, float] = {}             # rank -> end of its help task
+    helper: dict[int, tuple] = {}
+    own_children = {u: list(range(u + 1)) for u in range(pbar)}
+    help_of: dict[int, int] = {}
+    if helpers and world > 1:
+        for r in sorted(range(world), key=lambda q: (-loads[q], q)):
+            if len(owners[r]) != 1:
+                continue
+            u = owners[r][0]
+            if u == 0 or (own_end[r] <= ideal and not (force_helper and not helper)):
+                continue
+            cands = [q for q in range(world) if q != r and q not in help_of and owner_of.get(u) != q
+                     and not any(helper.get(v, (None,))[0] == q for v in helper)]
+            cands = [q for q in cands if all(owner_of[v] != q for v in helper)]
+            if not cands:
+                continue
+            h = min(cands, key=lambda q: (own_end[q], q))
+            best = None
+            for c in range(1, u + 1):  # children handed over (the largest indices)
+                e_owner = own_end[r] - c * lvl[u]
+                e_help = max(own_end[h], top + transfer) + c * lvl[u]
+                val = max(e_owner, e_help)
+                if best is None or val < best[0]:
+                    best = (val, c, e_owner, e_help)
+            val, c, e_owner, e_help = best
+            if val >= own_end[r] and not (force_helper and not helper):
+                continue
+            kids = list(range(u + 1 - c, u + 1))
+            helper[u] = (h, kids)
+            own_children[u] = list(range(u + 1 - c))
+            help_of[h] = u
+            own_end[r] = e_owner
+            help_end[h] = e_help
+    # release time of call (i, u): end of the task producing its T(m-2)
+    release, source = {}, {}
+    for u in range(pbar):
+        for i in own_children[u]:
+            release[(i, u)] = own_end[owner_of[u]]
+            source[(i, u)] = (owner_of[u], "own")
+        if u in helper:
+            h, kids = helper[u]
+            for i in kids:
+                release[(i, u)] = help_end[h]
+                source[(i, u)] = (h, "help")
     calls = sorted(((i, u) for u in range(pbar) for i in range(u + 1)),
-                   key=lambda c: (release[c[1]], -sub_cost[c[0]], c))
-    free = list(loads)
+                   key=lambda c: (release[c], -sub_cost[c[0]], c))
+    free = [max(own_end[r], help_end.get(r, 0.0)) for r in range(world)]
     subs: list[list[tuple]] = [[] for _ in range(world)]
-    starts: list[list[int]] = [[] for _ in range(world)]
+    starts: list[list[float]] = [[] for _ in range(world)]
     for c in calls:
-        rel, cost = release[c[1]], sub_cost[c[0]]
+        rel, cost = release[c], sub_cost[c[0]]
         r = min(range(world), key=lambda q: (max(free[q], rel) + cost, free[q], q))
         st = max(free[r], rel)
         subs[r].append(c)
@@ -185,14 +257,16 @@ def s5_groups(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: boo
     groups: list[list[tuple]] = [[] for _ in range(world)]
     for r in range(world):
         lo = 0
+        prod_end = max(own_end[r], help_end.get(r, 0.0))
         for j in range(1, len(subs[r]) + 1):
             # a call that would start later than the group's first call because it
-            # waits for its owner (not for the calls before it) opens a new group
-            if j == len(subs[r]) or release[subs[r][j][1]] > max(starts[r][lo], loads[r]):
-                src = sorted({owner_of[c[1]] for c in subs[r][lo:j]})
+            # waits for its producer (not for the calls before it) opens a new group
+            if j == len(subs[r]) or release[subs[r][j]] > max(starts[r][lo], prod_end):
+                src = sorted({source[c] for c in subs[r][lo:j]})
                 groups[r].append((lo, j, src))
                 lo = j
-    return [sorted(o) for o in owners], subs, groups
+    return {"owners": [sorted(o) for o in owners], "helper": helper, "own_children": own_children,
+            "help_of": help_of, "subs": subs, "groups": groups, "model_end": free, "ideal": ideal}
 
 
 def _gpu_compute(plan: SttsmPlan, inp, x, out) -> None:
@@ -248,125 +322,218 @@ def open_peer(handle: bytes) -> int:
 
 
 class S5Runner:
-    """One rank's share of the scheme-S5 schedule, with its plans, buffers and
-    exchange list built once; ``run`` executes one full step (phase 1,
-    T(m-2) exchange, phase 2) asynchronously on the current stream / NCCL.
+    """One rank's share of the scheme-S5 schedule (``s5_tasks``), with its
+    plans, buffers and exchange tables built once; ``run`` executes one full
+    step asynchronously on the current stream.
 
-    Phase 2 is one subtree plan per release group (``s5_groups``).  With the
-    fused exchange there is no barrier between the phases: every rank records
-    a CUDA IPC event after its owner plan, and each group's plan waits on the
-    events of the owners it reads from, so a rank whose owner work is short
-    starts its subtrees while the long owners still run."""
+    Tasks on a rank, in stream order:
+      1. owner work - either one plan over its units down to level m-2, or,
+         for an owner with a helper, the top-level plan (T(m-1)[u] into a
+         local buffer, then an NVLink peer copy of it into the helper's
+         receive buffer on a side stream) and a level-(m-2) plan over the
+         children it keeps;
+      2. help work - a level-(m-2) plan over the handed-over children, reading
+         the received T(m-1)[u] once the owner's copy event fired;
+      3. one subtree plan per release group.
+    Every level-(m-2) plan stores each call's T(m-2) straight into its
+    assignee's receive slot (fused exchange, CUDA IPC peer stores).  Tasks
+    of different ranks are ordered by CUDA IPC events ("sent", "own",
+    "help") that the waiting rank's stream waits on; host barriers run over
+    a gloo group, so they never wait for GPU work.  ``exchange="nccl"`` (or a
+    rank that cannot map its peers under "auto") uses the schedule without
+    helpers and NCCL send/recv between the phases.
+    """
 
     def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, rank: int, world: int, device,
-                 reuse: bool = True, group=None, compute=_gpu_compute, exchange: str = "nccl"):
-        import torch
-
-        self.m, self.rank, self.world, self.group, self.compute = m, rank, world, group, compute
+                 reuse: bool = True, group=None, compute=_gpu_compute, exchange: str = "nccl",
+                 helpers: bool = True, force_helper: bool = False):
         if exchange not in ("nccl", "peer", "auto"):
             raise ValueError(f"exchange must be 'nccl', 'peer' or 'auto', not {exchange!r}")
-        self.exchange = exchange
-        owners, subs, groups = s5_groups(m, n, p, b_a, b_c, world, reuse)
-        self.owners, self.subs, self.groups = owners, subs, groups[rank]
-        owner_of = {u: r for r in range(world) for u in owners[r]}
-        self.plan_o = (SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=owners[rank], stop_level=m - 2)
-                       if owners[rank] else None)
-        # one subtree plan per release group: slots subs[rank][lo:hi] of the receive buffer
-        self.plans_s = [SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2,
-                                  start_calls=subs[rank][lo:hi]) for lo, hi, _ in self.groups]
-        self._ev_own, self._ev_peer = None, {}
+        self.m, self.n, self.p, self.b_a, self.b_c, self.reuse = m, n, p, b_a, b_c, reuse
+        self.rank, self.world, self.group, self.compute, self.device = rank, world, group, compute, device
         probe = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, start_level=m - 2, start_calls=[(0, 0)])
         self.slice = probe.a_elems
         probe.close()
-        # call order of every owner's T(m-2) buffer (deterministic, no communication)
-        order = {}
-        for r in range(world):
-            if owners[r]:
-                pl = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, units=owners[r], stop_level=m - 2)
-                order[r] = {c: i for i, c in enumerate(pl.level_calls(m - 2))}
-                pl.close()
-        self.t2 = None  # owner output buffer (NCCL exchange only; the fused exchange stores to the slots)
-        self._buf, self._peers = None, []
-        if exchange in ("peer", "auto"):
-            # fused exchange: every rank's receive buffer is opened by the others
-            # (CUDA IPC); the owner's level-(m-2) kernel stores each call's
-            # T(m-2) slice straight into its assignee's slot (NVLink peer stores).
-            # "auto" falls back to NCCL send/recv if any rank cannot map a peer.
-            import torch.distributed as dist
-
-            ok, err = True, ""
-            solo = world == 1 or not dist.is_initialized()
-            try:
-                self._buf = DeviceBuffer(max(1, len(subs[rank])) * self.slice, device)
-                handle = None if solo else self._buf.ipc_handle()
-            except Exception as e:  # noqa: BLE001 - reported below / fallback
-                ok, err, handle = False, str(e), None
-            handles = [handle] * world
-            if not solo:
-                dist.all_gather_object(handles, handle, group=group)
-            base = {}
-            if ok and (solo or all(h is not None for h in handles)):
-                try:
-                    for r in range(world):
-                        if r == rank:
-                            base[r] = self._buf.ptr
-                        elif subs[r]:
-                            base[r] = open_peer(handles[r])
-                            self._peers.append(base[r])
-                except Exception as e:  # noqa: BLE001
-                    ok, err = False, str(e)
-            else:
-                ok = False
-            flags = [ok] * world
-            if not solo:
-                dist.all_gather_object(flags, ok, group=group)
-            if all(flags) and not solo:
-                # owner-done events: group g of an assignee waits on its sources' events
-                try:
-                    self._ev_own = torch.cuda.Event(interprocess=True)
-                    ev_handle = self._ev_own.ipc_handle()
-                except Exception as e:  # noqa: BLE001
-                    ok, err, ev_handle = False, str(e), None
-                ev_handles = [ev_handle] * world
-                dist.all_gather_object(ev_handles, ev_handle, group=group)
-                need = {q for _, _, src in self.groups for q in src if q != rank}
-                try:
-                    for q in need:
-                        if ev_handles[q] is None:
-                            raise RuntimeError(f"rank {q} has no owner event")
-                        self._ev_peer[q] = torch.cuda.Event.from_ipc_handle(device, ev_handles[q])
-                except Exception as e:  # noqa: BLE001
-                    ok, err = False, str(e)
-                flags = [ok] * world
-                dist.all_gather_object(flags, ok, group=group)
-            if all(flags):
-                self.exchange = "peer"
-                self.inp = self._buf.tensor
-                self.dest = self.peer_destinations(subs, rank)
-                if self.plan_o is not None:
-                    self.plan_o.set_call_outputs([base[r] + 8 * self.slice * j for r, j in self.dest])
-            elif exchange == "peer":
-                raise RuntimeError(f"fused peer exchange unavailable on some rank: {err}")
-            else:
-                self.exchange = "nccl"
-        if self.exchange != "peer":
-            self.inp = torch.empty(max(1, len(subs[rank])) * self.slice, dtype=torch.float64, device=device)
-            if self.plan_o is not None:
-                self.t2 = torch.empty(self.plan_o.c_elems, dtype=torch.float64, device=device)
-        self.local, self.sends, self.recvs = [], [], []  # (dst slot, src slot) / (peer, slot)
-        for r in range(world):
-            for j, c in enumerate(subs[r]):
-                q = owner_of[c[1]]
-                if q == rank and r == rank:
-                    self.local.append((j, order[q][c]))
-                elif q == rank:
-                    self.sends.append((r, order[q][c]))
-                elif r == rank:
-                    self.recvs.append((q, j))
-        self.exchange_bytes = 8 * self.slice * (len(self.sends) + len(self.recvs))
         full = SttsmPlan(m, n, p, b_a, b_c)
         self.c_elems = full.c_elems
         full.close()
+        self._plans_all: list[SttsmPlan] = []
+        self._peers: list[int] = []
+        self._bufs: list[DeviceBuffer] = []
+        if exchange in ("peer", "auto"):
+            err = self._setup(True, helpers, force_helper)
+            if err is None:
+                self.exchange = "peer"
+                return
+            if exchange == "peer":
+                raise RuntimeError(f"fused peer exchange unavailable on some rank: {err}")
+            self._teardown()
+        self._setup(False, False, False)
+        self.exchange = "nccl"
+
+    # ---- construction -----------------------------------------------------------
+    def _plan(self, **kw) -> SttsmPlan:
+        pl = SttsmPlan(self.m, self.n, self.p, self.b_a, self.b_c, reuse=self.reuse, **kw)
+        self._plans_all.append(pl)
+        return pl
+
+    def _teardown(self) -> None:
+        for pl in self._plans_all:
+            pl.close()
+        self._plans_all = []
+        for ptr in self._peers:
+            try:
+                from . import _native
+                import ctypes
+                _native.lib().bcss_ipc_close_handle(ctypes.c_void_p(ptr))
+            except Exception:  # noqa: BLE001 - best effort
+                pass
+        self._peers = []
+        for b in self._bufs:
+            b.close()
+        self._bufs = []
+
+    def _setup(self, peer: bool, helpers: bool, force_helper: bool):
+        """Build plans and buffers; returns None or the reason peer mode failed."""
+        import torch
+
+        m, rank, world, device = self.m, self.rank, self.world, self.device
+        sc = s5_tasks(self.m, self.n, self.p, self.b_a, self.b_c, world, self.reuse,
+                      helpers=helpers and peer, force_helper=force_helper)
+        self.sched = sc
+        owners, subs = sc["owners"], sc["subs"]
+        self.owners, self.subs, self.groups = owners, subs, sc["groups"][rank]
+        owner_of = {u: r for r in range(world) for u in owners[r]}
+        self.owner_of = owner_of
+        mine = owners[rank]
+        helped = [u for u in mine if u in sc["helper"]]
+        # 1. owner work
+        self.plan_o = self.plan_top = self.plan_lvl = None
+        self.top_unit = helped[0] if helped else None
+        if self.top_unit is not None:
+            u = self.top_unit
+            self.plan_top = self._plan(units=[u], stop_level=m - 1)
+            self.plan_lvl = self._plan(start_level=m - 1, start_calls=[(u,)],
+                                       start_children=sc["own_children"][u], stop_level=m - 2)
+        elif mine:
+            self.plan_o = self._plan(units=mine, stop_level=m - 2)
+        # 2. help work
+        self.help_unit = sc["help_of"].get(rank)
+        self.plan_help = None
+        if self.help_unit is not None:
+            v = self.help_unit
+            self.plan_help = self._plan(start_level=m - 1, start_calls=[(v,)],
+                                        start_children=sc["helper"][v][1], stop_level=m - 2)
+        # 3. subtree plans, one per release group: slots subs[rank][lo:hi]
+        self.plans_s = [self._plan(start_level=m - 2, start_calls=subs[rank][lo:hi]) for lo, hi, _ in self.groups]
+        where = {c: (r, j) for r in range(world) for j, c in enumerate(subs[r])}
+        self.producers = [pl for pl in (self.plan_o, self.plan_lvl, self.plan_help) if pl is not None]
+        self.t_top = None
+        if self.plan_top is not None:
+            self.t_top = torch.empty(self.plan_top.c_elems, dtype=torch.float64, device=device)
+        self._ev_own = self._ev_sent = self._ev_help = None
+        self._ev_peer: dict = {}
+        self._host_group = None
+        if not peer:
+            # NCCL exchange: the owner plan writes T(m-2) locally, then send/recv
+            self.inp = torch.empty(max(1, len(subs[rank])) * self.slice, dtype=torch.float64, device=device)
+            self.t2 = (torch.empty(self.plan_o.c_elems, dtype=torch.float64, device=device)
+                       if self.plan_o is not None else None)
+            order = {}
+            for r in range(world):
+                if owners[r]:
+                    pl = SttsmPlan(self.m, self.n, self.p, self.b_a, self.b_c, reuse=self.reuse,
+                                   units=owners[r], stop_level=m - 2)
+                    order[r] = {c: i for i, c in enumerate(pl.level_calls(m - 2))}
+                    pl.close()
+            self.local, self.sends, self.recvs = [], [], []  # (dst slot, src slot) / (peer, slot)
+            for r in range(world):
+                for j, c in enumerate(subs[r]):
+                    q = owner_of[c[1]]
+                    if q == rank and r == rank:
+                        self.local.append((j, order[q][c]))
+                    elif q == rank:
+                        self.sends.append((r, order[q][c]))
+                    elif r == rank:
+                        self.recvs.append((q, j))
+            self.exchange_bytes = 8 * self.slice * (len(self.sends) + len(self.recvs))
+            return None
+        # fused exchange: every rank's receive buffers are opened by the others
+        import torch.distributed as dist
+
+        solo = world == 1 or not dist.is_initialized()
+        hg = None
+        if not solo:
+            hg = self._host_group = dist.new_group(backend="gloo")  # host-only barriers and handle swaps
+        ok, err = True, ""
+        handles = (None, None, None)
+        try:
+            inbuf = DeviceBuffer(max(1, len(subs[rank])) * self.slice, device)
+            self._bufs.append(inbuf)
+            self.inp = inbuf.tensor
+            self.recv_top = None
+            if self.plan_help is not None:  # T(m-1) of the helped unit arrives here
+                rb = DeviceBuffer(self.plan_help.a_elems, device)
+                self._bufs.append(rb)
+                self.recv_top = rb
+            if not solo:
+                self._ev_own = torch.cuda.Event(interprocess=True)
+                self._ev_sent = torch.cuda.Event(interprocess=True)
+                self._ev_help = torch.cuda.Event(interprocess=True)
+                handles = (inbuf.ipc_handle(), self.recv_top.ipc_handle() if self.recv_top else None,
+                           (self._ev_own.ipc_handle(), self._ev_sent.ipc_handle(), self._ev_help.ipc_handle()))
+        except Exception as e:  # noqa: BLE001 - reported / fallback
+            ok, err, handles = False, str(e), (None, None, None)
+        allh = [handles] * world
+        if not solo:
+            dist.all_gather_object(allh, handles, group=hg)
+        base, top_dst = {rank: self.inp.data_ptr()} if ok else {}, None
+        if ok:
+            try:
+                for r in range(world):
+                    if r != rank and subs[r]:
+                        if allh[r][0] is None:
+                            raise RuntimeError(f"rank {r} has no receive buffer")
+                        base[r] = open_peer(allh[r][0])
+                        self._peers.append(base[r])
+                if self.top_unit is not None:
+                    h = sc["helper"][self.top_unit][0]
+                    if solo:
+                        top_dst = self.recv_top.ptr if h == rank else None
+                    else:
+                        if allh[h][1] is None:
+                            raise RuntimeError(f"helper rank {h} has no T(m-1) buffer")
+                        top_dst = open_peer(allh[h][1])
+                        self._peers.append(top_dst)
+                if not solo:
+                    need = set()
+                    for _, _, src in self.groups:
+                        need |= {(q, tag) for q, tag in src if q != rank}
+                    if self.help_unit is not None:
+                        need.add((owner_of[self.help_unit], "sent"))
+                    idx = {"own": 0, "sent": 1, "help": 2}
+                    for q, tag in need:
+                        self._ev_peer[(q, tag)] = torch.cuda.Event.from_ipc_handle(device, allh[q][2][idx[tag]])
+            except Exception as e:  # noqa: BLE001
+                ok, err = False, str(e)
+        flags = [ok] * world
+        if not solo:
+            dist.all_gather_object(flags, ok, group=hg)
+        if not all(flags):
+            return err or "a peer rank could not map the exchange buffers"
+        self.top_dst = top_dst
+        for pl in self.producers:
+            pl.set_call_outputs([base[r] + 8 * self.slice * j for r, j in
+                                 (where[tuple(c)] for c in pl.level_calls(m - 2))])
+        self.t2 = None
+        self.local, self.sends, self.recvs = [], [], []
+        self.exchange_bytes = 8 * self.slice * sum(1 for pl in self.producers for c in pl.level_calls(m - 2)
+                                                   if where[tuple(c)][0] != rank)
+        if self.plan_top is not None and sc["helper"][self.top_unit][0] != rank:
+            self.exchange_bytes += 8 * self.plan_top.c_elems
+        self._side = torch.cuda.Stream(device=device)
+        self._ev_top = torch.cuda.Event()
+        return None
 
     def peer_destinations(self, subs, rank) -> list[tuple[int, int]]:
         """(assignee rank, slot) of every call of this rank's owner plan, in the
@@ -377,8 +544,14 @@ class S5Runner:
         return [where[tuple(c)] for c in self.plan_o.level_calls(self.m - 2)]
 
     def plans(self):
-        return ([self.plan_o] if self.plan_o is not None else []) + list(self.plans_s)
+        return [pl for pl in (self.plan_o, self.plan_top, self.plan_lvl, self.plan_help) if pl is not None] + \
+            list(self.plans_s)
 
+    def attach_torch_workspace(self, device=None) -> None:
+        for pl in self.plans():
+            pl.attach_torch_workspace(device)
+
+    # ---- one step ---------------------------------------------------------------
     def _run_groups(self, x, c, wait_peers: bool) -> None:
         import torch
 
@@ -386,37 +559,63 @@ class S5Runner:
         stream = torch.cuda.current_stream(x.device) if wait_peers else None
         for (lo, hi, src), pl in zip(self.groups, self.plans_s):
             if wait_peers:
-                for q in src:
-                    if q != self.rank:  # own owner work precedes on this stream
-                        stream.wait_event(self._ev_peer[q])
+                for q, tag in src:
+                    if q != self.rank:  # own producer work precedes on this stream
+                        stream.wait_event(self._ev_peer[(q, tag)])
             self.compute(pl, self.inp[lo * s:hi * s], x, c)
 
-    def attach_torch_workspace(self, device=None) -> None:
-        for pl in self.plans():
-            pl.attach_torch_workspace(device)
+    def _run_ptr(self, pl: SttsmPlan, inp_ptr: int, x, out_ptr: int, stream) -> None:
+        if pl._ws is None:
+            pl.attach_torch_workspace(x.device)
+        pl.run_ptr(inp_ptr, x.data_ptr(), out_ptr, stream.cuda_stream)
 
     def run(self, a, x, c) -> None:
         import torch.distributed as dist
 
         s = self.slice
         if self.exchange == "peer":
+            import ctypes
+
             import torch
 
-            multi = self.world > 1 and self._ev_own is not None
+            from . import _native
+
+            multi = self._host_group is not None
+            hg = self._host_group
             if multi:
-                # the previous step's subtree plans finished reading every receive
-                # buffer before any owner overwrites one
+                # the previous step's readers of every receive buffer are done
+                # before any rank overwrites one
                 torch.cuda.synchronize()
-                dist.barrier(group=self.group)
+                dist.barrier(group=hg)
             stream = torch.cuda.current_stream(x.device)
-            if self.plan_o is not None:  # writes every T(m-2) slice into its assignee's buffer
-                # every call has a destination, so the output buffer is never touched
-                if self.plan_o._ws is None:
-                    self.plan_o.attach_torch_workspace(x.device)
-                self.plan_o.run_ptr(a.data_ptr(), x.data_ptr(), self.inp.data_ptr(), stream.cuda_stream)
+            # every call has a destination, so a producer's output buffer is never touched
+            sink = self.inp.data_ptr()
+            if self.plan_top is not None:
+                self._run_ptr(self.plan_top, a.data_ptr(), x, self.t_top.data_ptr(), stream)
+                if self.top_dst is not None:  # T(m-1)[u] -> helper over NVLink, beside the level work
+                    self._ev_top.record(stream)
+                    self._side.wait_event(self._ev_top)
+                    _native.check(_native.lib().bcss_copy_async(
+                        ctypes.c_void_p(self.top_dst), ctypes.c_void_p(self.t_top.data_ptr()),
+                        ctypes.c_size_t(8 * self.t_top.numel()), ctypes.c_void_p(self._side.cuda_stream)))
+                    if multi:
+                        self._ev_sent.record(self._side)
+                    else:
+                        stream.wait_stream(self._side)  # one process: the helper task follows on this stream
+                self._run_ptr(self.plan_lvl, self.t_top.data_ptr(), x, sink, stream)
+            elif self.plan_o is not None:
+                self._run_ptr(self.plan_o, a.data_ptr(), x, sink, stream)
             if multi:
                 self._ev_own.record(stream)
-                dist.barrier(group=self.group)  # every owner event of this step is recorded (host only)
+                dist.barrier(group=hg)  # every "own"/"sent" event of this step is recorded
+            if self.plan_help is not None:
+                if multi:
+                    stream.wait_event(self._ev_peer[(self.owner_of[self.help_unit], "sent")])
+                self._run_ptr(self.plan_help, self.recv_top.ptr, x, sink, stream)
+                if multi:
+                    self._ev_help.record(stream)
+            if multi:
+                dist.barrier(group=hg)  # every "help" event of this step is recorded
             self._run_groups(x, c, wait_peers=multi)
             return
         if self.plan_o is not None:

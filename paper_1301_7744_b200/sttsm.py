@@ -60,7 +60,7 @@ class SttsmPlan:
 
     def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, reuse: bool = True,
                  units=None, workspace_limit: int = 0, keep_temps: bool = False, pipeline: int = 0,
-                 stop_level: int = 0, start_level: int | None = None, start_calls=None):
+                 stop_level: int = 0, start_level: int | None = None, start_calls=None, start_children=None):
         lib = _native.lib()
         self.m, self.n, self.p, self.b_a, self.b_c, self.reuse = m, n, p, b_a, b_c, bool(reuse)
         h = ctypes.c_void_p()
@@ -85,10 +85,16 @@ class SttsmPlan:
             flat = [int(v) for call in start_calls for v in call]
             arr = (ctypes.c_int32 * max(1, len(flat)))(*flat)
             _native.check(lib.bcss_plan_set_start_calls(h, int(start_level), arr, len(start_calls)))
+            if start_children is not None:
+                # only these children of the single start call at the first level
+                kids = (ctypes.c_int32 * max(1, len(start_children)))(*[int(j) for j in start_children])
+                _native.check(lib.bcss_plan_set_start_children(h, kids, len(start_children)))
         self.units = None if units is None else sorted(set(int(u) for u in units))
         self.stop_level = int(stop_level)
         self.start_level = start_level if (start_level is not None and start_level < m) else None
         self.start_calls = [tuple(c) for c in start_calls] if self.start_level is not None else None
+        self.start_children = (None if self.start_level is None or start_children is None
+                               else [int(j) for j in start_children])
         ie, oe = ctypes.c_int64(), ctypes.c_int64()
         _native.check(lib.bcss_plan_io_elems(h, ctypes.byref(ie), ctypes.byref(oe)))
         self.a_elems = int(ie.value)   # input buffer: A, or start-level temporaries

@@ -124,3 +124,38 @@ def test_s5_schedule_balance_and_coverage():
     owners, subs = s5_schedule(*cfg, 8)
     assert sorted(u for o in owners for u in o) == list(range(8))
     assert sorted(c for s in subs for c in s) == sorted((i, u) for u in range(8) for i in range(u + 1))
+
+
+@pytest.mark.parametrize("cfg,world,force", [((4, 512, 256, 32, 32), 8, False), ((4, 192, 192, 16, 16), 8, True),
+                                             ((5, 96, 96, 8, 8), 8, True), ((4, 64, 32, 16, 16), 2, True)])
+def test_s5_helper_schedule_covers_every_call_once(cfg, world, force):
+    """S5 with helpers: every level-(m-2) call is produced exactly once (kept by
+    its owner or handed to one helper), assigned to exactly one subtree group,
+    and every group's sources are the producing tasks of its calls."""
+    from paper_1301_7744_b200.distributed import s5_tasks
+    m, n, p, ba, bc = cfg
+    pbar = p // bc
+    sc = s5_tasks(*cfg, world, force_helper=force)
+    assert sc["helper"]
+    owner_of = {u: r for r in range(world) for u in sc["owners"][r]}
+    produced = {}
+    for u in range(pbar):
+        for i in sc["own_children"][u]:
+            produced[(i, u)] = (owner_of[u], "own")
+        if u in sc["helper"]:
+            h, kids = sc["helper"][u]
+            assert h != owner_of[u] and sc["help_of"][h] == u and len(sc["owners"][owner_of[u]]) == 1
+            assert not set(kids) & set(sc["own_children"][u]) and sc["own_children"][u]
+            for i in kids:
+                produced[(i, u)] = (h, "help")
+    assert sorted(produced) == sorted((i, u) for u in range(pbar) for i in range(u + 1))
+    assigned = [c for s in sc["subs"] for c in s]
+    assert sorted(assigned) == sorted(produced)
+    for r in range(world):
+        groups = sc["groups"][r]
+        assert [g[0] for g in groups] == ([0] + [g[1] for g in groups[:-1]] if groups else [])
+        assert (groups[-1][1] if groups else 0) == len(sc["subs"][r])
+        for lo, hi, src in groups:
+            assert set(src) == {produced[c] for c in sc["subs"][r][lo:hi]}
+    if not force:  # config 5 at 8 GPUs: the helpers lift the modelled efficiency well above S5's 0.83
+        assert sc["ideal"] / max(sc["model_end"]) > 0.9

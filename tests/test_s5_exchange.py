@@ -42,7 +42,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, cfg=CFG, force=False):
     import torch
     import torch.distributed as dist
 
@@ -51,10 +51,11 @@ def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
-    m, n, p, ba, bc = CFG
+    m, n, p, ba, bc = cfg
     a = random_bcss_device(m, n, ba, 7)
     x = random_matrix_device(p, n, 8)
-    run = S5Runner(m, n, p, ba, bc, rank, world, x.device, exchange="peer")
+    run = S5Runner(m, n, p, ba, bc, rank, world, x.device, exchange="peer", force_helper=force)
+    assert run.exchange == "peer" and (not force or run.sched["helper"])
     run.attach_torch_workspace()
     c = torch.full((run.c_elems,), float("nan"), dtype=torch.float64, device="cuda")
     for _ in range(2):  # twice: buffers and tables are reused across steps
@@ -66,7 +67,7 @@ def _worker(rank, world, port, out):
     parts = [None] * world
     dist.all_gather_object(parts, mine)
     if rank == 0:
-        plan = bs.SttsmPlan(*CFG)
+        plan = bs.SttsmPlan(*cfg)
         want = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
         plan.run(a, x, want)
         want = want.cpu().numpy()
@@ -80,13 +81,17 @@ def _worker(rank, world, port, out):
 
 
 @pytest.mark.gpu
-def test_fused_peer_exchange_two_processes_one_gpu():
+@pytest.mark.parametrize("cfg,force", [(CFG, False), ((4, 64, 32, 16, 16), True)])
+def test_fused_peer_exchange_two_processes_one_gpu(cfg, force):
+    """force=True: rank 0 owns unit 1 and hands child 1 to rank 1 (helper): the
+    T(m-1) peer copy, the helper's start plan and the cross-process event
+    waits all run."""
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, q, cfg, force)) for r in range(2)]
     for pr in procs:
         pr.start()
     for pr in procs:

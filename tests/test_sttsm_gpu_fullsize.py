@@ -234,6 +234,62 @@ def test_s5_partial_plans_reassemble_c_bitwise(cfg_id, world):
     assert torch.equal(c, want)
 
 
+@pytest.mark.parametrize("cfg_id,world,force", [(5, 8, False), (3, 8, True), (4, 8, True)])
+def test_s5_helper_tasks_reassemble_c_bitwise(cfg_id, world, force):
+    """The S5 schedule with helpers on one GPU: an owner computes T(m-1)[u]
+    (top-level plan) and the level-(m-2) children it keeps (start plan with a
+    child subset); its helper computes the handed-over children from a copy of
+    T(m-1)[u]; every release group's subtree plan finishes the C blocks.  The
+    union equals the single-plan C bit for bit."""
+    from paper_1301_7744_b200.distributed import s5_tasks
+    m, n, p, ba, bc = CFG[cfg_id]
+    a = random_bcss_device(m, n, ba, 81 + cfg_id)
+    x = random_matrix_device(p, n, 82 + cfg_id)
+    want = run(CFG[cfg_id], a, x)
+    sc = s5_tasks(m, n, p, ba, bc, world, force_helper=force)
+    assert sc["helper"], "the schedule should hand work to a helper"
+    slices, tops = {}, {}
+
+    def produce(pl, inp):
+        out = torch.empty(pl.c_elems, dtype=torch.float64, device="cuda")
+        pl.run(inp, x, out)
+        calls = pl.level_calls(m - 2)
+        size = out.numel() // len(calls)
+        for i, c in enumerate(calls):
+            assert c not in slices
+            slices[c] = out[i * size:(i + 1) * size]
+        pl.close()
+
+    for r in range(world):
+        for u in sc["owners"][r]:
+            if u in sc["helper"]:
+                pt = bs.SttsmPlan(m, n, p, ba, bc, units=[u], stop_level=m - 1)
+                tops[u] = torch.empty(pt.c_elems, dtype=torch.float64, device="cuda")
+                pt.run(a, x, tops[u])
+                pt.close()
+                produce(bs.SttsmPlan(m, n, p, ba, bc, start_level=m - 1, start_calls=[(u,)],
+                                     start_children=sc["own_children"][u], stop_level=m - 2), tops[u])
+        mine = [u for u in sc["owners"][r] if u not in sc["helper"]]
+        if mine:
+            produce(bs.SttsmPlan(m, n, p, ba, bc, units=mine, stop_level=m - 2), a)
+    for u, (h, kids) in sc["helper"].items():
+        produce(bs.SttsmPlan(m, n, p, ba, bc, start_level=m - 1, start_calls=[(u,)], start_children=kids,
+                             stop_level=m - 2), tops[u].clone())
+    assert len(slices) == sum(u + 1 for u in range(p // bc))
+    c = torch.full_like(want, float("nan"))
+    for r in range(world):
+        for lo, hi, _ in sc["groups"][r]:
+            calls = sc["subs"][r][lo:hi]
+            pl = bs.SttsmPlan(m, n, p, ba, bc, start_level=m - 2, start_calls=calls)
+            part = torch.full_like(want, float("nan"))
+            pl.run(torch.cat([slices[cl] for cl in calls]), x, part)
+            idx = torch.as_tensor(pl.c_block_ranks(), device="cuda")
+            c.view(-1, bc**m)[idx] = part.view(-1, bc**m)[idx]
+            pl.close()
+    torch.cuda.synchronize()
+    assert torch.equal(c, want)
+
+
 @pytest.mark.parametrize("cfg_id", [3, 4])
 def test_unit_subsets_and_workspace_waves_are_bitwise_identical(cfg_id):
     """Plans restricted to unit subsets write exactly their C blocks (others
