@@ -1,7 +1,9 @@
 """Randomized parity sweep (dev tool): random shapes through every execution
 mode - device run, pipelined host run (mirrored order, cascade when chosen),
-pageable staging, reuse=False, a workspace limit that forces waves - against
-the numpy oracle (rel. Frobenius <= 1e-12).
+pageable staging, reuse=False, a workspace limit that forces waves, shard
+plans over random unit subsets (gathered top-level rows), and the S5 helper
+split (top-level plan, then start plans over a random child subset) - against
+the numpy oracle (rel. Frobenius <= 1e-12; partial plans on their own blocks).
 
 usage: python tools/fuzz.py [cases] [seed]
 """
@@ -66,6 +68,35 @@ while done < cases:
             plan.close()
         except MemoryError:
             pass  # a single unit does not fit half the workspace
+    blk = bc**m
+    partial = {}
+    # shard plan over a random subset of top-level units
+    units = sorted(int(u) for u in rng.choice(pbar, size=int(rng.integers(1, pbar + 1)), replace=False))
+    plan = bs.SttsmPlan(m, n, p, ba, bc, units=units)
+    c = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64, device="cuda")
+    plan.run(torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), c)
+    torch.cuda.synchronize()
+    partial["shard"] = (c.cpu().numpy(), plan.c_block_ranks())
+    plan.close()
+    # helper split of one unit: T(m-1)[u] by a stop-level plan, children subset below
+    u = int(rng.integers(0, pbar))
+    kids = sorted(int(j) for j in rng.choice(u + 1, size=int(rng.integers(1, u + 2)), replace=False))
+    top = bs.SttsmPlan(m, n, p, ba, bc, units=[u], stop_level=m - 1)
+    t = torch.empty(top.c_elems, dtype=torch.float64, device="cuda")
+    top.run(torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), t)
+    top.close()
+    plan = bs.SttsmPlan(m, n, p, ba, bc, start_level=m - 1, start_calls=[(u,)], start_children=kids)
+    c = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64, device="cuda")
+    plan.run(t, torch.from_numpy(x).cuda(), c)
+    torch.cuda.synchronize()
+    partial["helper"] = (c.cpu().numpy(), plan.c_block_ranks())
+    plan.close()
+    for k, (v, ranks) in partial.items():
+        idx = np.concatenate([np.arange(r * blk, (r + 1) * blk) for r in ranks]) if len(ranks) else np.zeros(0, int)
+        err = orc.rel_frobenius(v[idx], want[idx]) if len(idx) else 0.0
+        if not (err <= 1e-12):
+            bad += 1
+            print(f"MISMATCH {k} m={m} n={n} p={p} ba={ba} bc={bc}: rel {err:.3e}", flush=True)
     for k, v in modes.items():
         err = orc.rel_frobenius(v, want)
         if not (err <= 1e-12):
