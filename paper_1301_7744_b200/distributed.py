@@ -464,7 +464,9 @@ class S5Runner:
         solo = world == 1 or not dist.is_initialized()
         hg = None
         if not solo:
-            hg = self._host_group = dist.new_group(backend="gloo")  # host-only barriers and handle swaps
+            # host-only barriers and handle swaps over the same ranks as `group`
+            members = None if self.group is None else dist.get_process_group_ranks(self.group)
+            hg = self._host_group = dist.new_group(ranks=members, backend="gloo")
         ok, err = True, ""
         handles = (None, None, None)
         try:
