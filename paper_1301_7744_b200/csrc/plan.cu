@@ -281,6 +281,20 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       }
       L.n_calls = running;
     }
+    // b_a >= 32 levels of few rounds (e.g. config 2, and every level of a
+    // multi-GPU shard) run entirely on 32x256 tiles with 16 consumer warps:
+    // measured faster than the calibrated mix there (config 2: 5.09 -> 5.07
+    // ms; its 8-GPU shards 0.80 -> 0.75 ms) - the finest row granularity
+    // packs the last rounds best; large levels (config 5) keep the mix
+    constexpr int kSmallLevelShape = 5;  // ws32x256c16 (kernel_table.cuh)
+    int level_shape = -1;
+    if (fast_shape && P.bA >= 32 && P.reuse && policy.force < 0 && !getenv("BCSS_NO_SMALL_LEVEL_SHAPE")) {
+      const int bm = shape_bm(kSmallLevelShape), bn = bcss::kFast32[kSmallLevelShape].BN;
+      double items = 0;
+      for (const int4& w : parents) items += (double)((w.z + bm - 1) / bm);
+      items *= (double)L.keys_out * (double)((L.rest + bn - 1) / bn);
+      if (items < 148.0 * 128) level_shape = kSmallLevelShape;
+    }
     // group parents into launches by tile configuration
     std::map<int, LaunchHost> by_cfg;
     for (size_t wi = 0; wi < parents.size(); ++wi) {
@@ -294,7 +308,8 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       const bool gen = fast_shape && !fast && !getenv("BCSS_NO_GEN_TOP");
       unsigned gen_mask = 0;
       for (int g = 0; g < bcss::N_GEN; ++g) gen_mask |= 1u << bcss::BCSS_GEN_OF[g];
-      if (fast) pieces = policy.split(whole.z, P.bA);
+      if (fast && level_shape >= 0) pieces = {{level_shape, whole.z}};
+      else if (fast) pieces = policy.split(whole.z, P.bA);
       else if (gen) pieces = policy.split(whole.z, P.bA, gen_mask);
       else pieces = {{-1, whole.z}};
       int r0 = 0;
