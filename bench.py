@@ -482,8 +482,10 @@ def run_ours(args) -> None:
             line["rank0_flop_share"] = round(my_flops / total_flops, 4)
         if runner is not None:
             line["exchange_bytes_rank0"] = runner.exchange_bytes
-            line["exchange"] = ("fused: owner kernel stores into the assignee's buffer (CUDA IPC)"
+            line["exchange"] = ("fused: producing kernels store into the assignee's buffer (CUDA IPC), "
+                                "cross-rank order by CUDA IPC events"
                                 if runner.exchange == "peer" else "NCCL send/recv")
+            line["s5_helpers"] = {str(u): [h, kids] for u, (h, kids) in runner.sched["helper"].items()}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
