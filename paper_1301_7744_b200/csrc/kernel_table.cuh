@@ -36,9 +36,13 @@ KernelCfg make_cfg(const char* name) {
   X((WsLevelKernel<16, 512, 16, 1, 16, 3, BA>), "ws16x512c16k16") \
   X((WsLevelKernel<64, 256, 16, 2, 8, 5, BA>), "ws64x256c16k16s5") \
   X((WsLevelKernel<96, 128, 32, 3, 4, 3, BA>), "ws96x128c12")      \
-  X((WsLevelKernel<48, 256, 16, 3, 4, 4, BA>), "ws48x256c12k16")
+  X((WsLevelKernel<48, 256, 16, 3, 4, 4, BA>), "ws48x256c12k16")   \
+  X((WsLevelKernel<32, 128, 32, 1, 16, 5, BA>), "ws32x128c16s5")
 
-constexpr int N_SHAPES = 10;
+constexpr int N_SHAPES = 11;
+// shapes the calibrated policy chooses from (shape_costs.hpp); the others
+// serve special roles (ws32x128c16s5: half-width tiles of a launch's last round)
+constexpr int N_POLICY_SHAPES = 10;
 
 // General-redirection variants (reuse=False top level), a subset of the shapes
 // above; BCSS_GEN_OF[i] is the fast shape each one mirrors (its measured cost).

@@ -81,7 +81,7 @@ struct ShapePolicy {
     std::vector<int2> choice(rows + 1, int2{-1, 0});  // {shape, rows of the last tile}
     cost[0] = 0;
     for (int r = 1; r <= rows; ++r)
-      for (int sidx = 0; sidx < N_SHAPES; ++sidx) {
+      for (int sidx = 0; sidx < bcss::N_POLICY_SHAPES; ++sidx) {
         if (!((allowed >> sidx) & 1)) continue;
         const int bm = shape_bm(sidx);
         const int vmax = std::min(bm, r);
@@ -359,6 +359,43 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       if (grouped) X.group_items.push_back((long long)X.items.size());
       L.flops += kv.second.flops;
       L.launches.push_back(std::move(kv.second));
+    }
+    // Tail trim of a single-shape small level: when the launch's last round
+    // would hold only r <= SMs/2 tiles (config 2 level 0: 3264 = 22 x 148 + 8),
+    // those r tiles run as 2r half-width tiles (32x128) in a second launch, so
+    // the level ends half a tile earlier.  Not for chunk-gated / grouped levels
+    // (their item ranges follow keys) - and only when every tile is full.
+    if (level_shape >= 0 && !grouped && L.launches.size() == 1 && (k < P.m - 1 || P.pipeline_waves <= 1) &&
+        P.bC % 32 == 0 && L.rest % 256 == 0 && !getenv("BCSS_NO_TAIL_TRIM")) {
+      static const int sms = [] {
+        int dev = 0, v = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+          cudaGetLastError();
+          return 148;
+        }
+        return v > 0 ? v : 148;
+      }();
+      LaunchHost& X = L.launches[0];
+      const long long total = (long long)X.items.size(), r = total % sms;
+      constexpr int kHalfShape = 10;  // ws32x128c16s5
+      if (total > sms && r > 0 && r <= sms / 2) {
+        LaunchHost T;
+        T.cfg = fast_cfg(P.bA, kHalfShape);
+        T.n_tiles = (int)(L.rest / kernel_cfg(T.cfg).BN);
+        T.parents = X.parents;
+        for (long long i = total - r; i < total; ++i) {
+          const int4 it = X.items[(size_t)i];
+          T.items.push_back(int4{it.x, it.y, 2 * it.z, it.w});
+          T.items.push_back(int4{it.x, it.y, 2 * it.z + 1, it.w});
+        }
+        X.items.resize((size_t)(total - r));
+        const uint64_t per = X.flops / (uint64_t)total;  // every tile is full: equal flops
+        T.flops = per * (uint64_t)r;
+        X.flops -= T.flops;
+        X.item_off.assign({0, (long long)X.items.size()});
+        T.item_off.assign({0, (long long)T.items.size()});
+        L.launches.push_back(std::move(T));
+      }
     }
     if (k == P.m - 1 && P.start_level == 0) {
       prev_suffix.clear();
