@@ -196,6 +196,36 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+def time_transfers(a_h, c_h, dev) -> dict:
+    """the H2D of A and the D2H of C alone (pinned host memory,
+    one copy each into/out of scratch device buffers, CUDA events), so the
+    e2e number can be read against the PCIe floor."""
+    import torch
+
+    try:
+        a_d = torch.empty(a_h.numel(), dtype=torch.float64, device=dev)
+        c_d = torch.zeros(c_h.numel(), dtype=torch.float64, device=dev)
+    except torch.cuda.OutOfMemoryError:
+        torch.cuda.empty_cache()
+        return {"skipped": "no free HBM for the scratch copies"}
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    a_d.copy_(a_h, non_blocking=True)  # warm-up pair (first touch of the copy path)
+    c_h.copy_(c_d, non_blocking=True)
+    torch.cuda.synchronize()
+    ev[0].record()
+    a_d.copy_(a_h, non_blocking=True)
+    ev[1].record()
+    c_h.copy_(c_d, non_blocking=True)
+    ev[2].record()
+    torch.cuda.synchronize()
+    h2d, d2h = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    del a_d, c_d
+    torch.cuda.empty_cache()
+    return {"h2d_a_ms": round(h2d, 3), "h2d_a_gbs": round(a_h.numel() * 8 / h2d / 1e6, 2),
+            "d2h_c_ms": round(d2h, 3), "d2h_c_gbs": round(c_h.numel() * 8 / d2h / 1e6, 2),
+            "note": "one copy each after a warm-up pair, not overlapped with anything"}
+
+
 def run_dense(args, A, X, m, n, p, ba, rank, world, dev, job_ms):
     """Dense mode-product baseline (cuBLAS) on the same inputs, when it fits."""
     import torch
@@ -382,6 +412,7 @@ def run_ours(args) -> None:
             torch.cuda.empty_cache()
         c_h = torch.empty(c_elems, dtype=torch.float64).pin_memory()
         a_np, x_np, c_np = a_h.numpy(), x_h.numpy(), c_h.numpy()
+        xfer = time_transfers(a_h, c_h, dev) if rank == 0 else None
         if runner is not None:
             # S5: host -> every rank's HBM, the sharded step, own C blocks back
             def e2e_step():
@@ -437,7 +468,8 @@ def run_ours(args) -> None:
                             "host buffers, consecutive calls overlapped" if streamed
                        else "SttsmPlan.run_host (C ABI bcss_sttsm_run_host), pinned host buffers"),
                "sync_ms_per_call": round(sync_ms, 3) if sync_ms is not None else None,
-               "pipeline_waves": args.pipeline if (plan_e2e is not None and plan_e2e is not plan) else 0}
+               "pipeline_waves": args.pipeline if (plan_e2e is not None and plan_e2e is not plan) else 0,
+               "transfers": xfer}
         if plan_e2e is not None and plan_e2e is not plan:
             plan_e2e.close()
         del a_h, x_h, c_h
