@@ -126,6 +126,18 @@ def test_drop_in_argument_checks_without_gpu():
     part = bs.PartialSymTensor(2, 4, 2, (2,), payload=np.zeros(3 * 8))
     with pytest.raises(bs.ShapeError):
         bs.sttsm_bcss(part, d["X"], 2)
+    # empty and ragged inputs, as the reference answers them: p = 0 has no
+    # output blocks (ParameterError from simplex_count), X not a p x n matrix
+    with pytest.raises(bs.ParameterError):
+        bs.sttsm_bcss(a, np.zeros((0, 4)), 1)
+    for x in (np.zeros(4), np.zeros((4, 4, 1))):
+        with pytest.raises(bs.ShapeError):
+            bs.sttsm_bcss(a, x, 1)
+    # b_c <= 0: the reference fails with ZeroDivisionError / ParameterError;
+    # here a named BlockDivisibilityError (a ValueError like both)
+    for b_c in (0, -1):
+        with pytest.raises(ValueError):
+            bs.sttsm_bcss(a, d["X"], b_c)
 
 
 def test_status_codes_raise_named_errors():
