@@ -408,6 +408,24 @@ struct WsLevelKernel {
     if (a.k >= 0) return;
 #endif
     const long long tstride = (long long)a.bAk * a.bC;
+#ifndef BCSS_EPI_GENERAL
+    if (a.bAk >= BN && (nt + 1) * BN <= a.rest) {
+      // The whole n-tile lies inside one run of b_A^k contiguous output
+      // columns (b_A^k and BN are powers of two, the tile is BN-aligned):
+      // one base address per fragment row, immediate column offsets.
+      const long long n0 = (long long)nt * BN;
+      const long long tb = (n0 & (a.bAk - 1)) + tstride * (n0 >> kl) + wn * WTN + 2 * (lane & 3);
+#pragma unroll
+      for (int fm = 0; fm < FM; ++fm) {
+        if (roff[fm] == kNoRow) continue;
+        double* p = a.Tout + roff[fm] + tb;
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn)
+          *reinterpret_cast<double2*>(p + fn * 8) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+      }
+      return;
+    }
+#endif
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
       if (roff[fm] == kNoRow) continue;
