@@ -409,12 +409,15 @@ struct WsLevelKernel {
 #endif
     const long long tstride = (long long)a.bAk * a.bC;
 #ifndef BCSS_EPI_GENERAL
-    if (a.bAk >= BN && (nt + 1) * BN <= a.rest) {
-      // The whole n-tile lies inside one run of b_A^k contiguous output
-      // columns (b_A^k and BN are powers of two, the tile is BN-aligned):
-      // one base address per fragment row, immediate column offsets.
-      const long long n0 = (long long)nt * BN;
-      const long long tb = (n0 & (a.bAk - 1)) + tstride * (n0 >> kl) + wn * WTN + 2 * (lane & 3);
+    // (only where the consumers have register headroom beyond the
+    // accumulators and ptxas does not spill for it: not in the 104-register
+    // 16-warp 64x256 / 128x128 shapes, nor in 16x512)
+    const long long c0 = (long long)nt * BN + wn * WTN;  // this warp's first column
+    if (CONS_REGS - FM * FN * 4 >= 64 && BM > 16 && a.bAk >= WTN && c0 + WTN <= a.rest) {
+      // The warp's WTN columns lie inside one run of b_A^k contiguous output
+      // columns (b_A^k and WTN are powers of two, c0 is WTN-aligned): one
+      // base address per fragment row, immediate column offsets.
+      const long long tb = (c0 & (a.bAk - 1)) + tstride * (c0 >> kl) + 2 * (lane & 3);
 #pragma unroll
       for (int fm = 0; fm < FM; ++fm) {
         if (roff[fm] == kNoRow) continue;
