@@ -428,6 +428,24 @@ struct WsLevelKernel {
       }
       return;
     }
+#ifndef BCSS_EPI_L0_OFF  // (A/B switch)
+    if (CONS_REGS - FM * FN * 4 >= 64 && BM > 16 && a.bAk == 1 && !a.mirror_digits && c0 + WTN <= a.rest) {
+      // level 0: GEMM columns are the tail modes at stride b_c
+      const long long ts = tstride;
+      const long long tb = ts * (c0 + 2 * (lane & 3));
+#pragma unroll
+      for (int fm = 0; fm < FM; ++fm) {
+        if (roff[fm] == kNoRow) continue;
+        double* p = a.Tout + roff[fm] + tb;
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) {
+          p[ts * (fn * 8)] = acc[fm][fn][0];
+          p[ts * (fn * 8 + 1)] = acc[fm][fn][1];
+        }
+      }
+      return;
+    }
+#endif
 #endif
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
