@@ -428,6 +428,25 @@ struct WsLevelKernel {
       }
       return;
     }
+#ifndef BCSS_EPI_MID_OFF  // (A/B switch)
+    if (CONS_REGS - FM * FN * 4 >= 64 && BM > 16 && a.bAk >= 8 && c0 + WTN <= a.rest) {
+      // 8 <= b_A^k < WTN: each 8-column fragment lies inside one run and c0
+      // is run-aligned, so fragment fn's offset only depends on fn
+      const long long tb = tstride * (c0 >> kl) + 2 * (lane & 3);
+      long long fo[FN];
+#pragma unroll
+      for (int fn = 0; fn < FN; ++fn) fo[fn] = ((fn * 8) & (a.bAk - 1)) + tstride * ((fn * 8) >> kl);
+#pragma unroll
+      for (int fm = 0; fm < FM; ++fm) {
+        if (roff[fm] == kNoRow) continue;
+        double* p = a.Tout + roff[fm] + tb;
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn)
+          *reinterpret_cast<double2*>(p + fo[fn]) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+      }
+      return;
+    }
+#endif
 #ifndef BCSS_EPI_L0_OFF  // (A/B switch)
     if (CONS_REGS - FM * FN * 4 >= 64 && BM > 16 && a.bAk == 1 && !a.mirror_digits && c0 + WTN <= a.rest) {
       // level 0: GEMM columns are the tail modes at stride b_c
