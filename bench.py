@@ -5,7 +5,9 @@
 
 A *step* is one full ``sttsm_bcss`` (all levels, all C blocks of the
 workload) on device-resident A and X.  Default workload: BASELINE.json
-``configs[1]`` (m=3, n=p=512, b_A=b_C=32, fp64).  With N>1 (launched under
+``configs[4]`` (config 5: m=4, n=512, p=256, b_A=b_C=32, fp64; A is 32.5 GB
+packed), the largest configuration that fits one B200 - the one the metric's
+multi-GPU sharding is quoted on.  With N>1 (launched under
 torch.distributed.run, one rank per GPU) the C blocks are sharded by
 top-level subtree (LPT on exact flops), A and X are broadcast once over NCCL
 before timing, and no collective runs inside the timed region; the total
@@ -28,6 +30,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -45,7 +48,8 @@ CONFIGS = {
     4: (5, 96, 96, 8, 8),
     5: (4, 512, 256, 32, 32),
 }
-DEFAULT_CONFIG = 2  # BASELINE.json configs[1]
+DEFAULT_CONFIG = 5  # BASELINE.json configs[4]: the largest single-GPU configuration
+PARITY_TOL = 1e-12  # BASELINE north star: relative Frobenius, fp64
 SEED = 20261019
 METRIC = "sttsm FP64 GFLOP/s (blocked-alg flops)"
 REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
@@ -79,6 +83,14 @@ def parse_args():
     ap.add_argument("--pipeline", type=int, default=4,
                     help="waves of the e2e transfer/compute pipeline (0 = serial copies)")
     return ap.parse_args()
+
+
+def bench_config(cfg: int, n_gpus: int) -> dict:
+    """The ``config`` object of the JSON line; identical for both arms at the
+    same N (schedule details go in separate keys)."""
+    return dict(workload(cfg),
+                parallelism="single" if n_gpus <= 1 else f"dp{n_gpus}: C blocks sharded over {n_gpus} GPUs",
+                l2="flushed (256 MB write) between timed steps; A and temporaries also exceed L2")
 
 
 def workload(cfg: int) -> dict:
@@ -134,58 +146,125 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+# ---- work accounting of the CPU samples (pure Python, no product import) ------
+# The reference's descend (change_of_basis.py:269-283) makes one _level_product
+# call per suffix; a level-k call contracts, for each of its keys(k) canonical
+# keys and each of the n/b_A chunks, a (b_C x b_A) @ (b_A x rest(k)) product:
+# 2 * b_C * b_A * rest(k) flops, rest(k) = b_A^k * b_C^(m-1-k)
+# (_level_product, change_of_basis.py:185-236; costs.py:83-112 sums the same).
+
+def level_call_flops(m: int, n: int, ba: int, bc: int, k: int) -> int:
+    nbar = n // ba
+    keys = math.comb(nbar + k - 1, k) if k >= 1 else 1
+    return keys * nbar * 2 * bc * ba * ba**k * bc ** (m - 1 - k)
+
+
+def subtree_flops(m: int, n: int, ba: int, bc: int, u: int) -> int:
+    """Levels m-2..0 below the top-level call of unit u (jb_{m-1} = u): the
+    level-k calls are the nondecreasing suffixes ending in u, C(u+m-1-k, m-1-k)."""
+    return sum(math.comb(u + m - 1 - k, m - 1 - k) * level_call_flops(m, n, ba, bc, k) for k in range(m - 1))
+
+
+def unit_flops_port(m: int, n: int, ba: int, bc: int, u: int) -> int:
+    """Whole top-level subtree u: its top-level call plus the levels below."""
+    return level_call_flops(m, n, ba, bc, m - 1) + subtree_flops(m, n, ba, bc, u)
+
+
+def unit_block_mask(m: int, pbar: int, units) -> "np.ndarray":
+    """Packed C blocks (hypertriangle order) whose largest index is in ``units``."""
+    import numpy as np
+    from oracle import bcss_oracle as orc
+
+    us = set(units)
+    return np.array([key[-1] in us for key in orc.hypertriangle(pbar, m)], dtype=bool)
+
+
 def cpu_sample(a_np, x_np, m, n, p, ba, bc, budget_s: float):
-    """Time the oracle port on a bounded sample of the workload: whole
-    top-level subtrees (units jb_{m-1}=j), largest first, until ``budget_s``
-    of CPU time is spent or the workload is complete; returns
-    (GFLOP/s, description, seconds)."""
-    import paper_1301_7744_b200 as bs
+    """Time the oracle port on a bounded sample of the workload - whole
+    top-level subtrees (units jb_{m-1} = u), cheapest first, until
+    ``budget_s`` of CPU time is spent or the workload is complete - on the
+    benchmark's own A and X.  Returns (GFLOP/s, description, seconds, units,
+    oracle C payload) so the caller can check the GPU C of those units
+    against it (the parity of the benchmarked data)."""
     from oracle import bcss_oracle as orc
 
     pbar = p // bc
-    costs = [bs.SttsmPlan(m, n, p, ba, bc, units=[j]).stats()["flops"] for j in range(pbar)]
+    total = orc.bcss_flops(m, n, p, ba, bc)
     done, fl = [], 0
+    c_or = None
     t0 = time.perf_counter()
-    for j in sorted(range(pbar), key=lambda u: -costs[u]):
-        orc.sttsm_bcss_packed(a_np, x_np, m, n, ba, bc, units=[j])
-        done.append(j)
-        fl += costs[j]
+    for u in range(pbar):  # unit costs grow with u
+        c_u = orc.sttsm_bcss_packed(a_np, x_np, m, n, ba, bc, units=[u])
+        c_or = c_u if c_or is None else c_or + c_u  # disjoint blocks, others zero
+        done.append(u)
+        fl += unit_flops_port(m, n, ba, bc, u)
         if time.perf_counter() - t0 >= budget_s:
             break
     dt = time.perf_counter() - t0
-    total = bs.bcss_flops(m, n, p, ba, bc)
     desc = (f"oracle port (numpy, OpenBLAS {os.cpu_count()} threads) on {len(done)} of {pbar} "
-            f"top-level subtrees (jb_{m - 1} in {sorted(done)}): {fl / total:.1%} of the workload's flops")
-    return fl / dt / 1e9, desc, dt
+            f"top-level subtrees (jb_{m - 1} in {done}, all levels): {fl / total:.1%} of the workload's flops, "
+            f"on the benchmark's own A and X")
+    return fl / dt / 1e9, desc, dt, done, fl / total, c_or
 
 
 def run_reference(args) -> None:
+    """The reference arm: the reference algorithm's CPU implementation (the
+    numpy oracle port; the reference package is pure Python and does not
+    travel to the GPU box) on the host cores, rank 0 only.  Imports nothing
+    from the product.
+
+    Setup (untimed): A and X as the ours-arm's config names them, then the
+    whole top-level subtree u = 0 with its temporaries kept.  A step is the
+    subtree below the top-level call of unit 0 - levels m-2..0 from
+    T(m-1)[(0,)], the reference's descend (change_of_basis.py:269-283) -
+    repeated enough times to take about ``per_step`` seconds.  Every BASELINE
+    configuration has b_A = b_C, so every level's per-(key, chunk) product has
+    the same (b x b) @ (b x b^(m-1)) shape and the lower levels' rate is the
+    top level's.  ``value`` = sample flops / sample seconds."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return  # the CPU arm runs once, on rank 0
-    from oracle import bcss_oracle as orc
     import numpy as np
-    import paper_1301_7744_b200 as bs
+
+    from oracle import bcss_oracle as orc
 
     m, n, p, ba, bc = CONFIGS[args.config]
+    nbar = n // ba
+    t0 = time.perf_counter()
     a_np = orc.random_bcss_packed(m, n, ba, SEED)
     x_np = np.random.default_rng(SEED + 1).standard_normal((p, n))
-    per_step = max(1.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    gen_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    _, temps = orc.sttsm_bcss_packed(a_np, x_np, m, n, ba, bc, keep_temps=True, units=[0])
+    setup_s = time.perf_counter() - t0
+    setup_rate = unit_flops_port(m, n, ba, bc, 0) / setup_s / 1e9
+    t_top = orc.pack_temp(temps[(m - 1, (0,))], m - 1, nbar)
+    del a_np, temps
+    sub_fl = subtree_flops(m, n, ba, bc, 0)
+    per_step = max(1.0, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    reps = max(1, round(per_step / max(1e-6, sub_fl / (setup_rate * 1e9))))
+
+    def step() -> float:
+        s0 = time.perf_counter()
+        for _ in range(reps):
+            orc.sttsm_bcss_packed(None, x_np, m, n, ba, bc, start=(m - 1, {(0,): t_top}))
+        return time.perf_counter() - s0
+
     for _ in range(args.warmup):
-        cpu_sample(a_np, x_np, m, n, p, ba, bc, per_step / 4)
-    rates, secs = [], []
-    for _ in range(args.steps):
-        r, desc, dt = cpu_sample(a_np, x_np, m, n, p, ba, bc, per_step)
-        rates.append(r)
-        secs.append(dt)
-    value = sum(r * s for r, s in zip(rates, secs)) / sum(secs)
-    total = bs.bcss_flops(m, n, p, ba, bc)
+        step()
+    secs = [step() for _ in range(args.steps)]
+    value = sub_fl * reps * len(secs) / sum(secs) / 1e9
+    total = orc.bcss_flops(m, n, p, ba, bc)
+    desc = (f"oracle port (numpy, OpenBLAS {os.cpu_count()} threads): per step {reps} x the levels "
+            f"{m - 2}..0 below the top-level call of unit jb_{m - 1}=0 ({sub_fl / 1e9:.1f} GFLOP each, "
+            f"{sub_fl / total:.2%} of the workload) from its kept T({m - 1}); setup (untimed): "
+            f"A generated in {gen_s:.1f} s, unit 0 in full (top level included) at {setup_rate:.2f} GFLOP/s")
     line = {
         "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(total / (value * 1e9) * 1e3, 3), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(workload(args.config), parallelism="cpu"),
+        "config": bench_config(args.config, args.gpus),
         "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": os.cpu_count(),
                          "kind": "port", "sample": desc},
         "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
@@ -224,6 +303,57 @@ def time_transfers(a_h, c_h, dev) -> dict:
     return {"h2d_a_ms": round(h2d, 3), "h2d_a_gbs": round(a_h.numel() * 8 / h2d / 1e6, 2),
             "d2h_c_ms": round(d2h, 3), "d2h_c_gbs": round(c_h.numel() * 8 / d2h / 1e6, 2),
             "note": "one copy each after a warm-up pair, not overlapped with anything"}
+
+
+def dgemm_peak(dev) -> float | None:
+    """cuBLAS DGEMM throughput (8192^3, torch.matmul on fp64) in TFLOP/s."""
+    import torch
+
+    try:
+        a = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        b = torch.randn(8192, 8192, dtype=torch.float64, device=dev)
+        c = torch.empty_like(a)
+        torch.matmul(a, b, out=c)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(5):
+            torch.matmul(a, b, out=c)
+        e1.record()
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        del a, b, c
+        torch.cuda.empty_cache()
+        return 2 * 8192**3 / (ms * 1e-3) / 1e12
+    except Exception:
+        return None
+
+
+def run_dropin(a_pageable, x_np, m, n, ba, bc, c_device, sync_ms) -> dict:
+    """One reference-shaped call ``sttsm_bcss(BcssTensor, ndarray, b_c)`` with
+    pageable inputs, as a reference user makes it: the first call (plan build,
+    device buffers, page-locking the caller's payload in place) and a repeat
+    call on the same tensor (steady state)."""
+    import paper_1301_7744_b200 as bs
+    from oracle import bcss_oracle as orc
+
+    a_t = bs.BcssTensor(m, n, ba, payload=a_pageable)
+    t0 = time.perf_counter()
+    out = bs.sttsm_bcss(a_t, x_np, bc)
+    first = (time.perf_counter() - t0) * 1e3
+    del out
+    t0 = time.perf_counter()
+    out = bs.sttsm_bcss(a_t, x_np, bc)
+    again = (time.perf_counter() - t0) * 1e3
+    rel = orc.rel_frobenius(out.payload, c_device) if c_device is not None else None
+    del out, a_t
+    bs.clear_plan_cache()
+    return {"ms": round(again, 3), "first_call_ms": round(first, 3),
+            "vs_sync_e2e": round(again / sync_ms, 3) if sync_ms else None,
+            "rel_frob_vs_device": float(f"{rel:.3e}") if rel is not None else None,
+            "api": "sttsm_bcss(BcssTensor(payload=pageable ndarray), pageable ndarray X, b_c) -> BcssTensor "
+                   "(the caller's payload is page-locked in place on the first call; C comes back in pooled "
+                   "pinned memory)"}
 
 
 def run_dense(args, A, X, m, n, p, ba, rank, world, dev, job_ms):
@@ -331,6 +461,7 @@ def run_ours(args) -> None:
     step = runner.run if runner is not None else plan.run
 
     peak = bs.probe_fp64_peak()  # live FP64 DMMA peak of this GPU (roofline denominator)
+    dgemm = dgemm_peak(dev) if rank == 0 else None  # cuBLAS DGEMM, the library comparator
 
     # inputs resident in HBM before timing; A and X replicated over NCCL
     if rank == 0 or world == 1:
@@ -395,15 +526,17 @@ def run_ours(args) -> None:
 
     dense_line = run_dense(args, A, X, m, n, p, ba, rank, world, dev, job_ms) if args.dense else None
     noreuse_line = run_noreuse(args, A, X, m, n, p, ba, bc, rank, world, job_ms) if args.noreuse else None
-    a_np_cpu = x_np_cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        a_np_cpu, x_np_cpu = A.cpu().numpy(), X.cpu().numpy()
+    # host copies of the benchmark's own inputs and device result: the CPU
+    # sample / parity check, the drop-in call and the e2e source buffers
+    c_gpu = C.cpu().numpy() if (rank == 0 and world == 1) else None
+    a_pageable, x_np_cpu = A.cpu().numpy(), X.cpu().numpy()
 
     # end to end through the public host-buffer API (pinned host memory)
     e2e = None
+    dropin = None
     if not args.no_e2e:
-        a_h = A.cpu().pin_memory()
-        x_h = X.cpu().pin_memory()
+        a_h = torch.from_numpy(a_pageable).pin_memory()
+        x_h = torch.from_numpy(x_np_cpu).pin_memory()
         if runner is None and world == 1 and args.pipeline:
             # the host path owns its device buffers: release the device-resident run's
             del A, X, C
@@ -473,12 +606,26 @@ def run_ours(args) -> None:
         if plan_e2e is not None and plan_e2e is not plan:
             plan_e2e.close()
         del a_h, x_h, c_h
+        if world == 1 and runner is None:
+            dropin = run_dropin(a_pageable, x_np_cpu, m, n, ba, bc, c_gpu, sync_ms)
 
-    cpu = None
-    if a_np_cpu is not None:
-        rate, desc, dt = cpu_sample(a_np_cpu, x_np_cpu, m, n, p, ba, bc, args.cpu_budget_s)
+    cpu = parity = None
+    if c_gpu is not None and not args.no_cpu_baseline:
+        rate, desc, dt, units, share, c_or = cpu_sample(a_pageable, x_np_cpu, m, n, p, ba, bc, args.cpu_budget_s)
         cpu = {"value": round(rate, 3), "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
                "sample": desc, "seconds": round(dt, 2)}
+        from oracle import bcss_oracle as orc
+
+        mask = unit_block_mask(m, p // bc, units)
+        got, want = c_gpu.reshape(-1, bc**m)[mask], c_or.reshape(-1, bc**m)[mask]
+        rel = orc.rel_frobenius(got, want)
+        parity = {"rel_frob": float(f"{rel:.3e}"), "max_rel": float(f"{orc.max_rel(got, want):.3e}"),
+                  "tol": PARITY_TOL, "ok": bool(rel <= PARITY_TOL), "units": units,
+                  "flop_share": round(share, 4), "c_blocks": int(mask.sum()),
+                  "against": "oracle port (CPU, numpy) on the benchmark's own A and X, C blocks of those units "
+                             "from the timed device run"}
+        if dropin is not None:
+            parity["dropin_vs_device_rel_frob"] = dropin.pop("rel_frob_vs_device")
 
     if rank == 0:
         achieved = launch_fl / (launch_ms * 1e-3) / 1e12
@@ -492,17 +639,20 @@ def run_ours(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(job_ms / args.steps, 4),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": dict(workload(args.config),
-                           parallelism=(f"{schedule} x{world}" if (world > 1 or schedule == "s5") else "single"),
-                           l2="flushed (256 MB write) between timed steps; A and temporaries also exceed L2"),
+            "config": bench_config(args.config, world),
+            "schedule": schedule if (world > 1 or schedule == "s5") else "single plan",
             "roofline": {"bound": "tensor", "achieved": round(achieved, 3), "peak": round(peak, 3),
                          "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                          "peak_source": "FP64 DMMA (mma.sync m8n8k4) probe measured live on this GPU",
+                         "peak_cublas_dgemm": round(dgemm, 3) if dgemm else None,
+                         "frac_vs_cublas_dgemm": round(achieved / dgemm, 4) if dgemm else None,
                          "levels": {str(k): {"tflops": round(v[0] / (v[1] * 1e-3) / 1e12, 3),
                                              "ms_per_step": round(v[1] / args.steps, 4)}
                                     for k, v in sorted(levels.items(), reverse=True)}},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
+            "dropin": dropin,
             "gpu_launches": launches,
             "dense_baseline": dense_line,
             "noreuse_baseline": noreuse_line,
@@ -522,6 +672,8 @@ def run_ours(args) -> None:
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+    if parity is not None and not parity["ok"]:
+        sys.exit(f"parity failure: rel Frobenius {parity['rel_frob']} > {PARITY_TOL}")
 
 
 def main():

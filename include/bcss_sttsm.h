@@ -116,13 +116,15 @@ int bcss_sttsm_run(bcss_plan* plan, const double* A_packed, const double* X, dou
                    void* stream);
 
 /* Host-buffer run (the reference's call shape): copies A and X to the device,
- * runs, copies C back and synchronizes.  Pinned host memory gives full
+ * runs, copies C back and synchronizes.  The host buffers are sized by
+ * bcss_plan_io_elems: A / C for a full plan, the start-level temporaries in
+ * and the stop-level temporaries out for partial plans.  Pinned host memory gives full
  * PCIe bandwidth; pageable memory works too.  With a pipeline set (below) and
  * pinned buffers, the A upload, the compute and the C download overlap.  A
- * plan restricted to some units (bcss_plan_set_units) writes only its own C
- * blocks into C_packed and leaves the others untouched.  A pipelined plan given
- * pageable buffers stages them through plan-owned pinned memory (all host
- * cores) and then runs the pipeline. */
+ * plan restricted to some units (bcss_plan_set_units) or to start calls writes
+ * only its own C blocks into C_packed and leaves the others untouched.  A
+ * pipelined plan given pageable buffers stages those (only) through plan-owned
+ * pinned memory (all host cores) and then runs the pipeline. */
 int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X,
                         double* C_packed);
 /* Streaming form of the pipelined host run (pinned buffers, pipeline set):
@@ -133,6 +135,20 @@ int bcss_sttsm_run_host(bcss_plan* plan, const double* A_packed, const double* X
 int bcss_sttsm_run_host_async(bcss_plan* plan, const double* A_packed, const double* X,
                               double* C_packed);
 int bcss_plan_wait(bcss_plan* plan);
+
+/* Page-lock a caller-owned host range in place (cudaHostRegister), so host
+ * runs read / write it by DMA at PCIe speed instead of staging it through
+ * plan-owned pinned memory.  The drop-in registers a BcssTensor's packed
+ * payload once and unregisters it when the tensor is released; the reference
+ * has no counterpart (its arrays never leave the host).  Already-pinned
+ * ranges are accepted as they are. */
+int bcss_host_register(void* ptr, size_t bytes);
+int bcss_host_unregister(void* ptr);
+/* Pinned host allocations (cudaMallocHost) for results the drop-in returns. */
+int bcss_host_alloc(size_t bytes, void** out_ptr);
+int bcss_host_free(void* ptr);
+/* *out = 1 if ptr is pinned (cudaHostAlloc / registered) host memory. */
+int bcss_host_is_pinned(const void* ptr, int* out);
 
 /* Overlap host transfers with compute in bcss_sttsm_run_host: A is uploaded
  * in chunks (blocks with first index a) that gate the top-level work (and, when

@@ -4,8 +4,10 @@ tensor-core CUDA behind the reference's own entry point and tensor object.
 
 Public surface (reference names, /root/reference/pkg/src/blocksym/__init__.py):
 ``sttsm_bcss``, ``BcssTensor``, ``PartialSymTensor``, ``OpCounter``,
-``hypertriangle_iter``, ``simplex_count``, ``canonicalize``, the error types,
-plus the device-level ``SttsmPlan`` / ``sttsm_bcss_device``.
+``hypertriangle_iter``, ``simplex_count``, ``canonicalize``, ``DenseTensor``,
+``compress`` / ``decompress`` (and the ``_partial`` forms), ``save_bcss`` /
+``load_bcss``, ``temp_to_dense``, the error types, plus the device-level
+``SttsmPlan`` / ``sttsm_bcss_device``.
 """
 
 from .counters import OpCounter
@@ -20,7 +22,17 @@ from .errors import (
     SymmetryError,
 )
 from .indexing import canonicalize, hypertriangle_iter, hypertriangle_rank, hypertriangle_unrank, simplex_count
-from .storage import BcssTensor, PartialSymTensor, packed_payload
+from .dense_tensor import DenseTensor, symmetry_violation
+from .io import load_bcss, save_bcss
+from .storage import (
+    BcssTensor,
+    PartialSymTensor,
+    compress,
+    compress_partial,
+    decompress,
+    decompress_partial,
+    packed_payload,
+)
 from .sttsm import (
     DenseBlockTable,
     SttsmPlan,

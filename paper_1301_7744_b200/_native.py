@@ -57,6 +57,11 @@ SIGNATURES = {
     "bcss_plan_set_call_outputs": (_c_int, [_vp, _P(_vp), _i64]),
     "bcss_sttsm_run_host_async": (_c_int, [_vp, _vp, _vp, _vp]),
     "bcss_plan_wait": (_c_int, [_vp]),
+    "bcss_host_register": (_c_int, [_vp, _sz]),
+    "bcss_host_unregister": (_c_int, [_vp]),
+    "bcss_host_is_pinned": (_c_int, [_vp, _P(_c_int)]),
+    "bcss_host_alloc": (_c_int, [_sz, _P(_vp)]),
+    "bcss_host_free": (_c_int, [_vp]),
     "bcss_device_alloc": (_c_int, [_sz, _P(_vp)]),
     "bcss_device_free": (_c_int, [_vp]),
     "bcss_ipc_get_handle": (_c_int, [_vp, _vp]),

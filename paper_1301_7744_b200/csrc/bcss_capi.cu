@@ -386,9 +386,12 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
   if (!A || !X || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
   const bool can_pipe = P->pipeline_waves > 0 && !P->units_set && !P->keep_temps && P->start_level == 0 &&
                         P->stop_level == 0;
-  if (can_pipe && !(is_pinned(A) && is_pinned(X) && is_pinned(C))) {
-    // pageable buffers: stage through plan-owned pinned memory with all host
-    // cores (the DMA engines then run at PCIe speed and the pipeline applies)
+  const bool pa = is_pinned(A), px = is_pinned(X), pc = is_pinned(C);
+  if (can_pipe && !(pa && px && pc)) {
+    // pageable buffers: stage only those through plan-owned pinned memory
+    // with all host cores (the DMA engines then run at PCIe speed and the
+    // pipeline applies); pinned or registered buffers (bcss_host_register)
+    // are used in place
     const size_t a_b = (size_t)bcss::simplex_count(P->nbar, P->m) * (size_t)ipow(P->bA, P->m) * sizeof(double);
     const size_t x_b = (size_t)(P->p * P->n) * sizeof(double);
     const size_t c_b = (size_t)bcss::simplex_count(P->pbar, P->m) * (size_t)ipow(P->bC, P->m) * sizeof(double);
@@ -402,18 +405,62 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
       return BCSS_OK;
     };
     int st;
-    if ((st = grow_pinned(P->pinA, P->pinA_bytes, a_b))) return st;
-    if ((st = grow_pinned(P->pinX, P->pinX_bytes, x_b))) return st;
-    if ((st = grow_pinned(P->pinC, P->pinC_bytes, c_b))) return st;
+    if (!pa && (st = grow_pinned(P->pinA, P->pinA_bytes, a_b))) return st;
+    if (!px && (st = grow_pinned(P->pinX, P->pinX_bytes, x_b))) return st;
+    if (!pc && (st = grow_pinned(P->pinC, P->pinC_bytes, c_b))) return st;
     // (measured: staging the whole buffers around the pipelined run beats
     // chunk-gated staging overlapped with the DMA on this host's 16 cores)
-    par_copy(P->pinA, A, a_b);
-    memcpy(P->pinX, X, x_b);
-    if ((st = run_host_pinned(P, P->pinA, P->pinX, P->pinC, false))) return st;
-    par_copy(C, P->pinC, c_b);
+    if (!pa) par_copy(P->pinA, A, a_b);
+    if (!px) memcpy(P->pinX, X, x_b);
+    if ((st = run_host_pinned(P, pa ? A : P->pinA, px ? X : P->pinX, pc ? C : P->pinC, false))) return st;
+    if (!pc) par_copy(C, P->pinC, c_b);
     return BCSS_OK;
   }
   return run_host_pinned(P, A, X, C, false);
+}
+
+int bcss_host_register(void* ptr, size_t bytes) {
+  if (!ptr || !bytes) return fail(BCSS_ERR_PARAMETER, "null or empty host range");
+  if (is_pinned(ptr)) return BCSS_OK;
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BCSS_ERR_CUDA, "cudaHostRegister of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  }
+  return BCSS_OK;
+}
+
+int bcss_host_unregister(void* ptr) {
+  if (!ptr) return fail(BCSS_ERR_PARAMETER, "null host pointer");
+  const cudaError_t e = cudaHostUnregister(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(BCSS_ERR_CUDA, "cudaHostUnregister failed: %s", cudaGetErrorString(e));
+  }
+  return BCSS_OK;
+}
+
+int bcss_host_alloc(size_t bytes, void** out_ptr) {
+  if (!out_ptr) return fail(BCSS_ERR_PARAMETER, "null output");
+  *out_ptr = nullptr;
+  const cudaError_t e = cudaMallocHost(out_ptr, std::max<size_t>(bytes, 64));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    *out_ptr = nullptr;
+    return fail(BCSS_ERR_NOMEM, "cudaMallocHost of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
+  }
+  return BCSS_OK;
+}
+
+int bcss_host_free(void* ptr) {
+  if (ptr) CUDA_TRY(cudaFreeHost(ptr));
+  return BCSS_OK;
+}
+
+int bcss_host_is_pinned(const void* ptr, int* out) {
+  if (!out) return fail(BCSS_ERR_PARAMETER, "null output");
+  *out = ptr && is_pinned(ptr) ? 1 : 0;
+  return BCSS_OK;
 }
 
 int bcss_sttsm_run_host_async(bcss_plan* P, const double* A, const double* X, double* C) {
@@ -435,9 +482,14 @@ int bcss_plan_wait(bcss_plan* P) {
 
 static int run_host_pinned(bcss_plan* P, const double* A, const double* X, double* C, bool async) {
   const size_t blk_a = (size_t)ipow(P->bA, P->m);
-  const size_t a_bytes = (size_t)bcss::simplex_count(P->nbar, P->m) * blk_a * sizeof(double);
+  // input / output sizes of this plan: A and C for a full run, the
+  // start-level temporaries in / stop-level temporaries out for partial plans
+  int64_t in_elems = 0, out_elems = 0;
+  int st = bcss_plan_io_elems(P, &in_elems, &out_elems);
+  if (st) return st;
+  const size_t a_bytes = (size_t)in_elems * sizeof(double);
   const size_t x_bytes = (size_t)(P->p * P->n) * sizeof(double);
-  const size_t c_bytes = (size_t)bcss::simplex_count(P->pbar, P->m) * ipow(P->bC, P->m) * sizeof(double);
+  const size_t c_bytes = (size_t)out_elems * sizeof(double);
   auto grow = [&](double*& ptr, size_t& cap, size_t need) -> int {
     if (cap >= need) return BCSS_OK;
     if (ptr) cudaFree(ptr);
@@ -451,7 +503,6 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
     cap = need;
     return BCSS_OK;
   };
-  int st;
   if ((st = grow(P->hA, P->hA_bytes, a_bytes))) return st;
   if ((st = grow(P->hX, P->hX_bytes, x_bytes))) return st;
   if ((st = grow(P->hC, P->hC_bytes, c_bytes))) return st;
@@ -463,7 +514,7 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
     CUDA_TRY(cudaMemcpyAsync(P->hA, A, a_bytes, cudaMemcpyHostToDevice, P->host_stream));
     CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->host_stream));
     if ((st = run_impl(P, P->hA, P->hX, P->hC, P->host_stream, nullptr))) return st;
-    if (P->units_set && P->stop_level == 0) {
+    if ((P->units_set || P->start_level > 0) && P->stop_level == 0) {
       // a shard: only this plan's C blocks come back (runs of consecutive
       // ranks); the caller's other blocks are left as they are
       std::vector<int> ranks;
@@ -488,8 +539,9 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   }
   const auto h0 = std::chrono::steady_clock::now();
   if ((st = build_plan(*P))) return st;
-  // alternate device buffer sets between consecutive calls
-  const int set = (int)(P->host_calls++ & 1);
+  // alternate device buffer sets between consecutive asynchronous calls (a
+  // synchronous call has finished with its set when it returns: set 0)
+  const int set = async ? (int)(P->host_calls++ & 1) : 0;
   double* dA = P->hA;
   double* dX = P->hX;
   double* dC = P->hC;

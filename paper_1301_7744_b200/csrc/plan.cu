@@ -799,7 +799,10 @@ int upload_tables(bcss_plan& P, cudaStream_t stream) {
   int dev;
   CUDA_TRY(cudaGetDevice(&dev));
   if (P.d_tables && P.device == dev) return BCSS_OK;
-  if (P.d_tables) { cudaFree(P.d_tables); P.d_tables = nullptr; }
+  if (P.d_tables || (P.d_ws && P.device >= 0 && P.device != dev))
+    // tables, workspace and host-run buffers live on the device of the first
+    // run; a plan is bound to it
+    return fail(BCSS_ERR_STATE, "plan is bound to device %d but device %d is current", P.device, dev);
   std::vector<char> host(P.tables_bytes, 0);
   for (int k = 0; k < P.m; ++k)
     if (!P.nbr[k].empty()) memcpy(&host[P.nbr_off[k]], P.nbr[k].data(), P.nbr[k].size() * sizeof(int2));

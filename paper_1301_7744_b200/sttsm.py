@@ -22,11 +22,12 @@ from typing import Callable
 
 import numpy as np
 
-from . import _native
+from . import _native, hostmem
 from .costs import bcss_flops, bcss_memops
 from .counters import OpCounter
+from .dense_tensor import DenseTensor
 from .errors import BlockDivisibilityError, ParameterError, ShapeError
-from .indexing import simplex_count
+from .indexing import hypertriangle_iter, simplex_count
 from .storage import BcssTensor, PartialSymTensor, packed_payload
 
 TempHook = Callable[[int, object], None]
@@ -182,13 +183,14 @@ class SttsmPlan:
         nbytes = self.workspace_bytes
         if nbytes == 0:
             return
+        device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         free, _ = torch.cuda.mem_get_info(device)
         if (self._ws is None or self._ws.numel() < nbytes) and nbytes > 0.9 * free:
             # fit the temporaries into the free HBM: more waves, smaller workspace
             _native.check(_native.lib().bcss_plan_set_workspace_limit(self._h, int(0.85 * free)))
             nbytes = self.workspace_bytes
         if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=device or "cuda")
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=device)
         _native.check(_native.lib().bcss_plan_set_workspace(
             self._h, ctypes.c_void_p(self._ws.data_ptr()), self._ws.numel()))
 
@@ -209,10 +211,14 @@ class SttsmPlan:
                 raise ShapeError(f"{name} must be a contiguous float64 CUDA tensor")
             if t.numel() != numel:
                 raise ShapeError(f"{name} has {t.numel()} elements, expected {numel}")
-        if self._ws is None:
-            self.attach_torch_workspace(a.device)
-        s = stream if stream is not None else torch.cuda.current_stream(a.device)
-        self.run_ptr(a.data_ptr(), x.data_ptr(), c.data_ptr(), s.cuda_stream)
+        if not (x.device == a.device and c.device == a.device):
+            raise ShapeError(f"A, X and C must be on one device (got {a.device}, {x.device}, {c.device})")
+        # the library launches on the current device: make it A's
+        with torch.cuda.device(a.device):
+            if self._ws is None:
+                self.attach_torch_workspace(a.device)
+            s = stream if stream is not None else torch.cuda.current_stream(a.device)
+            self.run_ptr(a.data_ptr(), x.data_ptr(), c.data_ptr(), s.cuda_stream)
 
     def run_host(self, a: np.ndarray, x: np.ndarray, c: np.ndarray) -> None:
         """Host buffers in, host buffer out (copies + run + sync in the library)."""
@@ -283,10 +289,10 @@ class DenseBlockTable:
         return out
 
 
-def temp_to_dense(temp) -> np.ndarray:
-    """Dense array of a temporary handed to ``temp_hook`` (either flavour);
+def temp_to_dense(temp) -> DenseTensor:
+    """Dense tensor of a temporary handed to ``temp_hook`` (either flavour);
     counterpart of the reference's ``temp_to_dense`` (change_of_basis.py:170-182)."""
-    return temp.to_dense()
+    return DenseTensor(temp.to_dense())
 
 
 def _check_args(a, x) -> tuple[int, int, int]:
@@ -306,21 +312,31 @@ def _check_args(a, x) -> tuple[int, int, int]:
 
 
 def sttsm_bcss(a, x, b_c: int, counter: OpCounter | None = None, reuse: bool = True,
-               temp_hook: TempHook | None = None) -> BcssTensor:
+               temp_hook: TempHook | None = None):
     """Blocked change of basis over compact symmetric storage, on the GPU.
 
-    Same contract as the reference ``sttsm_bcss``: returns a fresh
-    ``BcssTensor`` of order m, dimension p, block dimension ``b_c``; inputs
-    are not modified.
+    Same contract as the reference ``sttsm_bcss``: returns a fresh BCSS
+    tensor of order m, dimension p, block dimension ``b_c``; inputs are not
+    modified.  The result is this package's ``BcssTensor`` (payload in pinned
+    host memory), or - when ``a`` is the reference package's own
+    ``BcssTensor`` - an object of that same class, so reference code
+    (``decompress``, ``save_bcss``, ``cli.compare_bcss_dense``) consumes it
+    unchanged.
     """
     x = np.asarray(x, dtype=np.float64)
     m, n, p = _check_args(a, x)
     b_a = a.b
     if b_c < 1 or p % b_c != 0:
         raise BlockDivisibilityError(f"output block dimension {b_c} does not divide {p}")
-    a_payload = np.ascontiguousarray(packed_payload(a), dtype=np.float64)
+    a_payload = packed_payload(a)
+    if not (a_payload.dtype == np.float64 and a_payload.flags.c_contiguous):
+        a_payload = np.ascontiguousarray(a_payload, dtype=np.float64)
+    elif isinstance(a, PartialSymTensor):
+        # page-lock the caller's payload in place for the tensor's lifetime:
+        # this and later calls DMA it without a staging copy
+        hostmem.register(a, a_payload)
     xc = np.ascontiguousarray(x)
-    c_payload = np.empty(simplex_count(p // b_c, m) * b_c**m, dtype=np.float64)
+    c_payload = hostmem.host_empty(simplex_count(p // b_c, m) * b_c**m)
     if temp_hook is not None:
         plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, keep_temps=True)
         try:
@@ -335,7 +351,25 @@ def sttsm_bcss(a, x, b_c: int, counter: OpCounter | None = None, reuse: bool = T
     if counter is not None:
         counter.count_flops(bcss_flops(m, n, p, b_a, b_c, reuse))
         counter.count_memops(bcss_memops(m, n, p, b_a, b_c, reuse))
+    if not isinstance(a, PartialSymTensor):
+        foreign = _foreign_result(type(a), m, p, b_c, c_payload)
+        if foreign is not None:
+            return foreign
     return BcssTensor(m, p, b_c, payload=c_payload)
+
+
+def _foreign_result(cls, m: int, p: int, b_c: int, c_payload: np.ndarray):
+    """The result as an instance of the caller's BCSS class (the reference's
+    ``BcssTensor(order, dim, block_dim, blocks)``, storage.py:155-159), its
+    blocks F-order views of the packed result; None if that class cannot be
+    built that way."""
+    bs = b_c**m
+    blocks = {key: c_payload[r * bs:(r + 1) * bs].reshape((b_c,) * m, order="F")
+              for r, key in enumerate(hypertriangle_iter(p // b_c, m))}
+    try:
+        return cls(m, p, b_c, blocks)
+    except Exception:
+        return None
 
 
 # Plans (tables + device workspace + transfer buffers) are reused across
