@@ -305,6 +305,64 @@ def time_transfers(a_h, c_h, dev) -> dict:
             "note": "one copy each after a warm-up pair, not overlapped with anything"}
 
 
+def run_e2e_sharded(args, A, X, C, plan, runner, m, n, p, ba, bc, rank, world, dev, total_flops) -> dict:
+    """Multi-GPU end to end: every rank holds (pinned) and uploads only its
+    pieces of A over its own PCIe link, the pieces reach the other GPUs by
+    NCCL broadcast over NVLink (ShardedInput), the top level starts per key
+    group as the chunks it reads land (bcss_sttsm_run_gated), and each rank
+    downloads its own C blocks.  One synchronous step per call, device-timed
+    per rank (CUDA events around the whole step), max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1301_7744_b200.distributed import OwnBlocksDownload, ShardedInput
+
+    shard = ShardedInput(m, n, ba, rank, world, dev)
+    for i in shard.mine:  # this rank's share of A into its pinned host buffer
+        lo, hi, _ = shard.pieces[i]
+        o = shard.host_off[i]
+        shard.host[o:o + hi - lo].copy_(A[lo:hi])
+    x_h = X.cpu().pin_memory()
+    ranks = runner.c_block_ranks() if runner is not None else plan.c_block_ranks()
+    down = OwnBlocksDownload(ranks, bc**m)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(e0=None):
+        X.copy_(x_h, non_blocking=True)
+        evs = shard.start(A, after=e0)
+        if runner is not None:
+            runner.run(A, X, C, gate_events=evs)
+        else:
+            plan.run_gated(A, X, C, evs, stream)
+        down.start(C, stream)
+
+    for _ in range(2):
+        step()
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms = 0.0
+    for _ in range(args.steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step(e0)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms += e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item()) / args.steps
+    sizes = torch.tensor([shard.host_bytes + x_h.numel() * 8, down.elems * 8], dtype=torch.float64, device=dev)
+    dist.all_reduce(sizes)
+    return {"value": round(total_flops / (ms * 1e-3) / 1e9, 3), "unit": "GFLOP/s",
+            "h2d_bytes_per_step": int(sizes[0].item()), "d2h_bytes_per_step": int(sizes[1].item()),
+            "ms_per_step": round(ms, 3), "h2d_bytes_rank0": shard.host_bytes + x_h.numel() * 8,
+            "api": "ShardedInput (each rank uploads its pieces of A, pinned, over its own PCIe link; NCCL "
+                   "broadcast per piece over NVLink) + gated run (bcss_sttsm_run_gated: top-level key groups "
+                   "wait for the chunks they read) + D2H of the rank's own C blocks; one synchronous step "
+                   "per call, CUDA-event timed, max over ranks",
+            "pieces": len(shard.pieces)}
+
+
 def dgemm_peak(dev) -> float | None:
     """cuBLAS DGEMM throughput (8192^3, torch.matmul on fp64) in TFLOP/s."""
     import torch
@@ -529,12 +587,15 @@ def run_ours(args) -> None:
     # host copies of the benchmark's own inputs and device result: the CPU
     # sample / parity check, the drop-in call and the e2e source buffers
     c_gpu = C.cpu().numpy() if (rank == 0 and world == 1) else None
-    a_pageable, x_np_cpu = A.cpu().numpy(), X.cpu().numpy()
+    a_pageable = A.cpu().numpy() if world == 1 else None  # N>1: no rank holds a full host copy of A
+    x_np_cpu = X.cpu().numpy()
 
     # end to end through the public host-buffer API (pinned host memory)
     e2e = None
     dropin = None
-    if not args.no_e2e:
+    if not args.no_e2e and world > 1:
+        e2e = run_e2e_sharded(args, A, X, C, plan, runner, m, n, p, ba, bc, rank, world, dev, total_flops)
+    elif not args.no_e2e:
         a_h = torch.from_numpy(a_pageable).pin_memory()
         x_h = torch.from_numpy(x_np_cpu).pin_memory()
         if runner is None and world == 1 and args.pipeline:

@@ -115,6 +115,18 @@ int bcss_plan_stats(bcss_plan* plan, int64_t* waves, int64_t* launches, uint64_t
 int bcss_sttsm_run(bcss_plan* plan, const double* A_packed, const double* X, double* C_packed,
                    void* stream);
 
+/* Device-resident run whose input A is still arriving: chunk_events[a]
+ * (cudaEvent_t, one per first block index a = 0..n/b_a-1) fires once the
+ * blocks of A whose first index is a (one contiguous range of the packed
+ * payload) are resident.  The top level's key groups wait only for the
+ * chunks they read (a key of first index a reads chunks 0..a), so the
+ * compute overlaps the rest of the transfer - e.g. the per-chunk NCCL
+ * broadcasts of the multi-GPU host path, where every rank uploads only its
+ * share of A over its own PCIe link.  Results are bit-identical to
+ * bcss_sttsm_run.  Plans that start below A (start calls) ignore the events. */
+int bcss_sttsm_run_gated(bcss_plan* plan, const double* A_packed, const double* X, double* C_packed,
+                         void* stream, const void* const* chunk_events, int n_events);
+
 /* Host-buffer run (the reference's call shape): copies A and X to the device,
  * runs, copies C back and synchronizes.  The host buffers are sized by
  * bcss_plan_io_elems: A / C for a full plan, the start-level temporaries in

@@ -52,6 +52,7 @@ SIGNATURES = {
     "bcss_plan_stats": (_c_int, [_vp, _P(_i64), _P(_i64), _P(_u64), _P(_i64)]),
     "bcss_sttsm_run": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
     "bcss_sttsm_run_host": (_c_int, [_vp, _vp, _vp, _vp]),
+    "bcss_sttsm_run_gated": (_c_int, [_vp, _vp, _vp, _vp, _vp, _P(_vp), _c_int]),
     "bcss_plan_set_pipeline": (_c_int, [_vp, _c_int]),
     "bcss_plan_set_stop_level": (_c_int, [_vp, _c_int]),
     "bcss_plan_set_call_outputs": (_c_int, [_vp, _P(_vp), _i64]),

@@ -87,6 +87,7 @@ int bcss_plan_create(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int 
   *out_plan = nullptr;
   int st = validate_problem(m, n, p, b_a, b_c);
   if (st) return st;
+  if ((st = check_int32_limits(m, n, p, b_a, b_c, reuse != 0))) return st;
   bcss_plan* P = new (std::nothrow) bcss_plan();
   if (!P) return fail(BCSS_ERR_NOMEM, "out of host memory");
   P->m = m; P->n = n; P->p = p; P->bA = b_a; P->bC = b_c;
@@ -197,6 +198,23 @@ int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, v
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
   if (!A || !X_ || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
   return run_impl(P, A, X_, C, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+int bcss_sttsm_run_gated(bcss_plan* P, const double* A, const double* X_, double* C, void* stream,
+                         const void* const* chunk_events, int n_events) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  if (!A || !X_ || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");
+  if (n_events != (int)P->nbar || !chunk_events)
+    return fail(BCSS_ERR_SHAPE, "%d chunk events for %lld first-index chunks of A", n_events, (long long)P->nbar);
+  for (int a = 0; a < n_events; ++a)
+    if (!chunk_events[a]) return fail(BCSS_ERR_PARAMETER, "null event for chunk %d", a);
+  if (P->start_level > 0)  // nothing reads A: a plain run
+    return run_impl(P, A, X_, C, static_cast<cudaStream_t>(stream), nullptr);
+  std::vector<cudaEvent_t> evs((size_t)n_events);
+  for (int a = 0; a < n_events; ++a) evs[(size_t)a] = static_cast<cudaEvent_t>(const_cast<void*>(chunk_events[a]));
+  Pipe pipe;  // no per-wave downloads; the caller reads C after the run
+  pipe.chunk_ev = evs.data();
+  return run_impl(P, A, X_, C, static_cast<cudaStream_t>(stream), &pipe);
 }
 
 int bcss_plan_set_stop_level(bcss_plan* P, int stop_level) {

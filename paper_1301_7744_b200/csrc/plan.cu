@@ -854,7 +854,8 @@ double* region_for(bcss_plan& P, const WaveHost& W, int k) {
 
 int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c) {
   if (m < 2) return fail(BCSS_ERR_PARAMETER, "change of basis is defined for order >= 2");
-  if (m > 8) return fail(BCSS_ERR_PARAMETER, "order %d > 8 is not supported", m);
+  // the neighbour-table code word packs each mode's stored position in 3 bits
+  if (m > 8) return fail(BCSS_ERR_PARAMETER, "order %d > 8 is not supported (at most 8 modes)", m);
   if (n < 1 || p < 1 || b_a < 1 || b_c < 1)
     return fail(BCSS_ERR_PARAMETER, "dimensions and block dimensions must be positive");
   if (n % b_a != 0) return fail(BCSS_ERR_BLOCK_DIVISIBILITY, "block dimension %lld does not divide %lld", (long long)b_a, (long long)n);
@@ -863,6 +864,33 @@ int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c) {
   const double blk = std::pow((double)std::max(b_a, b_c), m);
   if (blk >= 2147483647.0) return fail(BCSS_ERR_PARAMETER, "block of %g elements exceeds the int32 block offset range", blk);
   if (n > (1 << 30) || p > (1 << 30)) return fail(BCSS_ERR_PARAMETER, "dimension too large");
+  return BCSS_OK;
+}
+
+// The device tables hold block ranks, key indices, call indices and C block
+// ranks as int32 (nbr {rank, code}, work items {parent, key, ..}, parents
+// {in_call, row0, rows, child_off}, child_call): reject problems whose counts
+// would not fit instead of truncating them.
+int check_int32_limits(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, bool reuse) {
+  const int64_t nbar = n / b_a, pbar = p / b_c, lim = INT32_MAX;
+  auto too_big = [&](const char* what, long double v) {
+    return fail(BCSS_ERR_PARAMETER, "%s (%.4Lg) exceeds the int32 range of the device tables", what, v);
+  };
+  try {
+    // blocks of A and C (ranks in the neighbour table / child_call)
+    if (bcss::simplex_count(nbar, m) > lim) return too_big("number of canonical blocks of A", (long double)bcss::simplex_count(nbar, m));
+    if (bcss::simplex_count(pbar, m) > lim) return too_big("number of canonical blocks of C", (long double)bcss::simplex_count(pbar, m));
+    for (int k = 1; k < m; ++k) {
+      // keys of T(k) (work-item key, neighbour rank into T(k+1))
+      const long double keys = reuse ? (long double)bcss::simplex_count(nbar, k) : powl((long double)nbar, k);
+      if (keys * nbar > lim) return too_big("neighbour-table entries of one level", keys * nbar);
+      // calls of level k (call indices), and rows of one parent (child rows)
+      if (bcss::simplex_count(pbar, m - k) > lim) return too_big("calls of one level", (long double)bcss::simplex_count(pbar, m - k));
+    }
+    if ((long double)pbar * b_c > lim) return too_big("rows of one parent", (long double)pbar * b_c);
+  } catch (const std::exception& e) {
+    return fail(BCSS_ERR_PARAMETER, "problem size overflows: %s", e.what());
+  }
   return BCSS_OK;
 }
 

@@ -196,6 +196,7 @@ int upload_tables(bcss_plan& P, cudaStream_t stream);
 int ensure_workspace(bcss_plan& P);
 double* region_for(bcss_plan& P, const WaveHost& W, int k);
 int validate_problem(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c);
+int check_int32_limits(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, bool reuse);
 void invalidate(bcss_plan* P);
 int64_t first_rank_with(int64_t a, int m, int64_t extent);
 bool is_pinned(const void* p);
@@ -205,7 +206,10 @@ bool is_pinned(const void* p);
 // is split by key ranges that need only the chunks already landed, and each
 // wave's C blocks are downloaded while later waves compute.
 struct Pipe {
-  double* c_host = nullptr;
+  double* c_host = nullptr;         // per-wave C downloads go here (null: no downloads)
+  // A chunk a (blocks with first index a) is resident once chunk_ev[a] fired;
+  // null = the plan's own upload events (run_host)
+  const cudaEvent_t* chunk_ev = nullptr;
   // BCSS_TRACE=1: completion events (name, event) polled after the run
   std::vector<std::pair<std::string, cudaEvent_t>>* trace = nullptr;
 };

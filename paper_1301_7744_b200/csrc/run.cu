@@ -114,6 +114,7 @@ int64_t first_rank_with(int64_t a, int m, int64_t extent) {
 int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStream_t s, const Pipe* pipe) {
   int st = build_plan(*P);
   if (st) return st;
+  const cudaEvent_t* chunk_ev = pipe && pipe->chunk_ev ? pipe->chunk_ev : P->chunk_ev.data();
   // Without a caller workspace or an explicit limit, fit the temporaries into
   // the free HBM by splitting the units into more waves.
   if (!P->d_ws && P->ws_limit == 0 && !P->keep_temps && P->start_level == 0 && P->stop_level == 0) {
@@ -150,7 +151,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       P->dXm_bytes = xb;
     }
     // pipelined host run: X is uploaded on copy_in ahead of A chunk 0
-    if (pipe) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev[0], 0));
+    if (pipe) CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[0], 0));
     reverse_row_blocks<<<296, 256, 0, s>>>(X_, P->dXm, P->p, P->n, P->bC);
     CUDA_TRY(cudaGetLastError());
     X_ = P->dXm;
@@ -164,7 +165,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       CUDA_TRY(cudaMalloc(&P->dXt, xb));
       P->dXt_bytes = xb;
     }
-    if (pipe) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev[0], 0));  // X was uploaded ahead of A chunk 0
+    if (pipe) CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[0], 0));  // X was uploaded ahead of A chunk 0
     const int* rows = reinterpret_cast<const int*>(static_cast<char*>(P->d_tables) + P->off_gather_rows);
     gather_row_blocks<<<296, 256, 0, s>>>(X_, P->dXt, rows, (long long)P->gather_rows.size(), P->n, P->bC);
     CUDA_TRY(cudaGetLastError());
@@ -237,7 +238,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         for (int g = 0; g < G; ++g) {
           cudaStream_t ls = P->lvl_stream[2 * L.k + (g & 1)];
           if (L.k == P->m - 1) {
-            CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[P->group_a[g + 1] - 1], 0));
+            CUDA_TRY(cudaStreamWaitEvent(ls, chunk_ev[P->group_a[g + 1] - 1], 0));
           } else {  // groups <= g of level k+1: g on one stream, g-1 (and earlier) on the other
             CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g], 0));
             if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g - 1], 0));
@@ -281,7 +282,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       // product key K reads blocks whose first index is min(K), not K[0]
       bool gate_split = gate && P->reuse;
       for (const LaunchHost& X : L.launches) gate_split = gate_split && X.parents.size() == 1;
-      if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, P->chunk_ev.back(), 0));
+      if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[P->nbar - 1], 0));
       const bool conc = (P->concurrent && nl > 1) || gate_split;
       if (conc && (st = ensure_side(P, std::max(nl - 1, 1)))) return st;
       if (P->timing) {
@@ -313,7 +314,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
             const int64_t per_key = X.item_off.back() / L.keys_out;
             if (per_key == 0 || k_hi <= k_lo) continue;
             cudaStream_t ls = (sub++ % 2 == 0) ? s : P->side[0];
-            CUDA_TRY(cudaStreamWaitEvent(ls, P->chunk_ev[a1 - 1], 0));
+            CUDA_TRY(cudaStreamWaitEvent(ls, chunk_ev[a1 - 1], 0));
             if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, ls, sms)))
               return st;
             ++launches;
@@ -342,7 +343,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       }
       ++level_idx;
       trace_mark(pipe, "wave" + std::to_string(wi) + " level" + std::to_string(L.k) + " done", s);
-      if (pipe && L.k == 0) {
+      if (pipe && L.k == 0 && pipe->c_host) {
         // this wave's C blocks are final: download them (runs of consecutive ranks)
         while (P->wave_ev.size() <= wi) {  // the plan may have been rebuilt with more waves
           cudaEvent_t ev;
@@ -365,6 +366,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
           i = j;
         }
         trace_mark(pipe, "wave" + std::to_string(wi) + " C downloaded", P->copy_out);
+      }
+      if (pipe && L.k == 0) {
         if (cascade) {
           // deferred top-level rows of the later waves, then every later wave
           // may read T(m-1)
@@ -382,8 +385,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         }
         // submit what is queued so far (the driver otherwise batches it until a sync)
         cudaStreamQuery(s);
-        cudaStreamQuery(P->copy_out);
-        cudaStreamQuery(P->copy_out2);
+        if (P->copy_out) cudaStreamQuery(P->copy_out);
+        if (P->copy_out2) cudaStreamQuery(P->copy_out2);
       }
     }
   }

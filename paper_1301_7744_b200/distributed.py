@@ -269,6 +269,164 @@ def s5_tasks(m: int, n: int, p: int, b_a: int, b_c: int, world: int, reuse: bool
             "help_of": help_of, "subs": subs, "groups": groups, "model_end": free, "ideal": ideal}
 
 
+# ---- multi-GPU host input: sharded upload + NVLink broadcast ---------------------
+#
+# Every C block depends on all of A, so every GPU needs all of A; on one node
+# the host -> device links are per GPU (PCIe Gen5 x16, ~55 GB/s each) while
+# NVLink/NVSwitch moves ~700 GB/s per GPU.  So the packed A is cut into
+# pieces of equal size (at block boundaries), dealt round-robin to the ranks;
+# rank r holds and uploads only its pieces, and every piece reaches the other
+# GPUs by one NCCL broadcast from its owner, in ascending order.  Consecutive
+# pieces belong to different ranks, so all PCIe links work in parallel and
+# the front of A - what the top level's first key groups read (a key of first
+# index a reads the first-index chunks 0..a, io.py:53-55 order) - lands first
+# on every GPU.  The plan's top level waits per key group on per-chunk events
+# (bcss_sttsm_run_gated), so the compute overlaps the rest of the transfer.
+
+def chunk_elems(m: int, n: int, b_a: int) -> list[int]:
+    """Elements of A's first-index chunks a = 0..n/b_a-1 (packed order)."""
+    from math import comb
+
+    nbar = n // b_a
+    return [comb(nbar - a + m - 2, m - 1) * b_a**m for a in range(nbar)]
+
+
+def input_pieces(m: int, n: int, b_a: int, world: int, per_rank: int = 8, min_pieces: int = 32):
+    """(lo, hi, owner) element ranges of packed A: max(per_rank*world,
+    min_pieces) pieces of equal block counts, owner = piece index mod world."""
+    from math import comb
+
+    nbar = n // b_a
+    blocks = comb(nbar + m - 1, m)
+    q = max(1, min(blocks, max(per_rank * world, min_pieces)))
+    blk = b_a**m
+    cuts = [blocks * i // q for i in range(q + 1)]
+    return [(cuts[i] * blk, cuts[i + 1] * blk, i % world) for i in range(q) if cuts[i + 1] > cuts[i]]
+
+
+def chunk_ready_piece(m: int, n: int, b_a: int, pieces) -> list[int]:
+    """For every first-index chunk a, the index of the piece after whose
+    arrival (pieces arrive in order) all of chunk a is resident."""
+    sizes = chunk_elems(m, n, b_a)
+    out, end = [], 0
+    for e in sizes:
+        end += e
+        out.append(next(i for i, (_, hi, _) in enumerate(pieces) if hi >= end))
+    return out
+
+
+class ShardedInput:
+    """One rank's share of A for the multi-GPU host path.
+
+    Holds (pinned) only the pieces this rank owns (``input_pieces``); ``start``
+    uploads them into the device copy of A on a copy stream and enqueues, for
+    every piece in ascending order, an NCCL broadcast from its owner on a
+    communication stream, recording the event of first-index chunk a once
+    its last piece is resident.  With one rank it is a chunked upload with
+    the same per-chunk events.
+    """
+
+    def __init__(self, m: int, n: int, b_a: int, rank: int, world: int, device, group=None):
+        import torch
+
+        self.m, self.n, self.b_a, self.rank, self.world, self.group = m, n, b_a, rank, world, group
+        self.device = torch.device(device)
+        self.nbar = n // b_a
+        self.pieces = input_pieces(m, n, b_a, world)
+        self.chunk_done_after = chunk_ready_piece(m, n, b_a, self.pieces)
+        self.mine = [i for i, (_, _, r) in enumerate(self.pieces) if r == rank]
+        self.host_off = {}
+        off = 0
+        for i in self.mine:
+            lo, hi, _ = self.pieces[i]
+            self.host_off[i] = off
+            off += hi - lo
+        self.host = torch.empty(max(1, off), dtype=torch.float64, pin_memory=True)
+        self.h2d = torch.cuda.Stream(device=self.device)
+        self.comm = torch.cuda.Stream(device=self.device)
+        self.up_ev = {i: torch.cuda.Event() for i in self.mine}
+        self.chunk_ev = [torch.cuda.Event() for _ in range(self.nbar)]
+        self._src = [r for _, _, r in self.pieces]
+        if world > 1:
+            import torch.distributed as dist
+
+            ranks = dist.get_process_group_ranks(group) if group is not None else list(range(world))
+            self._src = [ranks[r] for r in self._src]  # global ranks of the owners
+
+    @property
+    def host_bytes(self) -> int:
+        return 8 * sum(self.pieces[i][1] - self.pieces[i][0] for i in self.mine)
+
+    def fill_from(self, a_full) -> None:
+        """Copy this rank's pieces out of a full packed A (numpy or torch, host)."""
+        import torch
+
+        src = torch.as_tensor(a_full).reshape(-1)
+        for i in self.mine:
+            lo, hi, _ = self.pieces[i]
+            o = self.host_off[i]
+            self.host[o:o + hi - lo].copy_(src[lo:hi])
+
+    def start(self, a_dev, after=None) -> list:
+        """Enqueue this step's uploads and broadcasts into ``a_dev`` (the
+        device copy of packed A); returns the per-chunk events.  ``after``
+        (a torch.cuda.Event) orders them behind earlier readers of ``a_dev``."""
+        import torch
+
+        if after is not None:
+            self.h2d.wait_event(after)
+            self.comm.wait_event(after)
+        with torch.cuda.stream(self.h2d):
+            for i in self.mine:
+                lo, hi, _ = self.pieces[i]
+                o = self.host_off[i]
+                a_dev[lo:hi].copy_(self.host[o:o + hi - lo], non_blocking=True)
+                self.up_ev[i].record(self.h2d)
+        done = {}
+        for a, i in enumerate(self.chunk_done_after):
+            done.setdefault(i, []).append(a)
+        with torch.cuda.stream(self.comm):
+            for i, (lo, hi, r) in enumerate(self.pieces):
+                if r == self.rank:
+                    self.comm.wait_event(self.up_ev[i])
+                if self.world > 1:
+                    import torch.distributed as dist
+
+                    work = dist.broadcast(a_dev[lo:hi], src=self._src[i], group=self.group, async_op=True)
+                    work.wait()  # the comm stream waits for the collective (the host does not block)
+                for a in done.get(i, ()):
+                    self.chunk_ev[a].record(self.comm)
+        return self.chunk_ev
+
+
+class OwnBlocksDownload:
+    """D2H of the C blocks one rank computed (runs of consecutive packed
+    ranks) into a compact pinned buffer."""
+
+    def __init__(self, ranks, blk_c: int):
+        import torch
+
+        r = np.sort(np.asarray(ranks, dtype=np.int64))
+        self.runs = []  # (device element offset, host element offset, elements)
+        h, i = 0, 0
+        while i < len(r):
+            j = i + 1
+            while j < len(r) and r[j] == r[j - 1] + 1:
+                j += 1
+            self.runs.append((int(r[i]) * blk_c, h, (j - i) * blk_c))
+            h += (j - i) * blk_c
+            i = j
+        self.host = torch.empty(max(1, h), dtype=torch.float64, pin_memory=True)
+        self.elems = h
+
+    def start(self, c_dev, stream) -> None:
+        import torch
+
+        with torch.cuda.stream(stream):
+            for d, h, e in self.runs:
+                self.host[h:h + e].copy_(c_dev[d:d + e], non_blocking=True)
+
+
 def _gpu_compute(plan: SttsmPlan, inp, x, out) -> None:
     plan.run(inp, x, out)
 
@@ -566,12 +724,19 @@ class S5Runner:
                         stream.wait_event(self._ev_peer[(q, tag)])
             self.compute(pl, self.inp[lo * s:hi * s], x, c)
 
-    def _run_ptr(self, pl: SttsmPlan, inp_ptr: int, x, out_ptr: int, stream) -> None:
+    def _run_ptr(self, pl: SttsmPlan, inp_ptr: int, x, out_ptr: int, stream, gate=None) -> None:
         if pl._ws is None:
             pl.attach_torch_workspace(x.device)
-        pl.run_ptr(inp_ptr, x.data_ptr(), out_ptr, stream.cuda_stream)
+        if gate is not None:
+            pl.run_gated_ptr(inp_ptr, x.data_ptr(), out_ptr, gate, stream.cuda_stream)
+        else:
+            pl.run_ptr(inp_ptr, x.data_ptr(), out_ptr, stream.cuda_stream)
 
-    def run(self, a, x, c) -> None:
+    def run(self, a, x, c, gate_events=None) -> None:
+        """One step on the current stream.  ``gate_events`` (one per
+        first-index chunk of A, ``ShardedInput.start``): the plans that read A
+        wait per top-level key group for the chunks they need instead of for
+        all of A."""
         import torch.distributed as dist
 
         s = self.slice
@@ -593,7 +758,7 @@ class S5Runner:
             # every call has a destination, so a producer's output buffer is never touched
             sink = self.inp.data_ptr()
             if self.plan_top is not None:
-                self._run_ptr(self.plan_top, a.data_ptr(), x, self.t_top.data_ptr(), stream)
+                self._run_ptr(self.plan_top, a.data_ptr(), x, self.t_top.data_ptr(), stream, gate_events)
                 if self.top_dst is not None:  # T(m-1)[u] -> helper over NVLink, beside the level work
                     self._ev_top.record(stream)
                     self._side.wait_event(self._ev_top)
@@ -606,7 +771,7 @@ class S5Runner:
                         stream.wait_stream(self._side)  # one process: the helper task follows on this stream
                 self._run_ptr(self.plan_lvl, self.t_top.data_ptr(), x, sink, stream)
             elif self.plan_o is not None:
-                self._run_ptr(self.plan_o, a.data_ptr(), x, sink, stream)
+                self._run_ptr(self.plan_o, a.data_ptr(), x, sink, stream, gate_events)
             if multi:
                 self._ev_own.record(stream)
                 dist.barrier(group=hg)  # every "own"/"sent" event of this step is recorded
@@ -621,7 +786,12 @@ class S5Runner:
             self._run_groups(x, c, wait_peers=multi)
             return
         if self.plan_o is not None:
-            self.compute(self.plan_o, a, x, self.t2)
+            if gate_events is not None:
+                import torch
+
+                self.plan_o.run_gated(a, x, self.t2, gate_events, torch.cuda.current_stream(x.device))
+            else:
+                self.compute(self.plan_o, a, x, self.t2)
         for j, i in self.local:
             self.inp[j * s:(j + 1) * s].copy_(self.t2[i * s:(i + 1) * s])
         ops = [dist.P2POp(dist.isend, self.t2[i * s:(i + 1) * s], r, group=self.group) for r, i in self.sends]

@@ -220,6 +220,30 @@ class SttsmPlan:
             s = stream if stream is not None else torch.cuda.current_stream(a.device)
             self.run_ptr(a.data_ptr(), x.data_ptr(), c.data_ptr(), s.cuda_stream)
 
+    def run_gated_ptr(self, a_ptr: int, x_ptr: int, c_ptr: int, events, stream: int = 0) -> None:
+        """Enqueue on raw device pointers while A is still arriving:
+        ``events[a]`` (torch.cuda.Event or raw cudaEvent_t) fires when A's
+        first-index chunk a is resident; the top level waits per key group."""
+        ptrs = [int(getattr(e, "cuda_event", e)) for e in events]
+        arr = (ctypes.c_void_p * max(1, len(ptrs)))(*[ctypes.c_void_p(q) for q in ptrs])
+        _native.check(_native.lib().bcss_sttsm_run_gated(
+            self._h, ctypes.c_void_p(a_ptr), ctypes.c_void_p(x_ptr), ctypes.c_void_p(c_ptr),
+            ctypes.c_void_p(stream), arr, len(ptrs)))
+
+    def run_gated(self, a, x, c, events, stream=None) -> None:
+        """``run`` whose top level waits, key group by key group, for the A
+        chunks it reads (``events``: one torch.cuda.Event per first block
+        index, recorded when that chunk of the packed A is resident)."""
+        import torch
+
+        if not (a.is_cuda and x.device == a.device and c.device == a.device):
+            raise ShapeError("A, X and C must be CUDA tensors on one device")
+        with torch.cuda.device(a.device):
+            if self._ws is None:
+                self.attach_torch_workspace(a.device)
+            s = stream if stream is not None else torch.cuda.current_stream(a.device)
+            self.run_gated_ptr(a.data_ptr(), x.data_ptr(), c.data_ptr(), events, s.cuda_stream)
+
     def run_host(self, a: np.ndarray, x: np.ndarray, c: np.ndarray) -> None:
         """Host buffers in, host buffer out (copies + run + sync in the library)."""
         for name, t, numel in (("A", a, self.a_elems), ("X", x, self.p * self.n),

@@ -113,6 +113,16 @@ def test_plan_validation_maps_to_reference_errors(args, exc):
         bs.SttsmPlan(*args)
 
 
+@pytest.mark.parametrize("args", [(3, 1 << 20, 64, 1, 1), (3, 64, 1 << 20, 1, 1), (2, 1 << 16, 64, 1, 1)])
+def test_int32_table_limits_raise_instead_of_truncating(args):
+    """Block / key / call counts past the int32 device tables are rejected
+    at plan creation (ranks were narrowed silently)."""
+    with pytest.raises(bs.ParameterError, match="int32"):
+        bs.SttsmPlan(*args)
+    with pytest.raises(bs.ParameterError, match="at most 8 modes"):
+        bs.SttsmPlan(9, 4, 4, 2, 2)
+
+
 def test_drop_in_argument_checks_without_gpu():
     """change_of_basis.py:54-63, 259-265: checks fire before any device work."""
     d = np.load(GOLDEN / "sttsm_small_m3_n4_p4_ba2_bc2.npz")

@@ -159,9 +159,9 @@ def test_bcss_temporaries_are_partially_symmetric():
     audited = []
 
     def hook(k, temp):
-        dense = bs.temp_to_dense(temp)
-        audited.append((k, dense.shape))
-        assert is_sym_in_modes(dense, range(k), 1e-12), k
+        dense = bs.temp_to_dense(temp)  # a DenseTensor, as in the reference
+        audited.append((k, dense.dims))
+        assert is_sym_in_modes(dense.array, range(k), 1e-12), k
 
     bs.sttsm_bcss(compress(a, 2), x, 2, temp_hook=hook)
     assert {k for k, _ in audited} == {1, 2, 3}
@@ -177,8 +177,7 @@ def test_bcss_temp_hook_no_reuse_flavor():
     bs.sttsm_bcss(compress(a, 2), x, 2, reuse=False, temp_hook=lambda k, t: seen.append((k, bs.temp_to_dense(t))))
     assert seen
     for k, dense in seen:
-        if k >= 2:
-            assert is_sym_in_modes(dense, range(k), 1e-12), k
+        assert bs.symmetry_violation(dense, range(k))[0] <= 1e-12 if k >= 2 else True
 
 
 def test_bcss_validations():
