@@ -1,5 +1,12 @@
-"""Run one BASELINE config's device path twice (dev tool for ncu captures:
-skip the first run's launches with --launch-skip)."""
+"""Run one BASELINE config's device path (dev tool for ncu captures).
+
+    python tools/profile_cfg.py CFG [--once]
+
+Twice by default (skip the first run's launches with --launch-skip for a
+warm capture); ``--once`` runs it a single time, deterministically (fixed
+seeds), for ``ncu --replay-mode application``, which re-runs the whole
+process once per metric pass instead of saving and restoring the ~130 GB of
+device memory a config-5 level kernel can touch."""
 import sys
 
 import torch
@@ -9,12 +16,14 @@ import paper_1301_7744_b200 as bs
 
 CFGS = {2: (3, 512, 512, 32, 32), 3: (4, 192, 192, 16, 16), 4: (5, 96, 96, 8, 8), 5: (4, 512, 256, 32, 32)}
 m, n, p, ba, bc = CFGS[int(sys.argv[1])]
+runs = 1 if "--once" in sys.argv else 2
 plan = bs.SttsmPlan(m, n, p, ba, bc)
-A = torch.rand(plan.a_elems, dtype=torch.float64, device="cuda")
-X = torch.randn(p, n, dtype=torch.float64, device="cuda")
+g = torch.Generator(device="cuda").manual_seed(1)
+A = torch.rand(plan.a_elems, dtype=torch.float64, device="cuda", generator=g)
+X = torch.randn(p, n, dtype=torch.float64, device="cuda", generator=g)
 C = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
 plan.attach_torch_workspace()
-for _ in range(2):
+for _ in range(runs):
     plan.run(A, X, C)
 torch.cuda.synchronize()
 print("launches per run", plan.last_launches)
