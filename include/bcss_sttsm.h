@@ -107,6 +107,10 @@ int bcss_plan_set_workspace(bcss_plan* plan, void* dev_ptr, size_t bytes);
 int bcss_plan_stats(bcss_plan* plan, int64_t* waves, int64_t* launches, uint64_t* flops,
                     int64_t* c_blocks);
 
+/* Launches per run on the warp-specialized DMMA kernels (b_a in {4, 8, 16,
+ * 32, 64}, any b_c) and on the generic kernel (other b_a, e.g. 1, 2, 3). */
+int bcss_plan_kernel_mix(bcss_plan* plan, int64_t* fast_launches, int64_t* generic_launches);
+
 /* ---- execution ------------------------------------------------------------ */
 
 /* Device-resident run: A_packed, X, C_packed are device pointers; the work is

@@ -194,6 +194,20 @@ int bcss_plan_stats(bcss_plan* P, int64_t* waves, int64_t* launches, uint64_t* f
   return BCSS_OK;
 }
 
+int bcss_plan_kernel_mix(bcss_plan* P, int64_t* fast_launches, int64_t* generic_launches) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  int st = build_plan(*P);
+  if (st) return st;
+  int64_t f = 0, g = 0;
+  for (auto& W : P->waves)
+    for (auto& L : W.levels)
+      for (auto& X : L.launches)
+        if (X.item_off.back() > 0) (X.cfg == CFG_GENERIC ? g : f) += 1;
+  if (fast_launches) *fast_launches = f;
+  if (generic_launches) *generic_launches = g;
+  return BCSS_OK;
+}
+
 int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, void* stream) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
   if (!A || !X_ || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");

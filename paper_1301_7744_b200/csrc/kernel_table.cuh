@@ -55,14 +55,18 @@ constexpr int N_POLICY_SHAPES = 10;
 constexpr int N_GEN = 4;
 constexpr int BCSS_GEN_OF[N_GEN] = {3, 4, 2, 8};
 
+// b_a variants of the fast kernels (one translation unit each): 4, 8, 16, 32, 64
+constexpr int N_BA = 5;
 extern const KernelCfg kFast4[N_SHAPES];
 extern const KernelCfg kFast8[N_SHAPES];
 extern const KernelCfg kFast16[N_SHAPES];
 extern const KernelCfg kFast32[N_SHAPES];
+extern const KernelCfg kFast64[N_SHAPES];
 extern const KernelCfg kGen4[N_GEN];
 extern const KernelCfg kGen8[N_GEN];
 extern const KernelCfg kGen16[N_GEN];
 extern const KernelCfg kGen32[N_GEN];
+extern const KernelCfg kGen64[N_GEN];
 extern const KernelCfg kGeneric;
 
 }  // namespace bcss

@@ -1,4 +1,4 @@
-// Fast level kernels for one power-of-two b_a (compile with -DBCSS_BA=4|8|16|32).
+// Fast level kernels for one power-of-two b_a (compile with -DBCSS_BA=4|8|16|32|64).
 #include "kernel_table.cuh"
 
 #ifndef BCSS_BA

@@ -24,24 +24,22 @@ int shape_bm(int shape) { return bcss::kFast32[shape].BM; }
 
 const KernelCfg& kernel_cfg(int cfg) {
   if (cfg == 0) return bcss::kGeneric;
-  if (cfg > 4 * N_SHAPES) {  // general-redirection variants
-    const int g = (cfg - 1 - 4 * N_SHAPES) / 4, ba = (cfg - 1) % 4;
-    const KernelCfg* t = ba == 0 ? bcss::kGen4 : ba == 1 ? bcss::kGen8 : ba == 2 ? bcss::kGen16 : bcss::kGen32;
-    return t[g];
-  }
-  const int shape = (cfg - 1) / 4, ba = (cfg - 1) % 4;
-  const KernelCfg* t = ba == 0 ? bcss::kFast4 : ba == 1 ? bcss::kFast8 : ba == 2 ? bcss::kFast16 : bcss::kFast32;
-  return t[shape];
+  const KernelCfg* const fast[bcss::N_BA] = {bcss::kFast4, bcss::kFast8, bcss::kFast16, bcss::kFast32, bcss::kFast64};
+  const KernelCfg* const gen[bcss::N_BA] = {bcss::kGen4, bcss::kGen8, bcss::kGen16, bcss::kGen32, bcss::kGen64};
+  const int ba = (cfg - 1) % bcss::N_BA;
+  if (cfg > bcss::N_BA * N_SHAPES)  // general-redirection variants
+    return gen[ba][(cfg - 1 - bcss::N_BA * N_SHAPES) / bcss::N_BA];
+  return fast[ba][(cfg - 1) / bcss::N_BA];
 }
 // general-redirection configuration mirroring fast shape `shape` (one of BCSS_GEN_OF), else -1
 int gen_cfg(int64_t bA, int shape) {
   const int f = fast_cfg(bA, 0);
   if (f < 0) return -1;
   for (int g = 0; g < N_GEN; ++g)
-    if (bcss::BCSS_GEN_OF[g] == shape) return 1 + 4 * N_SHAPES + g * 4 + (f - 1);
+    if (bcss::BCSS_GEN_OF[g] == shape) return 1 + bcss::N_BA * N_SHAPES + g * bcss::N_BA + (f - 1);
   return -1;
 }
-// fast configuration of tile shape `shape` for power-of-two b_a in {4, 8, 16, 32}, else -1
+// fast configuration of tile shape `shape` for power-of-two b_a in {4, 8, 16, 32, 64}, else -1
 int fast_cfg(int64_t bA, int shape) {
   int i;
   switch (bA) {
@@ -49,9 +47,10 @@ int fast_cfg(int64_t bA, int shape) {
     case 8: i = 1; break;
     case 16: i = 2; break;
     case 32: i = 3; break;
+    case 64: i = 4; break;
     default: return -1;
   }
-  return 1 + shape * 4 + i;
+  return 1 + shape * bcss::N_BA + i;
 }
 
 // Tile-shape policy.  A parent's rows are cut into tiles of the fast shapes;
@@ -185,7 +184,10 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
   // redirection; with reuse=False the levels below the top read dense block
   // tables with the identity mapping (contracted position k), which is that
   // form too - only the top level (unsorted keys into A) needs the generic kernel.
-  const bool fast_shape = is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0;
+  // (any b_c: rows are (jb, c) pairs addressed by division, the tail modes
+  // pass through the column index whole; the mirrored C order alone needs a
+  // power-of-two b_c)
+  const bool fast_shape = fast_cfg(P.bA, 0) >= 0;
   static const ShapePolicy policy;
   W.levels.clear();
   std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls

@@ -43,7 +43,7 @@ inline int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; r
 using bcss::KernelCfg;
 using bcss::N_SHAPES;
 using bcss::N_GEN;
-constexpr int N_CFGS = 1 + 4 * N_SHAPES + 4 * N_GEN;
+constexpr int N_CFGS = 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN;
 enum { CFG_GENERIC = 0 };
 const KernelCfg& kernel_cfg(int cfg);
 int fast_cfg(int64_t bA, int shape);

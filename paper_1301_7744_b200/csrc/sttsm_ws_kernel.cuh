@@ -108,7 +108,7 @@ struct WsLevelKernel {
   static_assert(BM <= PT, "one producer thread per output row");
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
   static_assert((BM * BK / 2) % PT == 0 && (BK * BN / 2) % PT == 0 && GP % 32 == 0, "loader balance");
-  static_assert((1 << LBA) == BA && RG % 4 == 0, "BA must be a power of two >= 4");
+  static_assert((1 << LBA) == BA && RG % 4 == 0, "BA must be a power of two in 4..64");
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 
   static __device__ __forceinline__ int swz(int col) { return ((col >> SW_SHIFT) & SW_MASK) << 2; }

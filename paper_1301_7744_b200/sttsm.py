@@ -126,7 +126,10 @@ class SttsmPlan:
         f = ctypes.c_uint64()
         _native.check(_native.lib().bcss_plan_stats(self._h, ctypes.byref(w), ctypes.byref(l),
                                                     ctypes.byref(f), ctypes.byref(c)))
-        return {"waves": w.value, "launches": l.value, "flops": int(f.value), "c_blocks": c.value}
+        fast, gen = ctypes.c_int64(), ctypes.c_int64()
+        _native.check(_native.lib().bcss_plan_kernel_mix(self._h, ctypes.byref(fast), ctypes.byref(gen)))
+        return {"waves": w.value, "launches": l.value, "flops": int(f.value), "c_blocks": c.value,
+                "fast_launches": fast.value, "generic_launches": gen.value}
 
     @property
     def last_launches(self) -> int:

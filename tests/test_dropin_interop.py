@@ -294,3 +294,39 @@ def test_run_host_on_partial_plans_matches_device_runs():
     got, want = c_sub.reshape(-1, bsz), np.asarray(d["C"]).reshape(-1, bsz)
     assert np.all(got[~mask] == -7.0)
     assert orc.rel_frobenius(got[mask], want[mask]) <= 1e-12
+
+
+def _compare_bcss_dense(result, oracle_dense):
+    """The reference's verification metric (cli.py:63-73): max relative error
+    over stored blocks, and the worst block index."""
+    scale = float(np.max(np.abs(oracle_dense))) or 1.0
+    b = result.b
+    worst = (0.0, next(iter(result.blocks)))
+    for key, blk in result.blocks.items():
+        sl = tuple(slice(i * b, (i + 1) * b) for i in key)
+        err = float(np.max(np.abs(np.asarray(blk) - oracle_dense[sl]))) / scale
+        if err > worst[0]:
+            worst = (err, key)
+    return worst
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("key", [(0, 1, 2), (3, 3, 3), (0, 0, 3)])
+def test_fault_injection_localises_corrupted_block(key):
+    """cli.verify_case(corrupt_block=...) (cli.py:84,121-122;
+    tests/test_cli.py:49-71): a block of the GPU result perturbed as the
+    reference does it is the worst block against the naive oracle, and the
+    unperturbed result passes the reference's 1e-10 bar."""
+    d, (m, n, p, ba, bc) = _golden("sttsm_small_m3_n16_p16_ba4_bc2.npz")
+    if max(key) >= p // bc:
+        key = tuple(min(v, p // bc - 1) for v in key)
+    out = bs.sttsm_bcss(bs.BcssTensor(m, n, ba, payload=d["A"]), d["X"], bc)
+    naive = orc.sttsm_naive_dense(orc.unpack_dense(d["A"], m, n, ba), d["X"])
+    err, _ = _compare_bcss_dense(out, naive)
+    assert err <= 1e-10
+    out.blocks[key] = out.blocks[key] + 1.0
+    err, worst = _compare_bcss_dense(out, naive)
+    assert worst == key and err > 1e-3
+    # the corruption is what the next GPU call would read, too
+    r = orc.hypertriangle_rank(key, p // bc)
+    assert np.allclose(out.payload[r * bc**m:(r + 1) * bc**m], np.asarray(out.blocks[key]).reshape(-1, order="F"))

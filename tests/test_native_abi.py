@@ -123,6 +123,23 @@ def test_int32_table_limits_raise_instead_of_truncating(args):
         bs.SttsmPlan(9, 4, 4, 2, 2)
 
 
+@pytest.mark.parametrize("cfg,fast", [
+    ((3, 128, 128, 64, 64), True), ((3, 256, 192, 64, 32), True),   # b_a = 64
+    ((3, 96, 96, 32, 6), True), ((4, 64, 60, 16, 12), True),        # b_c not a power of two
+    ((4, 32, 30, 8, 3), True), ((3, 64, 45, 32, 5), True),          # odd b_c
+    ((3, 12, 12, 3, 2), False), ((3, 16, 16, 2, 2), False), ((2, 8, 8, 1, 1), False),
+])
+def test_fast_kernel_coverage(cfg, fast):
+    """Every b_a in {4, 8, 16, 32, 64} runs on the warp-specialized DMMA
+    kernels for any b_c (b_a = 64 and non-power-of-two b_c fell
+    to the generic kernel); other b_a use the generic kernel."""
+    st = bs.SttsmPlan(*cfg).stats()
+    if fast:
+        assert st["generic_launches"] == 0 and st["fast_launches"] > 0
+    else:
+        assert st["generic_launches"] > 0
+
+
 def test_drop_in_argument_checks_without_gpu():
     """change_of_basis.py:54-63, 259-265: checks fire before any device work."""
     d = np.load(GOLDEN / "sttsm_small_m3_n4_p4_ba2_bc2.npz")
