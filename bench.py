@@ -59,11 +59,15 @@ REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_c
 
 def parse_args():
     ap = argparse.ArgumentParser()
+    ap.set_defaults(_shape=None)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--shape", default=None,
+                    help="m,n,p,b_A,b_C: a workload outside BASELINE's configs (e.g. the reference tests' "
+                         "b_A=3 / b_C=2 on the generic kernel); reported as config 0")
     ap.add_argument("--cpu-budget-s", type=float, default=12.0,
                     help="target CPU seconds of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -82,7 +86,11 @@ def parse_args():
                     help="time e2e as back-to-back synchronous calls instead of the streamed async API")
     ap.add_argument("--pipeline", type=int, default=4,
                     help="waves of the e2e transfer/compute pipeline (0 = serial copies)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.shape:
+        CONFIGS[0] = tuple(int(v) for v in args.shape.split(","))
+        args.config = 0
+    return args
 
 
 def bench_config(cfg: int, n_gpus: int) -> dict:
@@ -95,7 +103,8 @@ def bench_config(cfg: int, n_gpus: int) -> dict:
 
 def workload(cfg: int) -> dict:
     m, n, p, ba, bc = CONFIGS[cfg]
-    return {"workload": f"BASELINE config {cfg}: sttsm_bcss m={m} n={n} p={p} b_A={ba} b_C={bc}",
+    name = f"BASELINE config {cfg}" if cfg else "custom shape (--shape)"
+    return {"workload": f"{name}: sttsm_bcss m={m} n={n} p={p} b_A={ba} b_C={bc}",
             "m": m, "n": n, "p": p, "b_A": ba, "b_C": bc, "seed": SEED,
             "A": "random_bcss (U(-1,1) per canonical block, symmetrized diagonal blocks)",
             "X": "N(0,1) p x n"}
