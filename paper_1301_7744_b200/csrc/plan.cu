@@ -23,7 +23,10 @@ thread_local std::string g_last_error;
 int shape_bm(int shape) { return bcss::kFast32[shape].BM; }
 
 const KernelCfg& kernel_cfg(int cfg) {
-  if (cfg == 0) return bcss::kGeneric;
+  if (cfg == 0) {
+    static const int alt = getenv("BCSS_GENERIC_ALT") ? atoi(getenv("BCSS_GENERIC_ALT")) : 0;
+    return alt == 1 ? bcss::kGenericAlt1 : alt == 2 ? bcss::kGenericAlt2 : bcss::kGeneric;
+  }
   const KernelCfg* const fast[bcss::N_BA] = {bcss::kFast4, bcss::kFast8, bcss::kFast16, bcss::kFast32, bcss::kFast64};
   const KernelCfg* const gen[bcss::N_BA] = {bcss::kGen4, bcss::kGen8, bcss::kGen16, bcss::kGen32, bcss::kGen64};
   const int ba = (cfg - 1) % bcss::N_BA;
@@ -324,15 +327,19 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
         r0 += pc.second;
         LaunchHost& X = by_cfg[cfg];
         const KernelCfg& C = kernel_cfg(cfg);
+        // the generic kernel tiles the flat (key, column) space of a parent
+        const bool flat = cfg == CFG_GENERIC;
         if (X.parents.empty()) {
           X.cfg = cfg;
-          X.n_tiles = (int)((L.rest + C.BN - 1) / C.BN);
+          const int64_t ncols = flat ? L.keys_out * L.rest : L.rest;
+          if ((ncols + C.BN - 1) / C.BN > INT32_MAX) throw std::overflow_error("column tiles exceed int32");
+          X.n_tiles = (int)((ncols + C.BN - 1) / C.BN);
           X.item_off.push_back(0);
         }
         X.parents.push_back(par);
         if ((int)wi < n_w0_wholes) X.n_w0 = (int)X.parents.size();
         X.item_off.push_back(X.item_off.back() +
-                             (long long)L.keys_out * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
+                             (flat ? 1LL : (long long)L.keys_out) * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
         X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
       }
     }
@@ -352,6 +359,12 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
         for (size_t pi = 0; pi < X.parents.size(); ++pi) {
           if (grouped && (int)pi == X.n_w0) X.group_w0.push_back((long long)X.items.size());
           const int mtiles = (X.parents[pi].z + BM - 1) / BM;
+          if (X.cfg == CFG_GENERIC) {  // flat (key, column) tiles (never in key-grouped cascade levels)
+            if (grouped) throw std::logic_error("generic kernel in a cascade level");
+            for (int nt = 0; nt < X.n_tiles; ++nt)
+              for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, 0, nt, mt});
+            continue;
+          }
           for (int64_t key = k_lo; key < k_hi; ++key)
             for (int nt = 0; nt < X.n_tiles; ++nt)
               for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});

@@ -99,7 +99,10 @@ __device__ __forceinline__ TileInfo decode_item(const LevelArgs& a, long long it
 // ---------------------------------------------------------------------------
 // Generic kernel: any block sizes (including odd b_a / b_c, b = 1), either
 // reuse mode, any redirection permutation.  Per-element addressing with
-// div/mod and zero-filled bounds; correctness path for small/odd problems.
+// div/mod and zero-filled bounds.  Its GEMM columns run over (key, column)
+// pairs of the whole level (item key field unused, n-tiles over
+// keys_out * rest), so small blocks - whose keys have only b_a^k b_c^(m-1-k)
+// columns each - still fill the tile.
 // ---------------------------------------------------------------------------
 template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES>
 struct GenericLevelKernel {
@@ -127,19 +130,24 @@ struct GenericLevelKernel {
       const double* src = ok ? a.X + (long long)(t.row0 + rbase + r) * a.ldx + k0 + c : a.X;
       cp_async8(As + r * LDA + c, src, ok);
     }
-    const int n0 = t.nt * BN;
-    const int2* nrow = a.nbr + (long long)t.key * a.nbar;
+    // flat columns: GEMM column j of the parent is (key, c) = divmod(j, rest),
+    // so a tile spans several keys when a key's block has few columns (small b)
+    const long long n0 = (long long)t.nt * BN;
+    const long long ncols = a.keys_out * a.rest;
     const double* tin_call = a.Tin + (long long)t.in_call * a.keys_in * a.blk_in;
 #pragma unroll 1
     for (int it = 0; it < (BK * BN) / NT; ++it) {
       const int idx = tid + it * NT;
       const int r = idx / BN, col = idx % BN;
-      const int i = k0 + r, cg = n0 + col;
-      const bool ok = (i < a.n) && (cg < a.rest);
+      const int i = k0 + r;
+      const long long j = n0 + col;
+      const bool ok = (i < a.n) && (j < ncols);
       const double* src = a.X;
       if (ok) {
+        const long long key = j / a.rest;
+        const int cg = (int)(j - key * a.rest);
         const int ib = i / a.bA, e = i - ib * a.bA;
-        const int2 nb = __ldg(nrow + ib);
+        const int2 nb = __ldg(a.nbr + key * a.nbar + ib);
         int af = cg % a.bAk;
         const int tt = cg / a.bAk;
         long long off = (long long)tt * a.pw[a.k + 1] + (long long)e * a.pw[code_map(nb.y, a.k)];
@@ -180,6 +188,7 @@ struct GenericLevelKernel {
     const int wm = warp / WN, wn = warp % WN;
     const int jb0 = t.row0 / a.bC;
     const long long tstride = (long long)a.bAk * a.bC;
+    const long long ncols = a.keys_out * a.rest;
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm) {
       const int r = t.mt * BM + wm * WTM + fm * 8 + (lane >> 2);
@@ -189,16 +198,18 @@ struct GenericLevelKernel {
       const int call = __ldg(a.child_call + t.child_off + (jb - jb0));
       double* base = (a.call_out && a.call_out[call] ? const_cast<double*>(a.call_out[call])
                                                      : a.Tout + (long long)call * a.keys_out * a.blk_out) +
-                     (long long)t.key * a.blk_out + (long long)a.bAk * c;
+                     (long long)a.bAk * c;
 #pragma unroll
       for (int fn = 0; fn < FN; ++fn) {
-        const int col = t.nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);
+        const long long col = (long long)t.nt * BN + wn * WTN + fn * 8 + 2 * (lane & 3);
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          const int cq = col + q;
-          if (cq < a.rest) {
+          const long long j = col + q;
+          if (j < ncols) {  // flat column -> (key, column of the key's block)
+            const long long key = j / a.rest;
+            const int cq = (int)(j - key * a.rest);
             const int tt = cq / a.bAk, af = cq - tt * a.bAk;
-            base[af + tstride * tt] = acc[fm][fn][q];
+            base[key * a.blk_out + af + tstride * tt] = acc[fm][fn][q];
           }
         }
       }
