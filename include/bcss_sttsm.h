@@ -111,6 +111,16 @@ int bcss_plan_stats(bcss_plan* plan, int64_t* waves, int64_t* launches, uint64_t
  * 32, 64}, any b_c) and on the generic kernel (other b_a, e.g. 1, 2, 3). */
 int bcss_plan_kernel_mix(bcss_plan* plan, int64_t* fast_launches, int64_t* generic_launches);
 
+/* Level k's neighbour table as int32 pairs {rank of the stored block of
+ * T(k+1) holding the logical block (K, ib), redirection code word}, keys x
+ * n/b_a entries (2 * that many int32): from_device = 1 copies the table the
+ * device builder generated (the plan's tables are built on the device: the
+ * BCSS block index and redirection enumeration, canonicalize of
+ * indexing.py:34-54, rank of indexing.py:57-68), 0 builds the same table
+ * on the host (reference for tests).  out = NULL returns the size only. */
+int bcss_plan_neighbour_table(bcss_plan* plan, int k, int from_device, int32_t* out, int64_t n_max,
+                              int64_t* out_n);
+
 /* ---- execution ------------------------------------------------------------ */
 
 /* Device-resident run: A_packed, X, C_packed are device pointers; the work is

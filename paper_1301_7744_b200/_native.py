@@ -51,6 +51,7 @@ SIGNATURES = {
     "bcss_plan_set_workspace": (_c_int, [_vp, _vp, _sz]),
     "bcss_plan_stats": (_c_int, [_vp, _P(_i64), _P(_i64), _P(_u64), _P(_i64)]),
     "bcss_plan_kernel_mix": (_c_int, [_vp, _P(_i64), _P(_i64)]),
+    "bcss_plan_neighbour_table": (_c_int, [_vp, _c_int, _c_int, _P(ctypes.c_int32), _i64, _P(_i64)]),
     "bcss_sttsm_run": (_c_int, [_vp, _vp, _vp, _vp, _vp]),
     "bcss_sttsm_run_host": (_c_int, [_vp, _vp, _vp, _vp]),
     "bcss_sttsm_run_gated": (_c_int, [_vp, _vp, _vp, _vp, _vp, _P(_vp), _c_int]),

@@ -208,6 +208,27 @@ int bcss_plan_kernel_mix(bcss_plan* P, int64_t* fast_launches, int64_t* generic_
   return BCSS_OK;
 }
 
+int bcss_plan_neighbour_table(bcss_plan* P, int k, int from_device, int32_t* out, int64_t n_max, int64_t* out_n) {
+  if (!P || !out_n) return fail(BCSS_ERR_STATE, "null argument");
+  if (k < 0 || k >= P->m) return fail(BCSS_ERR_RANGE, "level %d outside 0..%d", k, P->m - 1);
+  int st = build_plan(*P);
+  if (st) return st;
+  const int64_t n = keys_at(*P, k) * P->nbar;
+  *out_n = 2 * n;
+  if (!out) return BCSS_OK;
+  if (2 * n > n_max) return fail(BCSS_ERR_RANGE, "output array too small");
+  if (from_device) {
+    if ((st = upload_tables(*P, nullptr))) return st;
+    CUDA_TRY(cudaMemcpy(out, static_cast<char*>(P->d_tables) + P->nbr_off[k], (size_t)n * sizeof(int2),
+                        cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<int2> h;
+    try { build_nbr(*P, k, h); } catch (const std::exception& e) { return fail(BCSS_ERR_PARAMETER, "%s", e.what()); }
+    memcpy(out, h.data(), (size_t)n * sizeof(int2));
+  }
+  return BCSS_OK;
+}
+
 int bcss_sttsm_run(bcss_plan* P, const double* A, const double* X_, double* C, void* stream) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
   if (!A || !X_ || !C) return fail(BCSS_ERR_PARAMETER, "null buffer");

@@ -35,14 +35,19 @@ inline int64_t simplex_count(int64_t extent, int m) {
 }
 
 // Lexicographic rank of a nondecreasing tuple among hypertriangle_iter(extent, m).
-// For position t, every value v in [idx[t-1], idx[t]) is followed by
-// simplex_count(extent - v, m-1-t) tuples that precede idx.
-inline int64_t hypertriangle_rank(const int64_t* idx, int m, int64_t extent) {
-  int64_t r = 0, lo = 0;
+// With c_t = idx[t] + t (strictly increasing over N = extent + m - 1 values,
+// c_{-1} = -1) the tuples before idx number
+//   sum_t sum_{v = c_{t-1}+1}^{c_t - 1} C(N-1-v, m-1-t)
+// and the hockey-stick identity collapses each inner sum:
+//   sum_t [ C(N - c_{t-1} - 1, m - t) - C(N - c_t, m - t) ]     (O(m) binomials)
+template <class I>
+inline int64_t hypertriangle_rank(const I* idx, int m, int64_t extent) {
+  const int64_t N = extent + m - 1;
+  int64_t r = 0, cprev = -1;
   for (int t = 0; t < m; ++t) {
-    const int rem = m - 1 - t;
-    for (int64_t v = lo; v < idx[t]; ++v) r += rem > 0 ? simplex_count(extent - v, rem) : 1;
-    lo = idx[t];
+    const int64_t c = (int64_t)idx[t] + t;
+    r += binom(N - cprev - 1, m - t) - binom(N - c, m - t);
+    cprev = c;
   }
   return r;
 }

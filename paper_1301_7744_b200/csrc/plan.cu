@@ -774,14 +774,11 @@ int build_plan(bcss_plan& P) {
     }
     }  // full run
     // tables
-    P.nbr.assign(P.m, {});
     P.nbr_off.assign(P.m, 0);
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
-    for (int k = 0; k < P.m; ++k) {
-      build_nbr(P, k, P.nbr[k]);
-      P.nbr_off[k] = take(P.nbr[k].size() * sizeof(int2));
-    }
+    for (int k = 0; k < P.m; ++k)  // neighbour tables: built on the device (build_nbr_device)
+      P.nbr_off[k] = take((size_t)keys_at(P, k) * (size_t)P.nbar * sizeof(int2));
     P.flops = 0;
     P.c_blocks = 0;
     const bool partial = P.start_level > 0 || P.stop_level > 0;
@@ -806,6 +803,96 @@ int build_plan(bcss_plan& P) {
   }
 }
 
+// ---- neighbour tables, built on the device ----------------------------------------
+// The largest plan table is the neighbour table of each level: keys(k) x n/b_a
+// entries {rank of the stored block sorted(K u ib) in T(k+1), code word of the
+// redirection}.  It is generated straight into the device table buffer (one
+// warp per key, lanes over ib), so neither its host construction nor its
+// upload grows with (n/b_a)^(k+1).  Same entries as build_nbr (tested bitwise).
+
+__device__ __forceinline__ long long dev_binom(long long n, int r) {
+  if (r < 0 || n < r) return 0;
+  if (r > n - r) r = (int)(n - r);
+  unsigned long long acc = 1;
+  for (int i = 1; i <= r; ++i) acc = acc * (unsigned long long)(n - r + i) / (unsigned long long)i;
+  return (long long)acc;
+}
+
+__device__ __forceinline__ long long dev_rank(const int* idx, int m, long long extent) {
+  const long long N = extent + m - 1;
+  long long r = 0, cprev = -1;
+  for (int t = 0; t < m; ++t) {
+    const long long c = (long long)idx[t] + t;
+    r += dev_binom(N - cprev - 1, m - t) - dev_binom(N - c, m - t);
+    cprev = c;
+  }
+  return r;
+}
+
+// mode 0: sorted keys (reuse, hypertriangle order); 1: product keys with the
+// general canonicalize mapping (reuse=False top level); 2: product keys of a
+// dense block table (reuse=False below the top: identity mapping)
+__global__ void build_nbr_kernel(int2* __restrict__ out, int k, long long nkeys, int nbar, int mode) {
+  const int lane = threadIdx.x & 31;
+  const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+  for (long long kr = warp0; kr < nkeys; kr += nwarps) {
+    int key[8];
+    if (mode == 0) {  // unrank kr among the nondecreasing k-tuples
+      long long rank = kr;
+      int lo = 0;
+      for (int t = 0; t < k; ++t) {
+        const int rem = k - 1 - t;
+        int v = lo;
+        for (;; ++v) {
+          const long long cnt = rem > 0 ? dev_binom((long long)(nbar - v) + rem - 1, rem) : 1;
+          if (rank < cnt) break;
+          rank -= cnt;
+        }
+        key[t] = v;
+        lo = v;
+      }
+    } else {
+      long long r = kr;
+      for (int d = k - 1; d >= 0; --d) { key[d] = (int)(r % nbar); r /= nbar; }
+    }
+    for (int ib = lane; ib < nbar; ib += 32) {
+      int rank, code;
+      if (mode == 2) {
+        rank = (int)(kr * nbar + ib);
+        code = k;
+        for (int d = 0; d <= k; ++d) code |= d << (4 + 3 * d);
+      } else {
+        int idx[9], canon[9], map[9];
+        for (int d = 0; d < k; ++d) idx[d] = key[d];
+        idx[k] = ib;
+        for (int d = 0; d <= k; ++d) canon[d] = idx[d];
+        for (int a = 1; a <= k; ++a)  // insertion sort (k + 1 <= 8 entries)
+          for (int b = a; b > 0 && canon[b - 1] > canon[b]; --b) {
+            const int tmp = canon[b]; canon[b] = canon[b - 1]; canon[b - 1] = tmp;
+          }
+        unsigned used = 0;  // canonicalize: first unused position of each value
+        for (int d = 0; d <= k; ++d)
+          for (int q = 0; q <= k; ++q)
+            if (!((used >> q) & 1u) && canon[q] == idx[d]) { used |= 1u << q; map[d] = q; break; }
+        rank = (int)dev_rank(canon, k + 1, nbar);
+        code = map[k];
+        for (int d = 0; d <= k; ++d) code |= map[d] << (4 + 3 * d);
+      }
+      out[kr * nbar + ib] = make_int2(rank, code);
+    }
+  }
+}
+
+int build_nbr_device(const bcss_plan& P, int k, int2* dst, cudaStream_t stream) {
+  const long long nkeys = keys_at(P, k);
+  const int mode = P.reuse ? 0 : (k + 1 == P.m ? 1 : 2);
+  const long long blocks = std::min<long long>((nkeys + 7) / 8, 148LL * 16);
+  build_nbr_kernel<<<(unsigned)std::max<long long>(1, blocks), 256, 0, stream>>>(dst, k, nkeys, (int)P.nbar, mode);
+  CUDA_TRY(cudaGetLastError());
+  return BCSS_OK;
+}
+
 // Upload the device tables once per plan.  The copy is stream-ordered on the
 // run's stream and synchronized: a plain cudaMemcpy from pageable memory can
 // return before its DMA lands, and kernels on a non-blocking stream would
@@ -819,8 +906,6 @@ int upload_tables(bcss_plan& P, cudaStream_t stream) {
     // run; a plan is bound to it
     return fail(BCSS_ERR_STATE, "plan is bound to device %d but device %d is current", P.device, dev);
   std::vector<char> host(P.tables_bytes, 0);
-  for (int k = 0; k < P.m; ++k)
-    if (!P.nbr[k].empty()) memcpy(&host[P.nbr_off[k]], P.nbr[k].data(), P.nbr[k].size() * sizeof(int2));
   for (auto& W : P.waves)
     for (auto& L : W.levels) {
       for (auto& X : L.launches) {
@@ -833,6 +918,10 @@ int upload_tables(bcss_plan& P, cudaStream_t stream) {
     memcpy(&host[P.off_gather_rows], P.gather_rows.data(), P.gather_rows.size() * sizeof(int));
   CUDA_TRY(cudaMalloc(&P.d_tables, std::max<size_t>(P.tables_bytes, 256)));
   CUDA_TRY(cudaMemcpyAsync(P.d_tables, host.data(), P.tables_bytes, cudaMemcpyHostToDevice, stream));
+  int st;
+  for (int k = 0; k < P.m; ++k)  // neighbour tables: generated on the device over the zeroed slots
+    if ((st = build_nbr_device(P, k, reinterpret_cast<int2*>(static_cast<char*>(P.d_tables) + P.nbr_off[k]), stream)))
+      return st;
   CUDA_TRY(cudaStreamSynchronize(stream));
   P.device = dev;
   static bool attr_done[64] = {false};

@@ -104,8 +104,7 @@ struct bcss_plan {
 
   bool built = false;
   std::vector<WaveHost> waves;
-  std::vector<std::vector<int2>> nbr;  // per k
-  std::vector<size_t> nbr_off;         // per k, into the table buffer
+  std::vector<size_t> nbr_off;         // per k, into the table buffer (neighbour tables built on device)
   size_t ws_bytes = 0;
   uint64_t flops = 0;
   int64_t c_blocks = 0;
@@ -192,6 +191,7 @@ namespace bcss_host {
 int64_t keys_at(const bcss_plan& P, int k);
 int64_t blk_at(const bcss_plan& P, int k);
 int build_plan(bcss_plan& P);
+void build_nbr(bcss_plan& P, int k, std::vector<int2>& out);  // host reference of the device builder
 int upload_tables(bcss_plan& P, cudaStream_t stream);
 int ensure_workspace(bcss_plan& P);
 double* region_for(bcss_plan& P, const WaveHost& W, int k);

@@ -147,6 +147,18 @@ class SttsmPlan:
             self._h, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), n.value, ctypes.byref(n)))
         return out
 
+    def neighbour_table(self, k: int, from_device: bool = True) -> np.ndarray:
+        """Level k's neighbour table, (keys x n/b_a, 2) int32 {stored-block
+        rank, redirection code}: the device-built one, or the host reference."""
+        n = ctypes.c_int64()
+        lib = _native.lib()
+        _native.check(lib.bcss_plan_neighbour_table(self._h, k, int(from_device), None, 0, ctypes.byref(n)))
+        out = np.empty(n.value, dtype=np.int32)
+        _native.check(lib.bcss_plan_neighbour_table(
+            self._h, k, int(from_device), out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), n.value,
+            ctypes.byref(n)))
+        return out.reshape(-1, 2)
+
     def set_call_outputs(self, ptrs) -> None:
         """Stop-level plans: write call i's T(stop_level) slice to device
         address ptrs[i] (0 = the output buffer's slot) - e.g. a peer GPU's
