@@ -1,6 +1,6 @@
 """Summarize ncu captures into profiles/ (markdown + JSON).
 
-usage: python tools/ncu_summary.py full <report.ncu-rep> <out.md> [--traffic-config N]
+usage: python tools/ncu_summary.py full <report.ncu-rep | raw.csv> <out.md> [--traffic-config N]
        python tools/ncu_summary.py launches <launches.csv> <out.md>
 """
 import csv
@@ -26,7 +26,11 @@ KEYS = [
 
 
 def raw_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if str(rep).endswith(".csv"):  # `ncu -i ... --page raw --csv` exported on the GPU box
+        out = Path(rep).read_text()
+        out = out[out.find('"ID"'):]
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]
     return hdr, units, rows[2:]
