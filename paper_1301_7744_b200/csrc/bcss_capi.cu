@@ -202,7 +202,7 @@ int bcss_plan_kernel_mix(bcss_plan* P, int64_t* fast_launches, int64_t* generic_
   for (auto& W : P->waves)
     for (auto& L : W.levels)
       for (auto& X : L.launches)
-        if (X.item_off.back() > 0) (X.cfg == CFG_GENERIC ? g : f) += 1;
+        if (X.item_off.back() > 0) (is_generic(X.cfg) ? g : f) += 1;
   if (fast_launches) *fast_launches = f;
   if (generic_launches) *generic_launches = g;
   return BCSS_OK;

@@ -67,8 +67,7 @@ extern const KernelCfg kGen8[N_GEN];
 extern const KernelCfg kGen16[N_GEN];
 extern const KernelCfg kGen32[N_GEN];
 extern const KernelCfg kGen64[N_GEN];
-extern const KernelCfg kGeneric;
-extern const KernelCfg kGenericAlt1;  // tile-shape experiments (BCSS_GENERIC_ALT=1|2)
-extern const KernelCfg kGenericAlt2;
+extern const KernelCfg kGeneric;      // other b_a, insertion-form levels
+extern const KernelCfg kGenericPerm;  // other b_a, reuse=False top level
 
 }  // namespace bcss

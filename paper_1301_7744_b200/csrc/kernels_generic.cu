@@ -2,7 +2,8 @@
 #include "kernel_table.cuh"
 
 namespace bcss {
-const KernelCfg kGeneric = make_cfg<GenericLevelKernel<32, 64, 16, 2, 2, 2>>("generic32x64");
-const KernelCfg kGenericAlt1 = make_cfg<GenericLevelKernel<64, 64, 16, 2, 2, 3>>("generic64x64s3");
-const KernelCfg kGenericAlt2 = make_cfg<GenericLevelKernel<64, 128, 16, 2, 4, 3>>("generic64x128s3");
+// insertion-form redirection (every level except a reuse=False top level)
+const KernelCfg kGeneric = make_cfg<GenericLevelKernel<64, 64, 16, 2, 2, 3, true>>("generic64x64ins");
+// any redirection permutation (reuse=False top level: unsorted keys into A)
+const KernelCfg kGenericPerm = make_cfg<GenericLevelKernel<64, 64, 16, 2, 2, 3, false>>("generic64x64perm");
 }  // namespace bcss

@@ -23,10 +23,8 @@ thread_local std::string g_last_error;
 int shape_bm(int shape) { return bcss::kFast32[shape].BM; }
 
 const KernelCfg& kernel_cfg(int cfg) {
-  if (cfg == 0) {
-    static const int alt = getenv("BCSS_GENERIC_ALT") ? atoi(getenv("BCSS_GENERIC_ALT")) : 0;
-    return alt == 1 ? bcss::kGenericAlt1 : alt == 2 ? bcss::kGenericAlt2 : bcss::kGeneric;
-  }
+  if (cfg == CFG_GENERIC) return bcss::kGeneric;
+  if (cfg == CFG_GENERIC_PERM) return bcss::kGenericPerm;
   const KernelCfg* const fast[bcss::N_BA] = {bcss::kFast4, bcss::kFast8, bcss::kFast16, bcss::kFast32, bcss::kFast64};
   const KernelCfg* const gen[bcss::N_BA] = {bcss::kGen4, bcss::kGen8, bcss::kGen16, bcss::kGen32, bcss::kGen64};
   const int ba = (cfg - 1) % bcss::N_BA;
@@ -319,7 +317,10 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       else pieces = {{-1, whole.z}};
       int r0 = 0;
       for (const auto& pc : pieces) {
-        const int cfg = fast ? fast_cfg(P.bA, pc.first) : gen ? gen_cfg(P.bA, pc.first) : CFG_GENERIC;
+        // generic kernel: the insertion-form addressing unless the level
+        // redirects through general permutations (reuse=False top level)
+        const int cfg = fast ? fast_cfg(P.bA, pc.first) : gen ? gen_cfg(P.bA, pc.first)
+                        : (P.reuse || k < P.m - 1) ? CFG_GENERIC : CFG_GENERIC_PERM;
         int4 par = whole;
         par.y = whole.y + r0;
         par.z = pc.second;
@@ -328,7 +329,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
         LaunchHost& X = by_cfg[cfg];
         const KernelCfg& C = kernel_cfg(cfg);
         // the generic kernel tiles the flat (key, column) space of a parent
-        const bool flat = cfg == CFG_GENERIC;
+        const bool flat = is_generic(cfg);
         if (X.parents.empty()) {
           X.cfg = cfg;
           const int64_t ncols = flat ? L.keys_out * L.rest : L.rest;
@@ -359,7 +360,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
         for (size_t pi = 0; pi < X.parents.size(); ++pi) {
           if (grouped && (int)pi == X.n_w0) X.group_w0.push_back((long long)X.items.size());
           const int mtiles = (X.parents[pi].z + BM - 1) / BM;
-          if (X.cfg == CFG_GENERIC) {  // flat (key, column) tiles (never in key-grouped cascade levels)
+          if (is_generic(X.cfg)) {  // flat (key, column) tiles (never in key-grouped cascade levels)
             if (grouped) throw std::logic_error("generic kernel in a cascade level");
             for (int nt = 0; nt < X.n_tiles; ++nt)
               for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, 0, nt, mt});

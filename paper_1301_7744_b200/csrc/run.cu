@@ -282,7 +282,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       // product key K reads blocks whose first index is min(K), not K[0]
       bool gate_split = gate && P->reuse;
       for (const LaunchHost& X : L.launches)
-        gate_split = gate_split && X.parents.size() == 1 && X.cfg != CFG_GENERIC;  // key-major items only
+        gate_split = gate_split && X.parents.size() == 1 && !is_generic(X.cfg);  // key-major items only
       if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[P->nbar - 1], 0));
       const bool conc = (P->concurrent && nl > 1) || gate_split;
       if (conc && (st = ensure_side(P, std::max(nl - 1, 1)))) return st;

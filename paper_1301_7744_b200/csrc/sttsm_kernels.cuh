@@ -104,10 +104,76 @@ __device__ __forceinline__ TileInfo decode_item(const LevelArgs& a, long long it
 // keys_out * rest), so small blocks - whose keys have only b_a^k b_c^(m-1-k)
 // columns each - still fill the tile.
 // ---------------------------------------------------------------------------
-template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES>
+// INS = true: the redirection is the insertion form (every reuse=True level and
+// the reuse=False levels below the top): the stored offset of logical column c
+// = (a-digits c_a < b_a^k, tail t) with the contracted digit e at stored
+// position p is lo_p + e b_a^p + b_a (c_a - lo_p) + t b_a^(k+1), lo_p = c_a mod
+// b_a^p, so a thread's column terms are computed once per tile and each
+// element costs one neighbour lookup and a few multiply-adds.
+template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, bool INS = false>
 struct GenericLevelKernel {
   static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int NT = WM * WN * 32;
+  static_assert(!INS || (NT % BN == 0 && (BK * BN) % NT == 0), "INS: one fixed column per thread");
+  static constexpr int RSTEP = NT / BN;  // INS: a thread's rows are r0 + i * RSTEP
+
+  // INS: per-thread column terms of the current load tile
+  struct ColInfo {
+    long long key_nbar;   // key * n/b_a (neighbour-table row), -1 = past the level's columns
+    long long tbase;      // t * b_a^(k+1)
+    long long q[8];       // q[p] = lo_p + b_a (c_a - lo_p)
+  };
+  static __device__ __forceinline__ void col_info(const LevelArgs& a, const TileInfo& t, ColInfo& ci) {
+    const long long j = (long long)t.nt * BN + (threadIdx.x % BN);
+    if (j >= a.keys_out * a.rest) { ci.key_nbar = -1; return; }
+    const long long key = j / a.rest;
+    const int c = (int)(j - key * a.rest);
+    const int ca = c % a.bAk, tt = c / a.bAk;
+    ci.key_nbar = key * a.nbar;
+    ci.tbase = (long long)tt * a.pw[a.k + 1];
+#pragma unroll
+    for (int p = 0; p < 8; ++p) {
+      const long long lo = p <= a.k ? ca % a.pw[p] : 0;
+      ci.q[p] = lo + (long long)a.bA * (ca - lo);
+    }
+  }
+  static __device__ __forceinline__ void load_stage_ins(const LevelArgs& a, const TileInfo& t, const ColInfo& ci,
+                                                        int kstep, double* As, double* Bs) {
+    const int tid = threadIdx.x;
+    const int k0 = kstep * BK;
+    const int rbase = t.mt * BM;
+#pragma unroll
+    for (int it = 0; it < (BM * BK) / NT; ++it) {
+      const int idx = tid + it * NT;
+      const int r = idx / BK, c = idx % BK;
+      const bool ok = (rbase + r < t.rows) && (k0 + c < a.n);
+      const double* src = ok ? a.X + (long long)(t.row0 + rbase + r) * a.ldx + k0 + c : a.X;
+      cp_async8(As + r * LDA + c, src, ok);
+    }
+    const double* tin_call = a.Tin + (long long)t.in_call * a.keys_in * a.blk_in;
+    const int col = tid % BN;
+    int i = k0 + tid / BN;
+    int ib = i / a.bA, e = i - ib * a.bA;
+#pragma unroll 4
+    for (int it = 0; it < (BK * BN) / NT; ++it) {
+      const int r = tid / BN + it * RSTEP;
+      const bool ok = ci.key_nbar >= 0 && i < a.n;
+      const double* src = a.X;
+      if (ok) {
+        const int2 nb = __ldg(a.nbr + ci.key_nbar + ib);
+        const int pos = code_p(nb.y);
+        long long q = ci.q[0];
+#pragma unroll
+        for (int p = 1; p < 8; ++p)
+          if (pos == p) q = ci.q[p];
+        src = tin_call + (long long)nb.x * a.blk_in + ci.tbase + q + (long long)e * a.pw[pos];
+      }
+      cp_async8(Bs + r * LDB + col, src, ok);
+      i += RSTEP;
+      e += RSTEP;
+      while (e >= a.bA) { e -= a.bA; ++ib; }
+    }
+  }
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
   static constexpr int LDA = BK + 4;
@@ -229,6 +295,8 @@ struct GenericLevelKernel {
     TileInfo cp = ld;
     int ld_k = 0;
     long long ld_step = 0;
+    ColInfo ci;
+    if constexpr (INS) col_info(a, ld, ci);
     double acc[FM][FN][2];
 #pragma unroll
     for (int fm = 0; fm < FM; ++fm)
@@ -238,13 +306,20 @@ struct GenericLevelKernel {
       ++ld_step;
       if (++ld_k == ksteps) {
         ld_k = 0;
-        if (ld_step < total_steps) ld = decode_item(a, ld.item + gridDim.x, BM);
+        if (ld_step < total_steps) {
+          ld = decode_item(a, ld.item + gridDim.x, BM);
+          if constexpr (INS) col_info(a, ld, ci);
+        }
       }
+    };
+    auto load = [&](double* As_, double* Bs_) {
+      if constexpr (INS) load_stage_ins(a, ld, ci, ld_k, As_, Bs_);
+      else load_stage(a, ld, ld_k, As_, Bs_);
     };
 #pragma unroll
     for (int s = 0; s < STAGES - 1; ++s) {
       if (ld_step < total_steps) {
-        load_stage(a, ld, ld_k, As + s * A_STAGE, Bs + s * B_STAGE);
+        load(As + s * A_STAGE, Bs + s * B_STAGE);
         advance_load();
       }
       cp_async_commit();
@@ -255,7 +330,7 @@ struct GenericLevelKernel {
       __syncthreads();
       if (ld_step < total_steps) {
         const int slot = (int)(ld_step % STAGES);
-        load_stage(a, ld, ld_k, As + slot * A_STAGE, Bs + slot * B_STAGE);
+        load(As + slot * A_STAGE, Bs + slot * B_STAGE);
         advance_load();
       }
       cp_async_commit();
