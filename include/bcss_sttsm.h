@@ -257,6 +257,14 @@ int bcss_plan_set_timing(bcss_plan* plan, int on);
 int bcss_plan_launch_times(bcss_plan* plan, int32_t* out_level, uint64_t* out_flops,
                            float* out_ms, int64_t n_max, int64_t* out_n);
 
+/* Blocked symmetrization of a packed BCSS payload in device memory (order m,
+ * dimension dim, block dimension b), in place on `stream`: every canonical
+ * block whose key repeats an index is averaged over the permutations of the
+ * modes of each run of equal indices, so the represented tensor becomes
+ * exactly symmetric - the blocked counterpart of the reference's
+ * symmetrize (change_of_basis.py:287-295). */
+int bcss_symmetrize_blocks(double* payload, int m, int64_t dim, int64_t b, void* stream);
+
 /* Diagnostic: FP64 tensor-core (DMMA) peak of the current device, measured
  * with a register-resident mma.sync m8n8k4 f64 loop over all SMs (TFLOP/s).
  * Used as the roofline denominator; no reference counterpart. */

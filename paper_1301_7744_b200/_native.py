@@ -82,6 +82,7 @@ SIGNATURES = {
     "bcss_plan_set_timing": (_c_int, [_vp, _c_int]),
     "bcss_plan_launch_times": (_c_int, [_vp, _P(ctypes.c_int32), _P(_u64), _P(ctypes.c_float), _i64, _P(_i64)]),
     "bcss_probe_fp64_peak": (_c_int, [_P(ctypes.c_double)]),
+    "bcss_symmetrize_blocks": (_c_int, [_vp, _c_int, _i64, _i64, _vp]),
 }
 
 _lib = None

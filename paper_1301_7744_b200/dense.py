@@ -9,9 +9,9 @@ reproduce the paper's BCSS-vs-Dense comparison on the
 same GPU.  It needs the dense tensor (n^m doubles), so it only fits small n.
 
 ``symmetrize_bcss_device`` averages every canonical block of a packed BCSS
-payload over the permutations of its repeated-index mode groups, making the
-represented tensor exactly symmetric to rounding — the blocked counterpart of
-the reference's ``symmetrize`` (change_of_basis.py:287-295), motivated at
+payload over the permutations of its repeated-index mode groups (native
+kernel, csrc/symmetrize.cu), making the represented tensor exactly
+symmetric — the blocked counterpart of the reference's ``symmetrize`` (change_of_basis.py:287-295), motivated at
 PAPER.md:1461-1466 (diagonal blocks of C carry 1-ulp asymmetry).
 
 ``bcss_to_dense_device`` expands a packed payload to the dense tensor
@@ -68,40 +68,23 @@ def bcss_to_dense_device(packed, m: int, dim: int, b: int):
 
 
 def symmetrize_bcss_device(packed, m: int, dim: int, b: int, chunk_blocks: int = 256):
-    """In-place symmetrization of the diagonal blocks of a packed payload."""
+    """In-place symmetrization of the diagonal blocks of a packed payload (a
+    float64 CUDA tensor): the native kernel ``bcss_symmetrize_blocks``
+    (csrc/symmetrize.cu) averages every block whose key repeats an index over
+    the permutations of each run of equal indices, on torch's current stream.
+    ``chunk_blocks`` is accepted for compatibility and unused."""
+    import ctypes
+
     import torch
 
-    g = dim // b
-    blocks = packed.view(simplex_count(g, m), *([b] * m))
-    by_pattern: dict[tuple, list[int]] = {}
-    for r, key in enumerate(hypertriangle_iter(g, m)):
-        runs, cur = [], 1
-        for u, v in zip(key, key[1:]):
-            if u == v:
-                cur += 1
-            else:
-                runs.append(cur)
-                cur = 1
-        runs.append(cur)
-        if max(runs) > 1:
-            by_pattern.setdefault(tuple(runs), []).append(r)
-    for runs, ranks in by_pattern.items():
-        groups, start = [], 0
-        for ln in runs:
-            if ln > 1:
-                groups.append([1 + (m - 1 - d) for d in range(start, start + ln)])
-            start += ln
-        idx_all = torch.tensor(ranks, dtype=torch.long, device=packed.device)
-        for c0 in range(0, len(ranks), chunk_blocks):
-            idx = idx_all[c0:c0 + chunk_blocks]
-            xb = blocks.index_select(0, idx)
-            for axes in groups:
-                acc = torch.zeros_like(xb)
-                for perm in itertools.permutations(axes):
-                    order = list(range(m + 1))
-                    for src, dst in zip(axes, perm):
-                        order[src] = dst
-                    acc += xb.permute(order)
-                xb = acc / math.factorial(len(axes))
-            blocks.index_copy_(0, idx, xb)
+    from . import _native
+
+    if not (packed.is_cuda and packed.dtype == torch.float64 and packed.is_contiguous()):
+        raise ValueError("symmetrize_bcss_device needs a contiguous float64 CUDA tensor")
+    if packed.numel() != simplex_count(dim // b, m) * b**m:
+        raise ValueError("payload size does not match (m, dim, b)")
+    with torch.cuda.device(packed.device):
+        stream = torch.cuda.current_stream(packed.device).cuda_stream
+        _native.check(_native.lib().bcss_symmetrize_blocks(
+            ctypes.c_void_p(packed.data_ptr()), m, dim, b, ctypes.c_void_p(stream)))
     return packed

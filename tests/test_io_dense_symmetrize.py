@@ -74,14 +74,20 @@ def test_dense_baseline_matches_reference(device):
     assert dense.dense_flops(3, 4, 2) == 448  # reference anchor, tests/test_costs.py:95-96
 
 
-@pytest.mark.parametrize("device", DEVICES)
-def test_symmetrize_makes_c_exactly_symmetric(device):
-    d = np.load(GOLDEN / "sttsm_rbcss_m4_n12_b4.npz")
+@pytest.mark.gpu
+@pytest.mark.parametrize("case", ["sttsm_rbcss_m4_n12_b4", "sttsm_rbcss_m5_n8_b2", "sttsm_rbcss_m3_n32_b8",
+                                  "sttsm_small_m6_n8_p8_ba4_bc4"])
+def test_symmetrize_makes_c_exactly_symmetric(case):
+    """The native blocked symmetrization (csrc/symmetrize.cu): exact symmetry
+    (every orbit one value), and a change within rounding of the reference's
+    output (its diagonal blocks are symmetric to ~1 ulp)."""
+    device = "cuda"
+    d = np.load(GOLDEN / f"{case}.npz")
     m, n, p, ba, bc = (int(v) for v in d["dims"])
     c = torch.from_numpy(d["C"].copy()).to(device)
     before = orc.unpack_dense(d["C"], m, p, bc)
     dense.symmetrize_bcss_device(c, m, p, bc)
     after = orc.unpack_dense(c.cpu().numpy(), m, p, bc)
     asym = lambda t: max(np.max(np.abs(t - np.transpose(t, q))) for q in itertools.permutations(range(m)))
-    assert asym(after) <= 4 * np.finfo(float).eps * np.max(np.abs(after))
+    assert asym(after) == 0.0
     assert orc.rel_frobenius(after, before) <= 1e-14
