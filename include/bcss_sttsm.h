@@ -187,6 +187,23 @@ int bcss_host_is_pinned(const void* ptr, int* out);
  * between bcss_sttsm_run and bcss_sttsm_run_host.  0 = off. */
 int bcss_plan_set_pipeline(bcss_plan* plan, int waves);
 
+/* Symmetric-aware upload for pipelined host runs (no reference counterpart:
+ * it exploits the symmetry a BCSS tensor represents, storage.py:177-216).
+ * Blocks whose key repeats an index carry each orbit of their repeated modes'
+ * permutations once; with `on`, bcss_sttsm_run_host[_async] moves only the
+ * 32-byte sectors holding orbit representatives of those blocks (read by a
+ * zero-copy kernel from the mapped pinned A; the other elements are filled from
+ * the representatives in HBM) and the distinct-key blocks by DMA.  Results are
+ * bit-identical to the full upload when the repeated-key blocks are exactly
+ * symmetric (the reference's compress(..., tol=0), bcss_symmetrize_blocks);
+ * otherwise every orbit contributes its representative's value.  Needs
+ * power-of-two b_a >= 4 and a pinned, device-mapped A; other runs upload all of
+ * A.  bcss_plan_upload_bytes: bytes of A one host run moves over PCIe. */
+int bcss_plan_set_symmetric_upload(bcss_plan* plan, int on);
+int bcss_plan_upload_bytes(bcss_plan* plan, int64_t* out_bytes);
+/* bytes of A the plan's last host run moved (-1 before the first) */
+int bcss_plan_last_upload_bytes(bcss_plan* plan, int64_t* out_bytes);
+
 /* Partial runs, the exchange points of the multi-GPU schedule:
  * stop_level > 0 computes levels m-1 .. stop_level only and writes T(stop_level)
  * (calls in bcss_plan_level_calls order, each keys x block doubles) to the

@@ -56,6 +56,9 @@ SIGNATURES = {
     "bcss_sttsm_run_host": (_c_int, [_vp, _vp, _vp, _vp]),
     "bcss_sttsm_run_gated": (_c_int, [_vp, _vp, _vp, _vp, _vp, _P(_vp), _c_int]),
     "bcss_plan_set_pipeline": (_c_int, [_vp, _c_int]),
+    "bcss_plan_set_symmetric_upload": (_c_int, [_vp, _c_int]),
+    "bcss_plan_upload_bytes": (_c_int, [_vp, _P(_i64)]),
+    "bcss_plan_last_upload_bytes": (_c_int, [_vp, _P(_i64)]),
     "bcss_plan_set_stop_level": (_c_int, [_vp, _c_int]),
     "bcss_plan_set_call_outputs": (_c_int, [_vp, _P(_vp), _i64]),
     "bcss_sttsm_run_host_async": (_c_int, [_vp, _vp, _vp, _vp]),

@@ -25,7 +25,8 @@ UNITS = [("bcss_capi", CSRC / "bcss_capi.cu", []),
          ("plan", CSRC / "plan.cu", []),
          ("run", CSRC / "run.cu", []),
          ("kernels_generic", CSRC / "kernels_generic.cu", []),
-         ("symmetrize", CSRC / "symmetrize.cu", [])] + [
+         ("symmetrize", CSRC / "symmetrize.cu", []),
+         ("sym_upload", CSRC / "sym_upload.cu", [])] + [
     (f"kernels_fast_ba{ba}", CSRC / "kernels_fast.cu", [f"-DBCSS_BA={ba}"]) for ba in (4, 8, 16, 32, 64)]
 HEADERS = [CSRC / "plan.hpp", CSRC / "sttsm_kernels.cuh", CSRC / "sttsm_ws_kernel.cuh", CSRC / "kernel_table.cuh", CSRC / "combinatorics.hpp", CSRC / "shape_costs.hpp",
            ROOT / "include" / "bcss_sttsm.h"]

@@ -133,6 +133,10 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->copy_out) cudaStreamDestroy(P->copy_out);
   if (P->copy_out2) cudaStreamDestroy(P->copy_out2);
   if (P->out2_done) cudaEventDestroy(P->out2_done);
+  if (P->d_sym) cudaFree(P->d_sym);
+  if (P->sym_stream) cudaStreamDestroy(P->sym_stream);
+  if (P->fill_stream) cudaStreamDestroy(P->fill_stream);
+  for (auto ev : P->fill_ev) cudaEventDestroy(ev);
   delete P;
   return BCSS_OK;
 }
@@ -411,6 +415,32 @@ int bcss_plan_set_pipeline(bcss_plan* P, int waves) {
   return BCSS_OK;
 }
 
+int bcss_plan_set_symmetric_upload(bcss_plan* P, int on) {
+  if (!P) return fail(BCSS_ERR_STATE, "null plan");
+  P->sym_upload = on != 0;
+  return BCSS_OK;
+}
+
+int bcss_plan_last_upload_bytes(bcss_plan* P, int64_t* out_bytes) {
+  if (!P || !out_bytes) return fail(BCSS_ERR_STATE, "null argument");
+  *out_bytes = P->last_upload_bytes;
+  return BCSS_OK;
+}
+
+int bcss_plan_upload_bytes(bcss_plan* P, int64_t* out_bytes) {
+  if (!P || !out_bytes) return fail(BCSS_ERR_STATE, "null argument");
+  int64_t in_elems = 0, out_elems = 0;
+  int st = bcss_plan_io_elems(P, &in_elems, &out_elems);
+  if (st) return st;
+  *out_bytes = in_elems * (int64_t)sizeof(double);
+  if (bcss_host::sym_eligible(*P) && P->pipeline_waves > 0 && !P->units_set && !P->keep_temps &&
+      P->start_level == 0 && P->stop_level == 0) {
+    if ((st = bcss_host::sym_prepare(*P))) return st;
+    *out_bytes = P->sym_fetch_elems * (int64_t)sizeof(double);
+  }
+  return BCSS_OK;
+}
+
 namespace {
 // memcpy with the host's cores (pageable <-> pinned staging)
 void par_copy(void* dst, const void* src, size_t bytes) {
@@ -475,7 +505,7 @@ int bcss_sttsm_run_host(bcss_plan* P, const double* A, const double* X, double* 
 int bcss_host_register(void* ptr, size_t bytes) {
   if (!ptr || !bytes) return fail(BCSS_ERR_PARAMETER, "null or empty host range");
   if (is_pinned(ptr)) return BCSS_OK;
-  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+  const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(BCSS_ERR_CUDA, "cudaHostRegister of %zu bytes failed: %s", bytes, cudaGetErrorString(e));
@@ -528,10 +558,31 @@ int bcss_sttsm_run_host_async(bcss_plan* P, const double* A, const double* X, do
 
 int bcss_plan_wait(bcss_plan* P) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
-  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream})
+  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream, P->sym_stream, P->fill_stream})
     if (q) CUDA_TRY(cudaStreamSynchronize(q));
+  if (!P->atrace.empty()) {  // BCSS_TRACE=3: device timeline of the streamed calls
+    fprintf(stderr, "[bcss trace] streamed host runs (device ms since the first mark):\n");
+    for (auto& t : P->atrace) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, P->atrace.front().second, t.second);
+      fprintf(stderr, "  %-34s %9.3f\n", t.first.c_str(), ms);
+    }
+    for (auto& t : P->atrace) cudaEventDestroy(t.second);
+    P->atrace.clear();
+  }
   return BCSS_OK;
 }
+
+namespace {
+// BCSS_TRACE=3: timing event on `s`, printed by bcss_plan_wait
+void amark(bcss_plan* P, const std::string& name, cudaStream_t s) {
+  static const bool on = [] { const char* t = getenv("BCSS_TRACE"); return t && atoi(t) == 3; }();
+  if (!on) return;
+  cudaEvent_t ev;
+  if (cudaEventCreate(&ev) != cudaSuccess || cudaEventRecord(ev, s) != cudaSuccess) return;
+  P->atrace.emplace_back("call " + std::to_string(P->host_calls) + " " + name, ev);
+}
+}  // namespace
 
 static int run_host_pinned(bcss_plan* P, const double* A, const double* X, double* C, bool async) {
   const size_t blk_a = (size_t)ipow(P->bA, P->m);
@@ -563,6 +614,7 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   const bool pipelined = P->pipeline_waves > 0 && !P->units_set && !P->keep_temps && P->start_level == 0 &&
                          P->stop_level == 0 && is_pinned(A) &&
                          is_pinned(X) && is_pinned(C);
+  P->last_upload_bytes = (int64_t)a_bytes;
   if (!pipelined) {
     CUDA_TRY(cudaMemcpyAsync(P->hA, A, a_bytes, cudaMemcpyHostToDevice, P->host_stream));
     CUDA_TRY(cudaMemcpyAsync(P->hX, X, x_bytes, cudaMemcpyHostToDevice, P->host_stream));
@@ -634,20 +686,61 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   const char* tr = getenv("BCSS_TRACE");
   if (tr && atoi(tr) == 1) pipe.trace = &trace;
   trace_mark(&pipe, "upload start", P->copy_in);
+  amark(P, "upload start (copy_in)", P->copy_in);
   CUDA_TRY(cudaMemcpyAsync(dX, X, x_bytes, cudaMemcpyHostToDevice, P->copy_in));
-  for (int64_t a = 0; a < P->nbar; ++a) {
-    const size_t r0 = (size_t)first_rank_with(a, P->m, P->nbar), r1 = (size_t)first_rank_with(a + 1, P->m, P->nbar);
-    CUDA_TRY(cudaMemcpyAsync(dA + r0 * blk_a, A + r0 * blk_a, (r1 - r0) * blk_a * sizeof(double),
-                             cudaMemcpyHostToDevice, P->copy_in));
-    CUDA_TRY(cudaEventRecord(P->chunk_ev[a], P->copy_in));
-    trace_mark(&pipe, "A chunk " + std::to_string(a) + " landed", P->copy_in);
+  // symmetric upload: distinct-key blocks by DMA, repeated-key blocks by the
+  // zero-copy streaming kernel + per-chunk fills (sym_upload.cu)
+  bool sym = bcss_host::sym_eligible(*P) && bcss_host::sym_supported();
+  if (sym) {
+    cudaPointerAttributes at;
+    sym = cudaPointerGetAttributes(&at, A) == cudaSuccess && at.devicePointer != nullptr;
+    cudaGetLastError();
+  }
+  if (sym) {
+    if ((st = bcss_host::sym_prepare(*P))) return st;
+    int lo = 0, hi = 0;
+    CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    if (!P->sym_stream) CUDA_TRY(cudaStreamCreateWithPriority(&P->sym_stream, cudaStreamNonBlocking, hi));
+    if (!P->fill_stream) CUDA_TRY(cudaStreamCreateWithPriority(&P->fill_stream, cudaStreamNonBlocking, hi));
+    // the kernel waits on the device for the set's previous symmetric run; a
+    // previous full-upload run on this set is waited for here
+    if (!P->sym_set_last[set]) CUDA_TRY(cudaStreamWaitEvent(P->sym_stream, P->set_compute_done[set], 0));
+    if ((st = bcss_host::sym_upload_issue(P, A, dA, set, async, P->copy_in, pipe))) return st;
+    P->last_upload_bytes = P->sym_fetch_elems * (int64_t)sizeof(double);
+    trace_mark(&pipe, "A DMA half landed", P->copy_in);
+    amark(P, "DMA half landed", P->copy_in);
+    amark(P, "zero-copy half landed", P->sym_stream);
+    amark(P, "fills done", P->fill_stream);
+    trace_mark(&pipe, "A zero-copy half landed", P->sym_stream);
+    trace_mark(&pipe, "A repeated-key blocks filled", P->fill_stream);
+    cudaStreamQuery(P->sym_stream);
+    cudaStreamQuery(P->fill_stream);
+  } else {
+    for (int64_t a = 0; a < P->nbar; ++a) {
+      const size_t r0 = (size_t)first_rank_with(a, P->m, P->nbar), r1 = (size_t)first_rank_with(a + 1, P->m, P->nbar);
+      CUDA_TRY(cudaMemcpyAsync(dA + r0 * blk_a, A + r0 * blk_a, (r1 - r0) * blk_a * sizeof(double),
+                               cudaMemcpyHostToDevice, P->copy_in));
+      CUDA_TRY(cudaEventRecord(P->chunk_ev[a], P->copy_in));
+      trace_mark(&pipe, "A chunk " + std::to_string(a) + " landed", P->copy_in);
+    }
   }
   cudaStreamQuery(P->copy_in);  // kick the driver to submit queued work now
-  if ((st = run_impl(P, dA, dX, dC, P->host_stream, &pipe))) return st;
+  amark(P, "compute enqueued from here", P->host_stream);
+  st = run_impl(P, dA, dX, dC, P->host_stream, &pipe);
+  if (sym && P->d_sym_free) {
+    // release the next symmetric upload into this set once this call's
+    // kernels are done (also after a failed enqueue: nothing may wait forever)
+    const int st2 = bcss_host::sym_release_set(P, set, P->host_stream);
+    if (!st) st = st2;
+  }
+  P->sym_set_last[set] = sym;
+  if (st) return st;
   CUDA_TRY(cudaEventRecord(P->set_compute_done[set], P->host_stream));
+  amark(P, "compute done", P->host_stream);
   CUDA_TRY(cudaEventRecord(P->out2_done, P->copy_out2));
   CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->out2_done, 0));
   CUDA_TRY(cudaEventRecord(P->set_d2h_done[set], P->copy_out));
+  amark(P, "C downloaded", P->copy_out);
   if (async) {
     cudaStreamQuery(P->host_stream);  // submit
     return BCSS_OK;

@@ -184,6 +184,32 @@ struct bcss_plan {
   std::vector<int> launch_level;
   std::vector<uint64_t> launch_flops;
   cudaStream_t timed_stream = nullptr;
+  // symmetric-aware upload of pipelined host runs (sym_upload.cu): distinct-key
+  // blocks by DMA, repeated-key blocks by a zero-copy kernel that reads only
+  // the sectors holding orbit representatives and fills the rest in HBM
+  bool sym_upload = false;
+  bool sym_built = false;
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> sym_runs;  // per chunk: DMA rank runs [r0, r1)
+  std::vector<int64_t> sym_ndiag;                                   // per chunk: repeated-key blocks
+  int64_t sym_n_diag = 0;
+  std::vector<int> sym_h_rank, sym_h_chunk;  // repeated-key blocks in chunk order: rank, chunk
+  std::vector<unsigned> sym_h_run;           // and run bits (bit d: key[d] == key[d-1])
+  int64_t sym_fetch_elems = 0;
+  int64_t last_upload_bytes = -1;   // bytes of A the last host run moved (-1: none yet)      // doubles one symmetric upload moves over PCIe
+  void* d_sym = nullptr;            // device tables + counters
+  unsigned long long* d_sym_work = nullptr;
+  unsigned* d_sym_ctr = nullptr;
+  unsigned* d_sym_free = nullptr;   // per device buffer set: calls whose compute is enqueued (stream-written)
+  uint64_t sym_set_issued[2] = {0, 0}, sym_set_released[2] = {0, 0};
+  bool sym_set_last[2] = {false, false};  // the set's last host run used the symmetric upload
+  cudaStream_t fill_stream = nullptr;
+  std::vector<std::pair<std::string, cudaEvent_t>> atrace;  // BCSS_TRACE=3 marks
+  std::vector<cudaEvent_t> fill_ev;  // per chunk: its repeated-key blocks are complete
+  const int* d_sym_rank = nullptr;
+  const int* d_sym_chunk = nullptr;
+  const unsigned* d_sym_run = nullptr;
+  uint64_t sym_uploads = 0, sym_ticket_base = 0;
+  cudaStream_t sym_stream = nullptr;
 };
 
 
@@ -211,10 +237,23 @@ struct Pipe {
   // A chunk a (blocks with first index a) is resident once chunk_ev[a] fired;
   // null = the plan's own upload events (run_host)
   const cudaEvent_t* chunk_ev = nullptr;
+  // symmetric upload: chunk a is also complete once fill_ev[a] fired
+  const cudaEvent_t* fill_ev = nullptr;
+  int reserve_sms = 0;              // SMs held by the upload kernel (compute grids leave them)
+  bool serial = false;              // one compute launch at a time (streamed symmetric uploads)
   // BCSS_TRACE=1: completion events (name, event) polled after the run
   std::vector<std::pair<std::string, cudaEvent_t>>* trace = nullptr;
 };
 void trace_mark(const Pipe* pipe, const std::string& name, cudaStream_t s);
 int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStream_t s, const Pipe* pipe);
+bool sym_eligible(const bcss_plan& P);
+bool sym_supported();  // the driver exposes stream wait-value operations
+int sym_prepare(bcss_plan& P);
+int sym_device(bcss_plan& P);
+int sym_upload_ctas(bool async);
+int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool async, cudaStream_t copy_in,
+                     Pipe& pipe);
+int sym_release_set(bcss_plan* P, int set, cudaStream_t s);
+int wait_chunks(bcss_plan* P, const Pipe* pipe, const cudaEvent_t* chunk_ev, cudaStream_t s, int64_t a);
 
 }  // namespace bcss_host

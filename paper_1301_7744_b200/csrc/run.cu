@@ -188,6 +188,9 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
   int dev, sms;
   CUDA_TRY(cudaGetDevice(&dev));
   CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // a symmetric upload's kernel holds pipe->reserve_sms SMs for the whole
+  // call: persistent grids that counted on them would wait a tile's worth
+  if (pipe && pipe->reserve_sms) sms = std::max(1, sms - pipe->reserve_sms);
   int64_t launches = 0;
   if (P->timing) {
     P->launch_level.clear();
@@ -201,7 +204,12 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
   const size_t blk_c = (size_t)ipow(P->bC, P->m);
   for (size_t wi = 0; wi < P->waves.size(); ++wi) {
     const WaveHost& W = P->waves[wi];
-    const bool cascade = pipe && P->cascade && wi == 0;
+    // a streamed symmetric upload's kernel must become resident on the SMs
+    // the compute grids leave free while the previous call computes: those
+    // runs issue one compute launch at a time (concurrent launches would fill
+    // the free SMs, and the next call's upload kernel would wait for them)
+    const bool serial = pipe && pipe->serial;
+    const bool cascade = pipe && P->cascade && wi == 0 && !serial;
     if (cascade) {
       // Levels m-1..1 of the first wave as key-group sub-launches, one stream
       // per level: group g of the top level waits for A chunks 0..a_{g+1}-1,
@@ -217,7 +225,9 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         while ((int)P->lvl_stream.size() < 2 * P->m) {
           const int k = (int)P->lvl_stream.size() / 2;
-          const int prio = std::max(hi, lo - (k * (lo - hi) + P->m - 2) / std::max(1, P->m - 1));
+          // (the greatest priority stays free for the symmetric upload's streams)
+          const int top = hi < lo ? hi + 1 : hi;
+          const int prio = std::max(top, lo - (k * (lo - top) + P->m - 2) / std::max(1, P->m - 1));
           cudaStream_t ss;
           CUDA_TRY(cudaStreamCreateWithPriority(&ss, cudaStreamNonBlocking, prio));
           P->lvl_stream.push_back(ss);
@@ -238,7 +248,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
         for (int g = 0; g < G; ++g) {
           cudaStream_t ls = P->lvl_stream[2 * L.k + (g & 1)];
           if (L.k == P->m - 1) {
-            CUDA_TRY(cudaStreamWaitEvent(ls, chunk_ev[P->group_a[g + 1] - 1], 0));
+            if ((st = wait_chunks(P, pipe, chunk_ev, ls, P->group_a[g + 1] - 1))) return st;
           } else {  // groups <= g of level k+1: g on one stream, g-1 (and earlier) on the other
             CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g], 0));
             if (g > 0) CUDA_TRY(cudaStreamWaitEvent(ls, P->grp_ev[(L.k + 1) * G + g - 1], 0));
@@ -283,8 +293,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
       bool gate_split = gate && P->reuse;
       for (const LaunchHost& X : L.launches)
         gate_split = gate_split && X.parents.size() == 1 && !is_generic(X.cfg);  // key-major items only
-      if (gate && !gate_split) CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[P->nbar - 1], 0));
-      const bool conc = (P->concurrent && nl > 1) || gate_split;
+      if (gate && !gate_split && (st = wait_chunks(P, pipe, chunk_ev, s, P->nbar - 1))) return st;
+      const bool conc = !serial && ((P->concurrent && nl > 1) || gate_split);
       if (conc && (st = ensure_side(P, std::max(nl - 1, 1)))) return st;
       if (P->timing) {
         while (P->events.size() < (size_t)(2 * (level_idx + 1))) {
@@ -314,8 +324,8 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
             const LaunchHost& X = L.launches[li];
             const int64_t per_key = X.item_off.back() / L.keys_out;
             if (per_key == 0 || k_hi <= k_lo) continue;
-            cudaStream_t ls = (sub++ % 2 == 0) ? s : P->side[0];
-            CUDA_TRY(cudaStreamWaitEvent(ls, chunk_ev[a1 - 1], 0));
+            cudaStream_t ls = (serial || sub++ % 2 == 0) ? s : P->side[0];
+            if ((st = wait_chunks(P, pipe, chunk_ev, ls, a1 - 1))) return st;
             if ((st = launch_one(P, W, L, X, A, X_, C, k_lo * per_key, k_hi * per_key, ls, sms)))
               return st;
             ++launches;

@@ -572,6 +572,13 @@ struct WsLevelKernel {
       for (int fn = 0; fn < FN; ++fn) acc[fm][fn][0] = acc[fm][fn][1] = 0.0;
     int k = 0, slot = 0;
     unsigned phase = 0;
+#ifdef BCSS_SKEW
+    // the second half of the consumer warps starts SKEW slices behind the
+    // first, so one half's epilogue overlaps the other half's DMMA
+    const bool lag = warp >= NCW / 2;
+    const long long skew_at = (BCSS_SKEW < total_steps ? BCSS_SKEW : total_steps) - 1;
+    if (lag) asm volatile("bar.sync 2, %0;\n" ::"n"(NCW * 32) : "memory");
+#endif
     for (long long step = 0; step < total_steps; ++step) {
       mbar_wait(full + slot, phase);
       const int4 tl = tiles[slot];
@@ -585,6 +592,9 @@ struct WsLevelKernel {
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + slot);
+#ifdef BCSS_SKEW
+      if (!lag && step == skew_at) asm volatile("bar.arrive 2, %0;\n" ::"n"(NCW * 32) : "memory");
+#endif
       if (++slot == STAGES) { slot = 0; phase ^= 1; }
       if (last) {
         k = 0;

@@ -1,0 +1,451 @@
+// Symmetric-aware upload of a packed BCSS payload (pipelined host runs).
+//
+// A canonical block whose key repeats an index is symmetric in the modes of
+// every run of equal key entries (a BCSS tensor represents a symmetric tensor;
+// the reference's compress(t, b, tol=0) stores exactly symmetric blocks,
+// storage.py:177-216).  Only one element per orbit carries information, so the
+// upload moves:
+//   * blocks with distinct key entries: whole, by DMA (cudaMemcpyAsync of runs
+//     of consecutive ranks, copy_in stream, one event per first-index chunk);
+//   * blocks with repeats: only the 32-byte sectors that hold an orbit
+//     representative (digits nondecreasing inside every run), read straight
+//     from mapped pinned host memory by a persistent streaming kernel on a few
+//     SMs (zero-copy: SM loads skip the sectors nobody asks for; one warp per
+//     block, blocks taken in chunk order from a ticket counter, a per-chunk
+//     counter bumped after each block);
+//   * then, per chunk, a short fill kernel on a high-priority stream (it waits
+//     for the chunk's counter with a stream wait-value operation) writes every
+//     other element of the chunk's repeated-key blocks from its representative
+//     in HBM and records the chunk's fill event.
+// The compute streams wait for the chunk's DMA event and fill event.  For
+// config 5 (m=4, n=512, b=32) 72 % of A's bytes cross PCIe.
+//
+// The streaming kernel of call i+1 is launched right behind call i's (so it
+// takes the SMs call i's kernel frees) and spins, on the device, until the
+// previous call on its device buffer set has finished computing (a flag the
+// compute stream writes with cuStreamWriteValue32); the compute launches of a
+// symmetric-upload run leave those SMs free.  Counters, tickets and flags are
+// cumulative across calls, so nothing is reset between them.
+//
+// Results are bitwise those of the full upload when the repeated-key blocks
+// are exactly symmetric (compress(..., tol=0), bcss_symmetrize_blocks); for
+// blocks symmetric to rounding (the reference's random_bcss: about 1 ulp)
+// every orbit contributes its representative's value.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <string>
+#include <vector>
+
+#include "plan.hpp"
+
+namespace {
+
+// Element e of a block (32-bit: blocks of < 2^31 doubles) has digits
+// d_j = (e >> j*lb) & (b-1), mode 0 least significant.  `run` bit j (j >= 1)
+// says modes j-1 and j are a run of equal key entries.
+template <int M>
+__device__ __forceinline__ void digits(unsigned e, int lb, int (&d)[M]) {
+  const unsigned mask = (1u << lb) - 1u;
+#pragma unroll
+  for (int j = 0; j < M; ++j) d[j] = (int)((e >> (j * lb)) & mask);
+}
+
+// the 32-byte sector (4 doubles along mode 0) of this element is uploaded: it
+// holds an orbit representative (nondecreasing digits inside every run)
+template <int M>
+__device__ __forceinline__ bool fetched(const int (&d)[M], unsigned run) {
+  bool ok = !((run >> 1) & 1u) || (d[0] >> 2) <= (d[1] >> 2);
+#pragma unroll
+  for (int j = 2; j < M; ++j) ok = ok && (!((run >> j) & 1u) || d[j - 1] <= d[j]);
+  return ok;
+}
+
+// representative of element d: digits sorted inside every run
+template <int M>
+__device__ __forceinline__ unsigned rep_of(int (&d)[M], unsigned run, int passes, int lb) {
+  for (int pass = 0; pass < passes; ++pass)
+#pragma unroll
+    for (int j = 1; j < M; ++j)
+      if (((run >> j) & 1u) && d[j - 1] > d[j]) { const int x = d[j]; d[j] = d[j - 1]; d[j - 1] = x; }
+  unsigned r = 0;
+#pragma unroll
+  for (int j = M - 1; j >= 0; --j) r = (r << lb) | (unsigned)d[j];
+  return r;
+}
+
+__device__ __forceinline__ int bubble_passes(unsigned run, int m) {
+  int passes = 0;  // longest run of equal key entries - 1
+  for (int d = 1, len = 0; d < m; ++d) {
+    len = ((run >> d) & 1u) ? len + 1 : 0;
+    passes = len > passes ? len : passes;
+  }
+  return passes;
+}
+
+struct UploadArgs {
+  const double* src;          // device-mapped pointer of the pinned host payload
+  double* dst;                // device payload
+  const int* rank;            // per repeated-key block (chunk order)
+  const unsigned* run;        // bit d (d >= 1): key[d] == key[d-1]
+  const int* chunk;           // first key index of each repeated-key block
+  unsigned* ctr;              // per-chunk uploaded blocks (cumulative)
+  unsigned long long* work;   // ticket counter (cumulative)
+  unsigned long long base;    // tickets issued before this upload
+  const unsigned* set_free;   // computes finished on this device buffer set
+  unsigned set_target;        // ... needed before dst may be overwritten
+  long long n_diag;
+  long long blk;              // b^m
+  int lb;                     // log2 b (b >= 4)
+};
+
+// Streaming half: one warp per repeated-key block, only the representatives'
+// sectors, U1 16-byte zero-copy loads in flight per lane.
+template <int M>
+__global__ void __launch_bounds__(512, 1) sym_upload_kernel(const UploadArgs a) {
+#ifndef BCSS_SYM_U1
+#define BCSS_SYM_U1 12
+#endif
+  constexpr int U1 = BCSS_SYM_U1;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    // the previous call on this buffer set must have stopped reading dst;
+    // a broken pipeline must not hang the GPU: give up after ~60 s
+    long long spins = 0;
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a.set_free) : "memory");
+      if ((int)(v - a.set_target) >= 0) break;
+      __nanosleep(2000);
+      if (++spins > 30000000LL) __trap();
+    }
+  }
+  __syncthreads();
+  const unsigned blk = (unsigned)a.blk;
+  const unsigned pairs = blk >> 1;
+  for (;;) {
+    unsigned long long tk = 0;
+    if (lane == 0) tk = atomicAdd(a.work, 1ull);
+    const long long t = (long long)(__shfl_sync(0xffffffffu, tk, 0) - a.base);
+    if (t >= a.n_diag) break;
+    const unsigned run = __ldg(a.run + t);
+    const long long off = (long long)__ldg(a.rank + t) * a.blk;
+    const double2* src = reinterpret_cast<const double2*>(a.src + off);
+    double2* dst = reinterpret_cast<double2*>(a.dst + off);
+    for (unsigned p0 = lane; p0 < pairs; p0 += 32 * U1) {  // a pair shares a sector
+      double2 v[U1];
+      bool need[U1];
+#pragma unroll
+      for (int u = 0; u < U1; ++u) {
+        const unsigned p = p0 + 32 * u;
+        int d[M];
+        digits<M>(p << 1, a.lb, d);
+        need[u] = p < pairs && fetched<M>(d, run);
+        if (need[u]) v[u] = src[p];
+      }
+#pragma unroll
+      for (int u = 0; u < U1; ++u)
+        if (need[u]) dst[p0 + 32 * u] = v[u];
+    }
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();  // the block's stores before its chunk counter
+      atomicAdd(a.ctr + __ldg(a.chunk + t), 1u);
+    }
+  }
+}
+
+// Fill half, one launch per chunk: blockIdx.y = repeated-key block of the
+// chunk, threads over its elements; every element left out gets its
+// representative's value (uploaded, same block: no element is both read and
+// written).  HBM/L2-bound, U loads in flight per thread.
+template <int M>
+__global__ void __launch_bounds__(256) sym_fill_kernel(double* __restrict__ dst, const int* __restrict__ rank,
+                                                      const unsigned* __restrict__ runs, long long blk, int lb) {
+  constexpr int U = 8;
+  const unsigned run = __ldg(runs + blockIdx.y);
+  const int passes = bubble_passes(run, M);
+  double* base = dst + (long long)__ldg(rank + blockIdx.y) * blk;
+  const unsigned n = (unsigned)blk;
+  for (unsigned e0 = blockIdx.x * blockDim.x * U + threadIdx.x; e0 < n; e0 += gridDim.x * blockDim.x * U) {
+    unsigned r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const unsigned e = e0 + u * blockDim.x;
+      int d[M];
+      digits<M>(e, lb, d);
+      r[u] = (e < n && !fetched<M>(d, run)) ? rep_of<M>(d, run, passes, lb) : 0xffffffffu;
+    }
+    double v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r[u] != 0xffffffffu) v[u] = base[r[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (r[u] != 0xffffffffu) base[e0 + u * blockDim.x] = v[u];
+  }
+}
+
+using UploadFn = void (*)(const UploadArgs&, int, cudaStream_t);
+template <int M>
+void upload_m(const UploadArgs& a, int ctas, cudaStream_t s) {
+  sym_upload_kernel<M><<<ctas, 512, 0, s>>>(a);
+}
+using FillFn = void (*)(double*, const int*, const unsigned*, long long, int, dim3, cudaStream_t);
+template <int M>
+void fill_m(double* dst, const int* rank, const unsigned* runs, long long blk, int lb, dim3 grid, cudaStream_t s) {
+  sym_fill_kernel<M><<<grid, 256, 0, s>>>(dst, rank, runs, blk, lb);
+}
+
+using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+template <class F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return reinterpret_cast<F>(p);
+}
+WaitFn wait_value_fn() {
+  static WaitFn fn = driver_fn<WaitFn>("cuStreamWaitValue32");
+  return fn;
+}
+WriteFn write_value_fn() {
+  static WriteFn fn = driver_fn<WriteFn>("cuStreamWriteValue32");
+  return fn;
+}
+
+int64_t binom(int64_t n, int64_t k) {
+  if (k < 0 || n < k) return 0;
+  int64_t r = 1;
+  for (int64_t i = 1; i <= k; ++i) r = r * (n - k + i) / i;
+  return r;
+}
+
+// doubles uploaded for one block with the given run bits (sector granular)
+int64_t fetched_elems(unsigned run, int m, int64_t b) {
+  int64_t total = 1;
+  for (int d = 0; d < m;) {
+    int q = d + 1;
+    while (q < m && ((run >> q) & 1u)) ++q;
+    const int r = q - d;  // run of r equal key entries: modes d..q-1
+    if (d > 0 || r == 1) {
+      total *= binom(b + r - 1, r);  // nondecreasing r-tuples
+    } else {
+      // first run, mode 0 by sectors: rows (d1 <= ... <= d_{r-1}) carry the
+      // sectors of mode 0 up to d1's
+      int64_t s = 0;
+      for (int64_t d1 = 0; d1 < b; ++d1)
+        s += binom(b - d1 + r - 3, r - 2) * std::min<int64_t>(b, (d1 / 4 + 1) * 4);
+      total *= s;
+    }
+    d = q;
+  }
+  return total;
+}
+
+}  // namespace
+
+namespace bcss_host {
+
+bool sym_eligible(const bcss_plan& P) {
+  return P.sym_upload && P.m >= 2 && P.m <= 8 && is_pow2(P.bA) && P.bA >= 4 && ipow(P.bA, P.m) < (int64_t(1) << 31);
+}
+
+bool sym_supported() { return wait_value_fn() != nullptr && write_value_fn() != nullptr; }
+
+int sym_prepare(bcss_plan& P) {
+  if (P.sym_built) return BCSS_OK;
+  const int m = P.m;
+  const int64_t nb = P.nbar;
+  std::vector<int> rank, chunk;
+  std::vector<unsigned> runs;
+  P.sym_runs.assign((size_t)nb, {});
+  P.sym_ndiag.assign((size_t)nb, 0);
+  P.sym_fetch_elems = 0;
+  const int64_t blk = ipow(P.bA, m);
+  try {
+    const std::vector<int32_t> keys = bcss::hypertriangle_list(nb, m);
+    const int64_t n = (int64_t)keys.size() / m;
+    for (int64_t r = 0; r < n; ++r) {
+      const int32_t* k = &keys[(size_t)(r * m)];
+      unsigned run = 0;
+      for (int d = 1; d < m; ++d)
+        if (k[d] == k[d - 1]) run |= 1u << d;
+      auto& rs = P.sym_runs[(size_t)k[0]];
+      if (run) {
+        rank.push_back((int)r);
+        runs.push_back(run);
+        chunk.push_back(k[0]);
+        ++P.sym_ndiag[(size_t)k[0]];
+        P.sym_fetch_elems += fetched_elems(run, m, P.bA);
+      } else {
+        if (!rs.empty() && rs.back().second == r) rs.back().second = r + 1;
+        else rs.emplace_back(r, r + 1);
+        P.sym_fetch_elems += blk;
+      }
+    }
+  } catch (const std::exception& e) {
+    return fail(BCSS_ERR_PARAMETER, "%s", e.what());
+  }
+  P.sym_n_diag = (int64_t)rank.size();
+  P.sym_h_rank.swap(rank);
+  P.sym_h_chunk.swap(chunk);
+  P.sym_h_run.swap(runs);
+  P.sym_built = true;
+  return BCSS_OK;
+}
+
+// device tables and counters of the symmetric upload (on first use):
+// [0,64) ticket counter, [64,128) per-set "computes done" flags, then the
+// per-chunk counters and the tables
+int sym_device(bcss_plan& P) {
+  if (P.d_sym) return BCSS_OK;
+  const int64_t nb = P.nbar;
+  const size_t nd = P.sym_h_rank.size();
+  const size_t head = 128 + (size_t)nb * sizeof(unsigned);
+  const size_t bytes = head + nd * (2 * sizeof(int) + sizeof(unsigned));
+  CUDA_TRY(cudaMalloc(&P.d_sym, bytes));
+  char* base = static_cast<char*>(P.d_sym);
+  P.d_sym_work = reinterpret_cast<unsigned long long*>(base);
+  P.d_sym_free = reinterpret_cast<unsigned*>(base + 64);
+  P.d_sym_ctr = reinterpret_cast<unsigned*>(base + 128);
+  int* d_rank = reinterpret_cast<int*>(base + head);
+  int* d_chunk = d_rank + nd;
+  unsigned* d_run = reinterpret_cast<unsigned*>(d_chunk + nd);
+  CUDA_TRY(cudaMemset(base, 0, head));
+  if (nd) {
+    CUDA_TRY(cudaMemcpy(d_rank, P.sym_h_rank.data(), nd * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_chunk, P.sym_h_chunk.data(), nd * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_run, P.sym_h_run.data(), nd * sizeof(unsigned), cudaMemcpyHostToDevice));
+  }
+  P.d_sym_rank = d_rank;
+  P.d_sym_chunk = d_chunk;
+  P.d_sym_run = d_run;
+  P.sym_uploads = 0;
+  P.sym_ticket_base = 0;
+  P.sym_set_issued[0] = P.sym_set_issued[1] = 0;
+  P.sym_set_released[0] = P.sym_set_released[1] = 0;
+  return BCSS_OK;
+}
+
+// SMs (one CTA each) for the streaming kernel: streamed (async) calls share
+// the GPU with the previous call's compute, so fewer; a synchronous call's
+// upload runs while the gated compute mostly waits for chunks, so more
+// (measured on config 5: 4 / 6).  BCSS_SYM_CTAS overrides both.
+int sym_upload_ctas(bool async) {
+  static int env = [] {
+    const char* e = getenv("BCSS_SYM_CTAS");
+    return e ? std::max(1, atoi(e)) : 0;
+  }();
+  return env ? env : (async ? 4 : 6);
+}
+
+// Issue one symmetric upload of A (pinned host `A`, device `dA`, buffer set
+// `set`): the DMA half on copy_in (chunk events), the streaming kernel on
+// P->sym_stream, the per-chunk fills on P->fill_stream (fill events).
+int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool async, cudaStream_t copy_in,
+                     Pipe& pipe) {
+  const size_t blk = (size_t)ipow(P->bA, P->m);
+  int st = sym_device(*P);
+  if (st) return st;
+  const double* srcd = nullptr;
+  if (P->sym_n_diag) CUDA_TRY(cudaHostGetDevicePointer((void**)&srcd, const_cast<double*>(A), 0));
+  for (int64_t a = 0; a < P->nbar; ++a) {
+    for (const auto& r : P->sym_runs[(size_t)a])
+      CUDA_TRY(cudaMemcpyAsync(dA + (size_t)r.first * blk, A + (size_t)r.first * blk,
+                               (size_t)(r.second - r.first) * blk * sizeof(double), cudaMemcpyHostToDevice, copy_in));
+    CUDA_TRY(cudaEventRecord(P->chunk_ev[(size_t)a], copy_in));
+  }
+  pipe.fill_ev = nullptr;
+  if (P->sym_n_diag == 0) return BCSS_OK;
+  // keep the cumulative chunk counters inside 32 bits (rare reset)
+  int64_t maxd = 0;
+  for (int64_t v : P->sym_ndiag) maxd = std::max(maxd, v);
+  if ((uint64_t)maxd * (P->sym_uploads + 2) >= (1ull << 31)) {
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemset(P->d_sym_ctr, 0, (size_t)P->nbar * sizeof(unsigned)));
+    P->sym_uploads = 0;
+  }
+  const uint64_t u = P->sym_uploads++;
+  UploadArgs ua;
+  ua.src = srcd;
+  ua.dst = dA;
+  ua.rank = P->d_sym_rank;
+  ua.run = P->d_sym_run;
+  ua.chunk = P->d_sym_chunk;
+  ua.ctr = P->d_sym_ctr;
+  ua.work = P->d_sym_work;
+  ua.base = P->sym_ticket_base;
+  ua.set_free = P->d_sym_free + set;
+  ua.set_target = P->sym_set_issued[set];  // computes on this set enqueued before this call
+  ua.n_diag = P->sym_n_diag;
+  ua.blk = (long long)blk;
+  ua.lb = ilog2(P->bA);
+  static const UploadFn ups[9] = {nullptr, nullptr, upload_m<2>, upload_m<3>, upload_m<4>,
+                                  upload_m<5>, upload_m<6>, upload_m<7>, upload_m<8>};
+  static const FillFn fills[9] = {nullptr, nullptr, fill_m<2>, fill_m<3>, fill_m<4>,
+                                  fill_m<5>, fill_m<6>, fill_m<7>, fill_m<8>};
+  const int ctas = sym_upload_ctas(async);
+  pipe.reserve_sms = ctas;
+  pipe.serial = async;
+  ups[P->m](ua, ctas, P->sym_stream);
+  CUDA_TRY(cudaGetLastError());
+  // every warp takes tickets until one is past the list: n_diag + warps in all
+  P->sym_ticket_base += (uint64_t)P->sym_n_diag + (uint64_t)ctas * 16;
+  // fills, chunk by chunk, as the chunk's repeated-key blocks land
+  while (P->fill_ev.size() < (size_t)P->nbar) {
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    P->fill_ev.push_back(ev);
+  }
+  WaitFn wait = wait_value_fn();
+  int64_t first = 0;
+  const unsigned per_blk_ctas = (unsigned)std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)blk / (256 * 8 * 4)));
+  for (int64_t a = 0; a < P->nbar; ++a) {
+    const int64_t nd = P->sym_ndiag[(size_t)a];
+    if (nd) {
+      const unsigned target = (unsigned)((u + 1) * (uint64_t)nd);
+      const CUresult r = wait(reinterpret_cast<CUstream>(P->fill_stream),
+                              reinterpret_cast<CUdeviceptr>(P->d_sym_ctr + a), target, CU_STREAM_WAIT_VALUE_GEQ);
+      if (r != CUDA_SUCCESS) return fail(BCSS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
+      fills[P->m](dA, P->d_sym_rank + first, P->d_sym_run + first, (long long)blk, ilog2(P->bA),
+                  dim3(per_blk_ctas, (unsigned)nd), P->fill_stream);
+      CUDA_TRY(cudaGetLastError());
+      first += nd;
+    }
+    CUDA_TRY(cudaEventRecord(P->fill_ev[(size_t)a], P->fill_stream));
+    if (a % 4 == 3) trace_mark(&pipe, "A chunk " + std::to_string(a) + " filled", P->fill_stream);
+  }
+  pipe.fill_ev = P->fill_ev.data();
+  return BCSS_OK;
+}
+
+// Everything that reads buffer set `set` in this call is enqueued on `s` up
+// to here: release the next symmetric upload into that set.  Called once per
+// symmetric-upload call (also on its error paths, so no upload kernel waits
+// for a call that never comes).
+int sym_release_set(bcss_plan* P, int set, cudaStream_t s) {
+  if (!P->d_sym_free) return BCSS_OK;
+  ++P->sym_set_issued[set];
+  const CUresult r = write_value_fn()(reinterpret_cast<CUstream>(s),
+                                      reinterpret_cast<CUdeviceptr>(P->d_sym_free + set),
+                                      ++P->sym_set_released[set], 0);
+  if (r != CUDA_SUCCESS) return fail(BCSS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  return BCSS_OK;
+}
+
+// stream s waits until A chunks 0..a are resident (DMA events + fill events)
+int wait_chunks(bcss_plan* P, const Pipe* pipe, const cudaEvent_t* chunk_ev, cudaStream_t s, int64_t a) {
+  (void)P;
+  CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[a], 0));
+  if (pipe && pipe->fill_ev) CUDA_TRY(cudaStreamWaitEvent(s, pipe->fill_ev[a], 0));
+  return BCSS_OK;
+}
+
+}  // namespace bcss_host

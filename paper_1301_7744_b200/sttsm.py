@@ -61,7 +61,8 @@ class SttsmPlan:
 
     def __init__(self, m: int, n: int, p: int, b_a: int, b_c: int, reuse: bool = True,
                  units=None, workspace_limit: int = 0, keep_temps: bool = False, pipeline: int = 0,
-                 stop_level: int = 0, start_level: int | None = None, start_calls=None, start_children=None):
+                 stop_level: int = 0, start_level: int | None = None, start_calls=None, start_children=None,
+                 symmetric_upload: bool = False):
         lib = _native.lib()
         self.m, self.n, self.p, self.b_a, self.b_c, self.reuse = m, n, p, b_a, b_c, bool(reuse)
         h = ctypes.c_void_p()
@@ -78,6 +79,10 @@ class SttsmPlan:
         if pipeline:
             # run_host overlaps A upload / compute / C download over `pipeline` waves
             _native.check(lib.bcss_plan_set_pipeline(h, int(pipeline)))
+        if symmetric_upload:
+            # pipelined host runs move only the orbit representatives of the
+            # repeated-key blocks (bit-identical for exactly symmetric blocks)
+            _native.check(lib.bcss_plan_set_symmetric_upload(h, 1))
         if stop_level:
             # partial run: stop after level `stop_level`, its T goes to the output buffer
             _native.check(lib.bcss_plan_set_stop_level(h, int(stop_level)))
@@ -99,6 +104,7 @@ class SttsmPlan:
         ie, oe = ctypes.c_int64(), ctypes.c_int64()
         _native.check(lib.bcss_plan_io_elems(h, ctypes.byref(ie), ctypes.byref(oe)))
         self.a_elems = int(ie.value)   # input buffer: A, or start-level temporaries
+        self.symmetric_upload = bool(symmetric_upload)
         self.c_elems = int(oe.value)   # output buffer: C, or stop-level temporaries
 
     # ---- lifecycle ------------------------------------------------------------
@@ -119,6 +125,21 @@ class SttsmPlan:
     def workspace_bytes(self) -> int:
         out = ctypes.c_size_t()
         _native.check(_native.lib().bcss_plan_workspace_bytes(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    @property
+    def upload_bytes(self) -> int:
+        """Bytes of A one host run moves to the device (less than A's payload
+        when a symmetric upload applies)."""
+        out = ctypes.c_int64()
+        _native.check(_native.lib().bcss_plan_upload_bytes(self._h, ctypes.byref(out)))
+        return int(out.value)
+
+    @property
+    def last_upload_bytes(self) -> int:
+        """Bytes of A the last host run moved (-1 before the first)."""
+        out = ctypes.c_int64()
+        _native.check(_native.lib().bcss_plan_last_upload_bytes(self._h, ctypes.byref(out)))
         return int(out.value)
 
     def stats(self) -> dict:
