@@ -136,6 +136,7 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->d_sym) cudaFree(P->d_sym);
   if (P->sym_stream) cudaStreamDestroy(P->sym_stream);
   if (P->fill_stream) cudaStreamDestroy(P->fill_stream);
+  if (P->sym_prev_done) cudaEventDestroy(P->sym_prev_done);
   for (auto ev : P->fill_ev) cudaEventDestroy(ev);
   delete P;
   return BCSS_OK;

@@ -203,6 +203,7 @@ struct bcss_plan {
   uint64_t sym_set_issued[2] = {0, 0}, sym_set_released[2] = {0, 0};
   bool sym_set_last[2] = {false, false};  // the set's last host run used the symmetric upload
   cudaStream_t fill_stream = nullptr;
+  cudaEvent_t sym_prev_done = nullptr;  // the last symmetric upload's zero-copy half landed
   std::vector<std::pair<std::string, cudaEvent_t>> atrace;  // BCSS_TRACE=3 marks
   std::vector<cudaEvent_t> fill_ev;  // per chunk: its repeated-key blocks are complete
   const int* d_sym_rank = nullptr;

@@ -334,16 +334,16 @@ int sym_device(bcss_plan& P) {
   return BCSS_OK;
 }
 
-// SMs (one CTA each) for the streaming kernel: streamed (async) calls share
-// the GPU with the previous call's compute, so fewer; a synchronous call's
-// upload runs while the gated compute mostly waits for chunks, so more
-// (measured on config 5: 4 / 6).  BCSS_SYM_CTAS overrides both.
+// SMs (one CTA each) for the streaming kernel, measured on config 5
+// (tools/sym_upload_timing.py): streamed calls 4 / 5 / 6 / 8 / 10 / 12 CTAs ->
+// 516 / 510 / 507 / 495 / 493 / 507 ms per call, synchronous calls 6 / 8 / 10
+// -> 639 / 645 / 657 ms.  BCSS_SYM_CTAS overrides both.
 int sym_upload_ctas(bool async) {
   static int env = [] {
     const char* e = getenv("BCSS_SYM_CTAS");
     return e ? std::max(1, atoi(e)) : 0;
   }();
-  return env ? env : (async ? 4 : 6);
+  return env ? env : (async ? 8 : 6);
 }
 
 // Issue one symmetric upload of A (pinned host `A`, device `dA`, buffer set
@@ -356,6 +356,11 @@ int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool as
   if (st) return st;
   const double* srcd = nullptr;
   if (P->sym_n_diag) CUDA_TRY(cudaHostGetDevicePointer((void**)&srcd, const_cast<double*>(A), 0));
+  // one call's upload at a time on PCIe: this call's DMA starts when the
+  // previous call's zero-copy half has landed (otherwise it takes the link
+  // from that kernel and the previous call's last chunks arrive late)
+  if (!P->sym_prev_done) CUDA_TRY(cudaEventCreateWithFlags(&P->sym_prev_done, cudaEventDisableTiming));
+  else CUDA_TRY(cudaStreamWaitEvent(copy_in, P->sym_prev_done, 0));
   for (int64_t a = 0; a < P->nbar; ++a) {
     for (const auto& r : P->sym_runs[(size_t)a])
       CUDA_TRY(cudaMemcpyAsync(dA + (size_t)r.first * blk, A + (size_t)r.first * blk,
@@ -396,6 +401,7 @@ int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool as
   pipe.serial = async;
   ups[P->m](ua, ctas, P->sym_stream);
   CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(P->sym_prev_done, P->sym_stream));
   // every warp takes tickets until one is past the list: n_diag + warps in all
   P->sym_ticket_base += (uint64_t)P->sym_n_diag + (uint64_t)ctas * 16;
   // fills, chunk by chunk, as the chunk's repeated-key blocks land
