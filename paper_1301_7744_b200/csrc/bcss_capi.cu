@@ -99,6 +99,11 @@ int bcss_plan_create(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int 
 
 int bcss_plan_destroy(bcss_plan* P) {
   if (!P) return BCSS_OK;
+  // nothing of this plan may still run when its buffers go (a streamed
+  // symmetric upload's kernel and fills live on their own streams)
+  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream, P->sym_stream, P->fill_stream})
+    if (q) cudaStreamSynchronize(q);
+  cudaGetLastError();
   if (P->d_tables) cudaFree(P->d_tables);
   if (P->d_ws && P->own_ws) cudaFree(P->d_ws);
   if (P->hA) cudaFree(P->hA);
