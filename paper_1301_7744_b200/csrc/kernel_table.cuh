@@ -24,13 +24,23 @@ KernelCfg make_cfg(const char* name) {
   return KernelCfg{K::BM, K::BN, K::NT, K::SMEM_BYTES, level_kernel<K>, name};
 }
 
+// shape 3 (the large levels' 128x128 tile): slice depth and stages can be
+// changed for experiments (-DBCSS_S3_BK=16 -DBCSS_S3_ST=5)
+#ifndef BCSS_S3_BK
+#define BCSS_S3_BK 32
+#endif
+#ifndef BCSS_S3_ST
+#define BCSS_S3_ST 3
+#endif
+#define BCSS_SHAPE3(BA) WsLevelKernel<128, 128, BCSS_S3_BK, 4, 4, BCSS_S3_ST, BA>
+
 // Fast tile shapes (BM, BN, BK, warps WM x WN, stages), in the order the
 // plan's shape policy indexes them.  Every b_a instantiates the same list.
 #define BCSS_FAST_SHAPES(X, BA)                                        \
   X((WsLevelKernel<128, 128, 32, 2, 4, 3, BA>), "ws128x128c8")    \
   X((WsLevelKernel<64, 256, 16, 2, 4, 4, BA>), "ws64x256c8")      \
   X((WsLevelKernel<32, 256, 32, 1, 8, 3, BA>), "ws32x256c8")      \
-  X((WsLevelKernel<128, 128, 32, 4, 4, 3, BA>), "ws128x128c16")   \
+  X((BCSS_SHAPE3(BA)), "ws128x128c16")   \
   X((WsLevelKernel<64, 256, 16, 2, 8, 4, BA>), "ws64x256c16")     \
   X((WsLevelKernel<32, 256, 32, 1, 16, 3, BA>), "ws32x256c16")     \
   X((WsLevelKernel<16, 512, 16, 1, 16, 3, BA>), "ws16x512c16k16") \
