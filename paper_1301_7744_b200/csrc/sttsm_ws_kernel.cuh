@@ -575,8 +575,11 @@ struct WsLevelKernel {
 #ifdef BCSS_SKEW
     // the second half of the consumer warps starts SKEW slices behind the
     // first, so one half's epilogue overlaps the other half's DMMA
+    // (at most STAGES: the leading half cannot get further ahead without the
+    // lagging half releasing slots)
+    constexpr int SKEW = BCSS_SKEW < STAGES ? BCSS_SKEW : STAGES;
     const bool lag = warp >= NCW / 2;
-    const long long skew_at = (BCSS_SKEW < total_steps ? BCSS_SKEW : total_steps) - 1;
+    const long long skew_at = (SKEW < total_steps ? SKEW : total_steps) - 1;
     if (lag) asm volatile("bar.sync 2, %0;\n" ::"n"(NCW * 32) : "memory");
 #endif
     for (long long step = 0; step < total_steps; ++step) {
