@@ -101,8 +101,11 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (!P) return BCSS_OK;
   // nothing of this plan may still run when its buffers go (a streamed
   // symmetric upload's kernel and fills live on their own streams)
-  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream, P->sym_stream, P->fill_stream})
+  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream, P->sym_stream, P->fill_stream,
+                         P->g_host_stream, P->g_sym_stream})
     if (q) cudaStreamSynchronize(q);
+  for (cudaStream_t q : P->g_side) cudaStreamSynchronize(q);
+  for (cudaStream_t q : P->g_lvl_stream) cudaStreamSynchronize(q);
   cudaGetLastError();
   if (P->d_tables) cudaFree(P->d_tables);
   if (P->d_ws && P->own_ws) cudaFree(P->d_ws);
@@ -142,6 +145,7 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->sym_stream) cudaStreamDestroy(P->sym_stream);
   if (P->fill_stream) cudaStreamDestroy(P->fill_stream);
   if (P->sym_prev_done) cudaEventDestroy(P->sym_prev_done);
+  bcss_host::green_destroy(P);
   for (auto ev : P->fill_ev) cudaEventDestroy(ev);
   delete P;
   return BCSS_OK;
@@ -564,7 +568,8 @@ int bcss_sttsm_run_host_async(bcss_plan* P, const double* A, const double* X, do
 
 int bcss_plan_wait(bcss_plan* P) {
   if (!P) return fail(BCSS_ERR_STATE, "null plan");
-  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream, P->sym_stream, P->fill_stream})
+  for (cudaStream_t q : {P->copy_in, P->copy_out, P->copy_out2, P->host_stream, P->sym_stream, P->fill_stream,
+                         P->g_host_stream, P->g_sym_stream})
     if (q) CUDA_TRY(cudaStreamSynchronize(q));
   if (!P->atrace.empty()) {  // BCSS_TRACE=3: device timeline of the streamed calls
     fprintf(stderr, "[bcss trace] streamed host runs (device ms since the first mark):\n");
@@ -682,10 +687,23 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   };
   if ((st = need_events(P->chunk_ev, (size_t)P->nbar))) return st;
   if ((st = need_events(P->wave_ev, P->waves.size()))) return st;
+  // symmetric upload: distinct-key blocks by DMA, repeated-key blocks by the
+  // zero-copy streaming kernel + per-chunk fills (sym_upload.cu); with an SM
+  // partition (green contexts) its kernel and the compute never share SMs
+  bool sym = bcss_host::sym_eligible(*P) && bcss_host::sym_supported();
+  if (sym) {
+    cudaPointerAttributes at;
+    sym = cudaPointerGetAttributes(&at, A) == cudaSuccess && at.devicePointer != nullptr;
+    cudaGetLastError();
+  }
+  if (sym && (st = bcss_host::sym_prepare(*P))) return st;
+  const bool green = sym && P->sym_n_zc > 0 && bcss_host::sym_green(P) == BCSS_OK;
+  cudaGetLastError();
+  cudaStream_t hs = green ? P->g_host_stream : P->host_stream;  // the compute's main stream
   // this set's device buffers: the upload waits until the set's previous call
   // stopped reading A / X, the kernels until its C was downloaded
   CUDA_TRY(cudaStreamWaitEvent(P->copy_in, P->set_compute_done[set], 0));
-  CUDA_TRY(cudaStreamWaitEvent(P->host_stream, P->set_d2h_done[set], 0));
+  CUDA_TRY(cudaStreamWaitEvent(hs, P->set_d2h_done[set], 0));
   Pipe pipe;
   pipe.c_host = C;
   std::vector<std::pair<std::string, cudaEvent_t>> trace;
@@ -694,32 +712,24 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   trace_mark(&pipe, "upload start", P->copy_in);
   amark(P, "upload start (copy_in)", P->copy_in);
   CUDA_TRY(cudaMemcpyAsync(dX, X, x_bytes, cudaMemcpyHostToDevice, P->copy_in));
-  // symmetric upload: distinct-key blocks by DMA, repeated-key blocks by the
-  // zero-copy streaming kernel + per-chunk fills (sym_upload.cu)
-  bool sym = bcss_host::sym_eligible(*P) && bcss_host::sym_supported();
   if (sym) {
-    cudaPointerAttributes at;
-    sym = cudaPointerGetAttributes(&at, A) == cudaSuccess && at.devicePointer != nullptr;
-    cudaGetLastError();
-  }
-  if (sym) {
-    if ((st = bcss_host::sym_prepare(*P))) return st;
     int lo = 0, hi = 0;
     CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     if (!P->sym_stream) CUDA_TRY(cudaStreamCreateWithPriority(&P->sym_stream, cudaStreamNonBlocking, hi));
     if (!P->fill_stream) CUDA_TRY(cudaStreamCreateWithPriority(&P->fill_stream, cudaStreamNonBlocking, hi));
+    cudaStream_t us = green ? P->g_sym_stream : P->sym_stream;
     // the kernel waits on the device for the set's previous symmetric run; a
     // previous full-upload run on this set is waited for here
-    if (!P->sym_set_last[set]) CUDA_TRY(cudaStreamWaitEvent(P->sym_stream, P->set_compute_done[set], 0));
-    if ((st = bcss_host::sym_upload_issue(P, A, dA, set, async, P->copy_in, pipe))) return st;
+    if (!P->sym_set_last[set]) CUDA_TRY(cudaStreamWaitEvent(us, P->set_compute_done[set], 0));
+    if ((st = bcss_host::sym_upload_issue(P, A, dA, set, async, green, P->copy_in, us, pipe))) return st;
     P->last_upload_bytes = P->sym_fetch_elems * (int64_t)sizeof(double);
     trace_mark(&pipe, "A DMA half landed", P->copy_in);
     amark(P, "DMA half landed", P->copy_in);
-    amark(P, "zero-copy half landed", P->sym_stream);
+    amark(P, "zero-copy half landed", us);
     amark(P, "fills done", P->fill_stream);
-    trace_mark(&pipe, "A zero-copy half landed", P->sym_stream);
+    trace_mark(&pipe, "A zero-copy half landed", us);
     trace_mark(&pipe, "A repeated-key blocks filled", P->fill_stream);
-    cudaStreamQuery(P->sym_stream);
+    cudaStreamQuery(us);
     cudaStreamQuery(P->fill_stream);
   } else {
     for (int64_t a = 0; a < P->nbar; ++a) {
@@ -731,24 +741,34 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
     }
   }
   cudaStreamQuery(P->copy_in);  // kick the driver to submit queued work now
-  amark(P, "compute enqueued from here", P->host_stream);
-  st = run_impl(P, dA, dX, dC, P->host_stream, &pipe);
+  amark(P, "compute enqueued from here", hs);
+  if (green) {  // side and level streams of the compute partition
+    std::swap(P->side, P->g_side);
+    std::swap(P->lvl_stream, P->g_lvl_stream);
+    P->green_active = true;
+  }
+  st = run_impl(P, dA, dX, dC, hs, &pipe);
+  if (green) {
+    std::swap(P->side, P->g_side);
+    std::swap(P->lvl_stream, P->g_lvl_stream);
+    P->green_active = false;
+  }
   if (sym && P->d_sym_free) {
     // release the next symmetric upload into this set once this call's
     // kernels are done (also after a failed enqueue: nothing may wait forever)
-    const int st2 = bcss_host::sym_release_set(P, set, P->host_stream);
+    const int st2 = bcss_host::sym_release_set(P, set, hs);
     if (!st) st = st2;
   }
   P->sym_set_last[set] = sym;
   if (st) return st;
-  CUDA_TRY(cudaEventRecord(P->set_compute_done[set], P->host_stream));
-  amark(P, "compute done", P->host_stream);
+  CUDA_TRY(cudaEventRecord(P->set_compute_done[set], hs));
+  amark(P, "compute done", hs);
   CUDA_TRY(cudaEventRecord(P->out2_done, P->copy_out2));
   CUDA_TRY(cudaStreamWaitEvent(P->copy_out, P->out2_done, 0));
   CUDA_TRY(cudaEventRecord(P->set_d2h_done[set], P->copy_out));
   amark(P, "C downloaded", P->copy_out);
   if (async) {
-    cudaStreamQuery(P->host_stream);  // submit
+    cudaStreamQuery(hs);  // submit
     return BCSS_OK;
   }
   if (pipe.trace) {
@@ -773,7 +793,7 @@ static int run_host_pinned(bcss_plan* P, const double* A, const double* X, doubl
   CUDA_TRY(cudaStreamSynchronize(P->copy_out));
   const auto h2 = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(P->copy_out2));
-  CUDA_TRY(cudaStreamSynchronize(P->host_stream));
+  CUDA_TRY(cudaStreamSynchronize(hs));
   const auto h3 = std::chrono::steady_clock::now();
   if (tr && atoi(tr) == 2)
     fprintf(stderr, "[bcss trace] enqueue %.3f ms, copy_out sync at %.3f ms, all synced at %.3f ms\n",

@@ -190,10 +190,13 @@ struct bcss_plan {
   bool sym_upload = false;
   bool sym_built = false;
   std::vector<std::vector<std::pair<int64_t, int64_t>>> sym_runs;  // per chunk: DMA rank runs [r0, r1)
-  std::vector<int64_t> sym_ndiag;                                   // per chunk: repeated-key blocks
-  int64_t sym_n_diag = 0;
-  std::vector<int> sym_h_rank, sym_h_chunk;  // repeated-key blocks in chunk order: rank, chunk
-  std::vector<unsigned> sym_h_run;           // and run bits (bit d: key[d] == key[d-1])
+  bool sym_dma = true;              // distinct-key blocks by DMA (long runs) or by the zero-copy kernel
+  std::vector<int64_t> sym_nzc, sym_nfill;  // per chunk: zero-copy blocks, repeated-key blocks to fill
+  int64_t sym_n_zc = 0;
+  std::vector<int> sym_h_rank, sym_h_chunk;  // the zero-copy kernel's blocks in chunk order: rank, chunk
+  std::vector<unsigned> sym_h_run;           // and run bits (bit d: key[d] == key[d-1]; 0: distinct key)
+  std::vector<int> sym_h_frank;              // repeated-key blocks (the fills), chunk order
+  std::vector<unsigned> sym_h_frun;
   int64_t sym_fetch_elems = 0;
   int64_t last_upload_bytes = -1;   // bytes of A the last host run moved (-1: none yet)      // doubles one symmetric upload moves over PCIe
   void* d_sym = nullptr;            // device tables + counters
@@ -204,11 +207,21 @@ struct bcss_plan {
   bool sym_set_last[2] = {false, false};  // the set's last host run used the symmetric upload
   cudaStream_t fill_stream = nullptr;
   cudaEvent_t sym_prev_done = nullptr;  // the last symmetric upload's zero-copy half landed
+  // SM partition for symmetric-upload runs (green contexts, sym_upload.cu)
+  int green_state = 0;              // 0 untried, 1 ready, -1 unavailable
+  void* g_up = nullptr;             // CUgreenCtx: the upload kernel's SMs
+  void* g_comp = nullptr;           // CUgreenCtx: the rest (compute)
+  int g_up_sms = 0;
+  cudaStream_t g_sym_stream = nullptr, g_host_stream = nullptr;
+  std::vector<cudaStream_t> g_side, g_lvl_stream;  // swapped into side / lvl_stream during green runs
+  bool green_active = false;
   std::vector<std::pair<std::string, cudaEvent_t>> atrace;  // BCSS_TRACE=3 marks
   std::vector<cudaEvent_t> fill_ev;  // per chunk: its repeated-key blocks are complete
   const int* d_sym_rank = nullptr;
   const int* d_sym_chunk = nullptr;
   const unsigned* d_sym_run = nullptr;
+  const int* d_sym_frank = nullptr;
+  const unsigned* d_sym_frun = nullptr;
   uint64_t sym_uploads = 0, sym_ticket_base = 0;
   cudaStream_t sym_stream = nullptr;
 };
@@ -252,8 +265,11 @@ bool sym_supported();  // the driver exposes stream wait-value operations
 int sym_prepare(bcss_plan& P);
 int sym_device(bcss_plan& P);
 int sym_upload_ctas(bool async);
-int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool async, cudaStream_t copy_in,
-                     Pipe& pipe);
+int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool async, bool green,
+                     cudaStream_t copy_in, cudaStream_t up_stream, Pipe& pipe);
+int sym_green(bcss_plan* P);
+int green_compute_stream(bcss_plan* P, int priority, cudaStream_t* out);
+void green_destroy(bcss_plan* P);
 int sym_release_set(bcss_plan* P, int set, cudaStream_t s);
 int wait_chunks(bcss_plan* P, const Pipe* pipe, const cudaEvent_t* chunk_ev, cudaStream_t s, int64_t a);
 

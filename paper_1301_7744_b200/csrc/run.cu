@@ -94,7 +94,12 @@ __global__ void gather_row_blocks(const double* __restrict__ src, double* __rest
 int ensure_side(bcss_plan* P, int n) {
   while ((int)P->side.size() < n) {
     cudaStream_t ss;
-    CUDA_TRY(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    if (P->green_active) {  // a green symmetric-upload run: the compute partition
+      const int st = green_compute_stream(P, 0, &ss);
+      if (st) return st;
+    } else {
+      CUDA_TRY(cudaStreamCreateWithFlags(&ss, cudaStreamNonBlocking));
+    }
     P->side.push_back(ss);
     cudaEvent_t ev;
     CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -229,7 +234,11 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
           const int top = hi < lo ? hi + 1 : hi;
           const int prio = std::max(top, lo - (k * (lo - top) + P->m - 2) / std::max(1, P->m - 1));
           cudaStream_t ss;
-          CUDA_TRY(cudaStreamCreateWithPriority(&ss, cudaStreamNonBlocking, prio));
+          if (P->green_active) {
+            if ((st = green_compute_stream(P, prio, &ss))) return st;
+          } else {
+            CUDA_TRY(cudaStreamCreateWithPriority(&ss, cudaStreamNonBlocking, prio));
+          }
           P->lvl_stream.push_back(ss);
         }
       }

@@ -96,7 +96,7 @@ struct UploadArgs {
   unsigned long long base;    // tickets issued before this upload
   const unsigned* set_free;   // computes finished on this device buffer set
   unsigned set_target;        // ... needed before dst may be overwritten
-  long long n_diag;
+  long long n_diag;           // blocks on the zero-copy list
   long long blk;              // b^m
   int lb;                     // log2 b (b >= 4)
 };
@@ -134,6 +134,17 @@ __global__ void __launch_bounds__(512, 1) sym_upload_kernel(const UploadArgs a) 
     const long long off = (long long)__ldg(a.rank + t) * a.blk;
     const double2* src = reinterpret_cast<const double2*>(a.src + off);
     double2* dst = reinterpret_cast<double2*>(a.dst + off);
+    if (run == 0) {  // a distinct-key block: all of it, no predicates
+      for (unsigned p0 = lane; p0 < pairs; p0 += 32 * U1) {
+        double2 v[U1];
+#pragma unroll
+        for (int u = 0; u < U1; ++u)
+          if (p0 + 32 * u < pairs) v[u] = src[p0 + 32 * u];
+#pragma unroll
+        for (int u = 0; u < U1; ++u)
+          if (p0 + 32 * u < pairs) dst[p0 + 32 * u] = v[u];
+      }
+    } else
     for (unsigned p0 = lane; p0 < pairs; p0 += 32 * U1) {  // a pair shares a sector
       double2 v[U1];
       bool need[U1];
@@ -263,40 +274,63 @@ int sym_prepare(bcss_plan& P) {
   if (P.sym_built) return BCSS_OK;
   const int m = P.m;
   const int64_t nb = P.nbar;
-  std::vector<int> rank, chunk;
-  std::vector<unsigned> runs;
-  P.sym_runs.assign((size_t)nb, {});
-  P.sym_ndiag.assign((size_t)nb, 0);
-  P.sym_fetch_elems = 0;
   const int64_t blk = ipow(P.bA, m);
+  std::vector<int32_t> keys;
   try {
-    const std::vector<int32_t> keys = bcss::hypertriangle_list(nb, m);
-    const int64_t n = (int64_t)keys.size() / m;
-    for (int64_t r = 0; r < n; ++r) {
-      const int32_t* k = &keys[(size_t)(r * m)];
-      unsigned run = 0;
-      for (int d = 1; d < m; ++d)
-        if (k[d] == k[d - 1]) run |= 1u << d;
-      auto& rs = P.sym_runs[(size_t)k[0]];
-      if (run) {
-        rank.push_back((int)r);
-        runs.push_back(run);
-        chunk.push_back(k[0]);
-        ++P.sym_ndiag[(size_t)k[0]];
-        P.sym_fetch_elems += fetched_elems(run, m, P.bA);
-      } else {
-        if (!rs.empty() && rs.back().second == r) rs.back().second = r + 1;
-        else rs.emplace_back(r, r + 1);
-        P.sym_fetch_elems += blk;
-      }
-    }
+    keys = bcss::hypertriangle_list(nb, m);
   } catch (const std::exception& e) {
     return fail(BCSS_ERR_PARAMETER, "%s", e.what());
   }
-  P.sym_n_diag = (int64_t)rank.size();
-  P.sym_h_rank.swap(rank);
-  P.sym_h_chunk.swap(chunk);
-  P.sym_h_run.swap(runs);
+  const int64_t n = (int64_t)keys.size() / m;
+  std::vector<unsigned> run_of((size_t)n, 0);
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> runs((size_t)nb);
+  int64_t n_runs = 0, distinct = 0;
+  for (int64_t r = 0; r < n; ++r) {
+    const int32_t* k = &keys[(size_t)(r * m)];
+    unsigned run = 0;
+    for (int d = 1; d < m; ++d)
+      if (k[d] == k[d - 1]) run |= 1u << d;
+    run_of[(size_t)r] = run;
+    if (!run) {
+      auto& rs = runs[(size_t)k[0]];
+      if (!rs.empty() && rs.back().second == r) rs.back().second = r + 1;
+      else { rs.emplace_back(r, r + 1); ++n_runs; }
+      ++distinct;
+    }
+  }
+  // distinct-key blocks go by DMA: while the previous call computes, zero-copy
+  // reads from the SMs get ~23 GB/s (51 alone) but the copy engines keep
+  // ~49 GB/s, even in the short runs of small blocks (config 4 streamed:
+  // 26.3 ms with DMA, 28.3 ms with every block on the zero-copy kernel).
+  // BCSS_SYM_DMA=0 puts them on the kernel (whole blocks, nothing to fill).
+  (void)n_runs;
+  (void)distinct;
+  P.sym_dma = true;
+  if (const char* e = getenv("BCSS_SYM_DMA")) P.sym_dma = atoi(e) != 0;
+  P.sym_runs.assign((size_t)nb, {});
+  if (P.sym_dma) P.sym_runs = runs;
+  P.sym_nzc.assign((size_t)nb, 0);
+  P.sym_nfill.assign((size_t)nb, 0);
+  P.sym_h_rank.clear(); P.sym_h_chunk.clear(); P.sym_h_run.clear();
+  P.sym_h_frank.clear(); P.sym_h_frun.clear();
+  P.sym_fetch_elems = 0;
+  for (int64_t r = 0; r < n; ++r) {  // packed order is chunk order
+    const int a = keys[(size_t)(r * m)];
+    const unsigned run = run_of[(size_t)r];
+    if (run || !P.sym_dma) {
+      P.sym_h_rank.push_back((int)r);
+      P.sym_h_chunk.push_back(a);
+      P.sym_h_run.push_back(run);
+      ++P.sym_nzc[(size_t)a];
+    }
+    if (run) {
+      P.sym_h_frank.push_back((int)r);
+      P.sym_h_frun.push_back(run);
+      ++P.sym_nfill[(size_t)a];
+    }
+    P.sym_fetch_elems += run ? fetched_elems(run, m, P.bA) : blk;
+  }
+  P.sym_n_zc = (int64_t)P.sym_h_rank.size();
   P.sym_built = true;
   return BCSS_OK;
 }
@@ -307,9 +341,9 @@ int sym_prepare(bcss_plan& P) {
 int sym_device(bcss_plan& P) {
   if (P.d_sym) return BCSS_OK;
   const int64_t nb = P.nbar;
-  const size_t nd = P.sym_h_rank.size();
+  const size_t nd = P.sym_h_rank.size(), nf = P.sym_h_frank.size();
   const size_t head = 128 + (size_t)nb * sizeof(unsigned);
-  const size_t bytes = head + nd * (2 * sizeof(int) + sizeof(unsigned));
+  const size_t bytes = head + nd * (2 * sizeof(int) + sizeof(unsigned)) + nf * (sizeof(int) + sizeof(unsigned));
   CUDA_TRY(cudaMalloc(&P.d_sym, bytes));
   char* base = static_cast<char*>(P.d_sym);
   P.d_sym_work = reinterpret_cast<unsigned long long*>(base);
@@ -318,7 +352,15 @@ int sym_device(bcss_plan& P) {
   int* d_rank = reinterpret_cast<int*>(base + head);
   int* d_chunk = d_rank + nd;
   unsigned* d_run = reinterpret_cast<unsigned*>(d_chunk + nd);
+  int* d_frank = reinterpret_cast<int*>(d_run + nd);
+  unsigned* d_frun = reinterpret_cast<unsigned*>(d_frank + nf);
   CUDA_TRY(cudaMemset(base, 0, head));
+  if (nf) {
+    CUDA_TRY(cudaMemcpy(d_frank, P.sym_h_frank.data(), nf * sizeof(int), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(d_frun, P.sym_h_frun.data(), nf * sizeof(unsigned), cudaMemcpyHostToDevice));
+  }
+  P.d_sym_frank = d_frank;
+  P.d_sym_frun = d_frun;
   if (nd) {
     CUDA_TRY(cudaMemcpy(d_rank, P.sym_h_rank.data(), nd * sizeof(int), cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(d_chunk, P.sym_h_chunk.data(), nd * sizeof(int), cudaMemcpyHostToDevice));
@@ -349,13 +391,13 @@ int sym_upload_ctas(bool async) {
 // Issue one symmetric upload of A (pinned host `A`, device `dA`, buffer set
 // `set`): the DMA half on copy_in (chunk events), the streaming kernel on
 // P->sym_stream, the per-chunk fills on P->fill_stream (fill events).
-int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool async, cudaStream_t copy_in,
-                     Pipe& pipe) {
+int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool async, bool green,
+                     cudaStream_t copy_in, cudaStream_t up_stream, Pipe& pipe) {
   const size_t blk = (size_t)ipow(P->bA, P->m);
   int st = sym_device(*P);
   if (st) return st;
   const double* srcd = nullptr;
-  if (P->sym_n_diag) CUDA_TRY(cudaHostGetDevicePointer((void**)&srcd, const_cast<double*>(A), 0));
+  if (P->sym_n_zc) CUDA_TRY(cudaHostGetDevicePointer((void**)&srcd, const_cast<double*>(A), 0));
   // one call's upload at a time on PCIe: this call's DMA starts when the
   // previous call's zero-copy half has landed (otherwise it takes the link
   // from that kernel and the previous call's last chunks arrive late)
@@ -368,10 +410,10 @@ int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool as
     CUDA_TRY(cudaEventRecord(P->chunk_ev[(size_t)a], copy_in));
   }
   pipe.fill_ev = nullptr;
-  if (P->sym_n_diag == 0) return BCSS_OK;
+  if (P->sym_n_zc == 0) return BCSS_OK;
   // keep the cumulative chunk counters inside 32 bits (rare reset)
   int64_t maxd = 0;
-  for (int64_t v : P->sym_ndiag) maxd = std::max(maxd, v);
+  for (int64_t v : P->sym_nzc) maxd = std::max(maxd, v);
   if ((uint64_t)maxd * (P->sym_uploads + 2) >= (1ull << 31)) {
     CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemset(P->d_sym_ctr, 0, (size_t)P->nbar * sizeof(unsigned)));
@@ -389,21 +431,23 @@ int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool as
   ua.base = P->sym_ticket_base;
   ua.set_free = P->d_sym_free + set;
   ua.set_target = P->sym_set_issued[set];  // computes on this set enqueued before this call
-  ua.n_diag = P->sym_n_diag;
+  ua.n_diag = P->sym_n_zc;
   ua.blk = (long long)blk;
   ua.lb = ilog2(P->bA);
   static const UploadFn ups[9] = {nullptr, nullptr, upload_m<2>, upload_m<3>, upload_m<4>,
                                   upload_m<5>, upload_m<6>, upload_m<7>, upload_m<8>};
   static const FillFn fills[9] = {nullptr, nullptr, fill_m<2>, fill_m<3>, fill_m<4>,
                                   fill_m<5>, fill_m<6>, fill_m<7>, fill_m<8>};
-  const int ctas = sym_upload_ctas(async);
+  // the upload kernel's SMs: its green partition, or SMs the compute grids leave
+  // free (then streamed calls issue one compute launch at a time)
+  const int ctas = green ? P->g_up_sms : sym_upload_ctas(async);
   pipe.reserve_sms = ctas;
-  pipe.serial = async;
-  ups[P->m](ua, ctas, P->sym_stream);
+  pipe.serial = async && !green;
+  ups[P->m](ua, ctas, up_stream);
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(P->sym_prev_done, P->sym_stream));
+  CUDA_TRY(cudaEventRecord(P->sym_prev_done, up_stream));
   // every warp takes tickets until one is past the list: n_diag + warps in all
-  P->sym_ticket_base += (uint64_t)P->sym_n_diag + (uint64_t)ctas * 16;
+  P->sym_ticket_base += (uint64_t)P->sym_n_zc + (uint64_t)ctas * 16;
   // fills, chunk by chunk, as the chunk's repeated-key blocks land
   while (P->fill_ev.size() < (size_t)P->nbar) {
     cudaEvent_t ev;
@@ -414,16 +458,18 @@ int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool as
   int64_t first = 0;
   const unsigned per_blk_ctas = (unsigned)std::max<int64_t>(1, std::min<int64_t>(16, (int64_t)blk / (256 * 8 * 4)));
   for (int64_t a = 0; a < P->nbar; ++a) {
-    const int64_t nd = P->sym_ndiag[(size_t)a];
-    if (nd) {
-      const unsigned target = (unsigned)((u + 1) * (uint64_t)nd);
+    const int64_t nz = P->sym_nzc[(size_t)a], nf = P->sym_nfill[(size_t)a];
+    if (nz) {  // the chunk's zero-copy blocks landed
+      const unsigned target = (unsigned)((u + 1) * (uint64_t)nz);
       const CUresult r = wait(reinterpret_cast<CUstream>(P->fill_stream),
                               reinterpret_cast<CUdeviceptr>(P->d_sym_ctr + a), target, CU_STREAM_WAIT_VALUE_GEQ);
       if (r != CUDA_SUCCESS) return fail(BCSS_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", (int)r);
-      fills[P->m](dA, P->d_sym_rank + first, P->d_sym_run + first, (long long)blk, ilog2(P->bA),
-                  dim3(per_blk_ctas, (unsigned)nd), P->fill_stream);
+    }
+    if (nf) {  // fill its repeated-key blocks
+      fills[P->m](dA, P->d_sym_frank + first, P->d_sym_frun + first, (long long)blk, ilog2(P->bA),
+                  dim3(per_blk_ctas, (unsigned)nf), P->fill_stream);
       CUDA_TRY(cudaGetLastError());
-      first += nd;
+      first += nf;
     }
     CUDA_TRY(cudaEventRecord(P->fill_ev[(size_t)a], P->fill_stream));
     if (a % 4 == 3) trace_mark(&pipe, "A chunk " + std::to_string(a) + " filled", P->fill_stream);
@@ -444,6 +490,99 @@ int sym_release_set(bcss_plan* P, int set, cudaStream_t s) {
                                       ++P->sym_set_released[set], 0);
   if (r != CUDA_SUCCESS) return fail(BCSS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
   return BCSS_OK;
+}
+
+// ---- SM partition (green contexts) ---------------------------------------------
+// A streamed call's upload kernel must stay resident while the previous call
+// computes.  Green contexts split the SMs: the upload kernel's stream lives in
+// a small partition, every compute stream of a symmetric-upload run in the
+// complementary one, so concurrent launches and the cascade can no longer take
+// the upload's SMs (measured: tools/green_probe.cu, disjoint SM sets, runtime
+// launches into green-context streams on primary-context memory).  Driver
+// entry points are looked up at run time.  Opt-in (BCSS_SYM_GREEN=1); by
+// default streamed symmetric runs issue one compute launch at a time instead.
+namespace {
+using GetResFn = CUresult (*)(CUdevice, CUdevResource*, CUdevResourceType);
+using SplitFn = CUresult (*)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+using DescFn = CUresult (*)(CUdevResourceDesc*, CUdevResource*, unsigned);
+using GreenCreateFn = CUresult (*)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+using GreenStreamFn = CUresult (*)(CUstream*, CUgreenCtx, unsigned, int);
+using GreenDestroyFn = CUresult (*)(CUgreenCtx);
+using DeviceGetFn = CUresult (*)(CUdevice*, int);
+}  // namespace
+
+int sym_green(bcss_plan* P) {
+  if (P->green_state != 0) return P->green_state > 0 ? BCSS_OK : BCSS_ERR_STATE;
+  P->green_state = -1;
+  // opt-in: on config 5 the partition measured slightly slower than leaving the
+  // upload's SMs free by grid size (streamed 500 vs 490 ms, one call 651 vs 639
+  // ms), on config 4 slightly faster (26.3 vs 27.1 ms streamed)
+  const char* e = getenv("BCSS_SYM_GREEN");
+  if (!e || !atoi(e)) return BCSS_ERR_STATE;
+  auto dget = driver_fn<DeviceGetFn>("cuDeviceGet");
+  auto getres = driver_fn<GetResFn>("cuDeviceGetDevResource");
+  auto split = driver_fn<SplitFn>("cuDevSmResourceSplitByCount");
+  auto gdesc = driver_fn<DescFn>("cuDevResourceGenerateDesc");
+  auto gcreate = driver_fn<GreenCreateFn>("cuGreenCtxCreate");
+  auto gstream = driver_fn<GreenStreamFn>("cuGreenCtxStreamCreate");
+  if (!dget || !getres || !split || !gdesc || !gcreate || !gstream) return BCSS_ERR_STATE;
+  int ord = 0;
+  if (cudaGetDevice(&ord) != cudaSuccess) return BCSS_ERR_STATE;
+  CUdevice dev;
+  CUdevResource all, grp[1], rem;
+  unsigned nb = 1;
+  CUdevResourceDesc d_up, d_comp;
+  if (dget(&dev, ord) || getres(dev, &all, CU_DEV_RESOURCE_TYPE_SM) ||
+      split(grp, &nb, &all, &rem, 0, (unsigned)sym_upload_ctas(true)) || nb != 1 || rem.sm.smCount == 0 ||
+      gdesc(&d_up, grp, 1) || gdesc(&d_comp, &rem, 1)) {
+    cudaGetLastError();
+    return BCSS_ERR_STATE;
+  }
+  CUgreenCtx g_up = nullptr, g_comp = nullptr;
+  if (gcreate(&g_up, d_up, dev, CU_GREEN_CTX_DEFAULT_STREAM) ||
+      gcreate(&g_comp, d_comp, dev, CU_GREEN_CTX_DEFAULT_STREAM)) {
+    auto gdestroy = driver_fn<GreenDestroyFn>("cuGreenCtxDestroy");
+    if (gdestroy && g_up) gdestroy(g_up);
+    cudaGetLastError();
+    return BCSS_ERR_STATE;
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  CUstream up = nullptr, host = nullptr;
+  if (gstream(&up, g_up, CU_STREAM_NON_BLOCKING, hi) || gstream(&host, g_comp, CU_STREAM_NON_BLOCKING, 0)) {
+    cudaGetLastError();
+    return BCSS_ERR_STATE;
+  }
+  P->g_up = g_up;
+  P->g_comp = g_comp;
+  P->g_sym_stream = reinterpret_cast<cudaStream_t>(up);
+  P->g_host_stream = reinterpret_cast<cudaStream_t>(host);
+  P->g_up_sms = (int)grp[0].sm.smCount;
+  P->green_state = 1;
+  return BCSS_OK;
+}
+
+// a stream in the compute partition (green runs' side and level streams)
+int green_compute_stream(bcss_plan* P, int priority, cudaStream_t* out) {
+  auto gstream = driver_fn<GreenStreamFn>("cuGreenCtxStreamCreate");
+  CUstream s = nullptr;
+  if (!gstream || !P->g_comp || gstream(&s, static_cast<CUgreenCtx>(P->g_comp), CU_STREAM_NON_BLOCKING, priority))
+    return fail(BCSS_ERR_CUDA, "cuGreenCtxStreamCreate failed");
+  *out = reinterpret_cast<cudaStream_t>(s);
+  return BCSS_OK;
+}
+
+void green_destroy(bcss_plan* P) {
+  auto gdestroy = driver_fn<GreenDestroyFn>("cuGreenCtxDestroy");
+  for (cudaStream_t q : P->g_side) cudaStreamDestroy(q);
+  for (cudaStream_t q : P->g_lvl_stream) cudaStreamDestroy(q);
+  if (P->g_sym_stream) cudaStreamDestroy(P->g_sym_stream);
+  if (P->g_host_stream) cudaStreamDestroy(P->g_host_stream);
+  if (gdestroy) {
+    if (P->g_up) gdestroy(static_cast<CUgreenCtx>(P->g_up));
+    if (P->g_comp) gdestroy(static_cast<CUgreenCtx>(P->g_comp));
+  }
+  cudaGetLastError();
 }
 
 // stream s waits until A chunks 0..a are resident (DMA events + fill events)
