@@ -132,3 +132,36 @@ def test_symmetric_upload_falls_back_where_it_does_not_apply():
     assert orc.rel_frobenius(c2, orc.sttsm_bcss_packed(a2, x2, 3, 64, 16, 16)) <= 1e-12
     plan.close()
     plan2.close()
+
+
+@pytest.mark.parametrize("env", [{"BCSS_SYM_GREEN": "1"}, {"BCSS_SYM_DMA": "0"}], ids=["green", "zc_all"])
+def test_symmetric_upload_optional_modes(env, monkeypatch):
+    # the SM partition (green contexts: upload kernel and compute on disjoint
+    # SMs, streamed calls keep concurrent launches) and the all-zero-copy list:
+    # same C bit for bit as the full upload, streamed and synchronous
+    import torch
+
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    m, n, p, ba, bc = 4, 64, 48, 16, 8
+    full = bs.SttsmPlan(m, n, p, ba, bc, pipeline=2)
+    sym = bs.SttsmPlan(m, n, p, ba, bc, pipeline=2, symmetric_upload=True)
+    ins = []
+    for i in range(3):
+        a = _exact_symmetric(m, n, ba, 300 + i)
+        x = np.random.default_rng(400 + i).standard_normal((p, n))
+        ins.append((_pinned(a), _pinned(x), _host_run(full, a, x)))
+    outs = [torch.full((sym.c_elems,), float("nan"), dtype=torch.float64).pin_memory() for _ in ins]
+    for rep in range(2):
+        for (ta, tx, _), tc in zip(ins, outs):
+            sym.run_host_async(ta.numpy(), tx.numpy(), tc.numpy())
+        sym.wait()
+        for (_, _, want), tc in zip(ins, outs):
+            assert np.array_equal(tc.numpy(), want)
+    ta, tx, want = ins[0]
+    c = torch.full((sym.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    sym.run_host(ta.numpy(), tx.numpy(), c.numpy())
+    assert np.array_equal(c.numpy(), want)
+    assert sym.last_upload_bytes < 8 * sym.a_elems
+    full.close()
+    sym.close()
