@@ -372,7 +372,7 @@ def _check_args(a, x) -> tuple[int, int, int]:
 
 
 def sttsm_bcss(a, x, b_c: int, counter: OpCounter | None = None, reuse: bool = True,
-               temp_hook: TempHook | None = None):
+               temp_hook: TempHook | None = None, *, symmetric_upload: bool = False):
     """Blocked change of basis over compact symmetric storage, on the GPU.
 
     Same contract as the reference ``sttsm_bcss``: returns a fresh BCSS
@@ -382,6 +382,12 @@ def sttsm_bcss(a, x, b_c: int, counter: OpCounter | None = None, reuse: bool = T
     ``BcssTensor`` - an object of that same class, so reference code
     (``decompress``, ``save_bcss``, ``cli.compare_bcss_dense``) consumes it
     unchanged.
+
+    ``symmetric_upload=True`` (an extension, keyword-only) moves only the
+    orbit representatives of A's repeated-key blocks to the GPU (SttsmPlan's
+    option of the same name): the result is bit-identical when those blocks
+    are exactly symmetric, e.g. made by ``compress(t, b)`` with ``tol=0`` and
+    not edited since; otherwise every orbit takes its representative's value.
     """
     x = np.asarray(x, dtype=np.float64)
     m, n, p = _check_args(a, x)
@@ -406,7 +412,7 @@ def sttsm_bcss(a, x, b_c: int, counter: OpCounter | None = None, reuse: bool = T
             plan.close()
     else:
         with _PLAN_CACHE_LOCK:
-            plan = _cached_plan(m, n, p, b_a, b_c, reuse)
+            plan = _cached_plan(m, n, p, b_a, b_c, reuse, symmetric_upload)
             plan.run_host(a_payload, xc, c_payload)
     if counter is not None:
         counter.count_flops(bcss_flops(m, n, p, b_a, b_c, reuse))
@@ -441,16 +447,16 @@ _PLAN_CACHE_SIZE = 4
 _PLAN_CACHE_LOCK = threading.Lock()
 
 
-def _cached_plan(m, n, p, b_a, b_c, reuse) -> SttsmPlan:
+def _cached_plan(m, n, p, b_a, b_c, reuse, symmetric_upload: bool = False) -> SttsmPlan:
     global _PLAN_CACHE
     if _PLAN_CACHE is None:
         _PLAN_CACHE = OrderedDict()
-    key = (m, n, p, b_a, b_c, bool(reuse))
+    key = (m, n, p, b_a, b_c, bool(reuse), bool(symmetric_upload))
     plan = _PLAN_CACHE.pop(key, None)
     if plan is None:
         # pipelined: the host run stages the caller's (pageable) arrays through
         # pinned memory with all host cores and overlaps upload, compute, download
-        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, pipeline=4)
+        plan = SttsmPlan(m, n, p, b_a, b_c, reuse=reuse, pipeline=4, symmetric_upload=symmetric_upload)
     _PLAN_CACHE[key] = plan
     while len(_PLAN_CACHE) > _PLAN_CACHE_SIZE:
         _, old = _PLAN_CACHE.popitem(last=False)

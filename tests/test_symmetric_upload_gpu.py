@@ -165,3 +165,24 @@ def test_symmetric_upload_optional_modes(env, monkeypatch):
     assert sym.last_upload_bytes < 8 * sym.a_elems
     full.close()
     sym.close()
+
+
+def test_dropin_symmetric_upload_on_compressed_tensor():
+    # the reference idiom decompress(sttsm_bcss(compress(a, b), x, b_c)) with the
+    # opt-in: compress(tol=0) guarantees exact symmetry, so C is bit-identical
+    rng = np.random.default_rng(77)
+    n, b, p, bc = 32, 8, 24, 8
+    t = rng.uniform(-1, 1, (n, n, n))
+    import itertools
+
+    t = sum(np.transpose(t, perm) for perm in itertools.permutations(range(3))) / 6.0
+    # exact symmetry: copy the canonical value into every permutation
+    for i, j, k in itertools.product(range(n), repeat=3):
+        s = tuple(sorted((i, j, k)))
+        t[i, j, k] = t[s]
+    a = bs.compress(t, b)
+    x = rng.standard_normal((p, n))
+    c_full = bs.sttsm_bcss(a, x, bc)
+    c_sym = bs.sttsm_bcss(a, x, bc, symmetric_upload=True)
+    assert np.array_equal(c_sym.payload, c_full.payload)
+    assert np.array_equal(bs.decompress(c_sym).array, bs.decompress(c_full).array)
