@@ -15,6 +15,7 @@ import torch
 sys.path.insert(0, ".")
 import paper_1301_7744_b200 as bs
 from oracle import bcss_oracle as orc
+from paper_1301_7744_b200.dense import symmetrize_bcss_device
 
 cases = int(sys.argv[1]) if len(sys.argv) > 1 else 60
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
@@ -48,6 +49,26 @@ while done < cases:
     cp = np.full(plan.c_elems, np.nan)
     plan.run_host(a, x, cp)
     modes["pageable"] = cp
+    plan.close()
+    # symmetric upload: on the (rounding-symmetric) input within 1e-12, and on
+    # an exactly symmetrized copy bit for bit equal to the full upload
+    plan = bs.SttsmPlan(m, n, p, ba, bc, pipeline=waves, symmetric_upload=True)
+    ch = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    plan.run_host(torch.from_numpy(a).pin_memory().numpy(), torch.from_numpy(x).pin_memory().numpy(), ch.numpy())
+    modes["symmetric"] = ch.numpy().copy()
+    a_ex = torch.from_numpy(a).cuda()
+    symmetrize_bcss_device(a_ex, m, n, ba)
+    a_ex = a_ex.cpu().pin_memory()
+    ch.fill_(float("nan"))
+    plan.run_host_async(a_ex.numpy(), torch.from_numpy(x).pin_memory().numpy(), ch.numpy())
+    plan.wait()
+    full_p = bs.SttsmPlan(m, n, p, ba, bc, pipeline=waves)
+    cf = torch.full((full_p.c_elems,), float("nan"), dtype=torch.float64).pin_memory()
+    full_p.run_host(a_ex.numpy(), torch.from_numpy(x).pin_memory().numpy(), cf.numpy())
+    if not np.array_equal(ch.numpy(), cf.numpy()):
+        bad += 1
+        print(f"MISMATCH symmetric-vs-full bitwise m={m} n={n} p={p} ba={ba} bc={bc}", flush=True)
+    full_p.close()
     plan.close()
     plan = bs.SttsmPlan(m, n, p, ba, bc, reuse=False)
     c = torch.empty(plan.c_elems, dtype=torch.float64, device="cuda")
