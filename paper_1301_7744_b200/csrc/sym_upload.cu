@@ -103,8 +103,12 @@ struct UploadArgs {
 
 // Streaming half: one warp per repeated-key block, only the representatives'
 // sectors, U1 16-byte zero-copy loads in flight per lane.
+#ifndef BCSS_SYM_THREADS
+#define BCSS_SYM_THREADS 512
+#endif
+constexpr int kSymThreads = BCSS_SYM_THREADS;
 template <int M>
-__global__ void __launch_bounds__(512, 1) sym_upload_kernel(const UploadArgs a) {
+__global__ void __launch_bounds__(kSymThreads, 1) sym_upload_kernel(const UploadArgs a) {
 #ifndef BCSS_SYM_U1
 #define BCSS_SYM_U1 12
 #endif
@@ -202,7 +206,7 @@ __global__ void __launch_bounds__(256) sym_fill_kernel(double* __restrict__ dst,
 using UploadFn = void (*)(const UploadArgs&, int, cudaStream_t);
 template <int M>
 void upload_m(const UploadArgs& a, int ctas, cudaStream_t s) {
-  sym_upload_kernel<M><<<ctas, 512, 0, s>>>(a);
+  sym_upload_kernel<M><<<ctas, kSymThreads, 0, s>>>(a);
 }
 using FillFn = void (*)(double*, const int*, const unsigned*, long long, int, dim3, cudaStream_t);
 template <int M>
@@ -447,7 +451,7 @@ int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool as
   CUDA_TRY(cudaGetLastError());
   CUDA_TRY(cudaEventRecord(P->sym_prev_done, up_stream));
   // every warp takes tickets until one is past the list: n_diag + warps in all
-  P->sym_ticket_base += (uint64_t)P->sym_n_zc + (uint64_t)ctas * 16;
+  P->sym_ticket_base += (uint64_t)P->sym_n_zc + (uint64_t)ctas * (kSymThreads / 32);
   // fills, chunk by chunk, as the chunk's repeated-key blocks land
   while (P->fill_ev.size() < (size_t)P->nbar) {
     cudaEvent_t ev;
