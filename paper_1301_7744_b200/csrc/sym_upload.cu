@@ -488,11 +488,14 @@ int sym_upload_issue(bcss_plan* P, const double* A, double* dA, int set, bool as
 // for a call that never comes).
 int sym_release_set(bcss_plan* P, int set, cudaStream_t s) {
   if (!P->d_sym_free) return BCSS_OK;
-  ++P->sym_set_issued[set];
+  // the counts advance only with the write that makes them true, so a failed
+  // write leaves the next upload's target at what the flag will hold
   const CUresult r = write_value_fn()(reinterpret_cast<CUstream>(s),
                                       reinterpret_cast<CUdeviceptr>(P->d_sym_free + set),
-                                      ++P->sym_set_released[set], 0);
+                                      (cuuint32_t)(P->sym_set_released[set] + 1), 0);
   if (r != CUDA_SUCCESS) return fail(BCSS_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", (int)r);
+  ++P->sym_set_released[set];
+  ++P->sym_set_issued[set];
   return BCSS_OK;
 }
 
@@ -542,21 +545,24 @@ int sym_green(bcss_plan* P) {
     cudaGetLastError();
     return BCSS_ERR_STATE;
   }
+  auto gdestroy = driver_fn<GreenDestroyFn>("cuGreenCtxDestroy");
   CUgreenCtx g_up = nullptr, g_comp = nullptr;
-  if (gcreate(&g_up, d_up, dev, CU_GREEN_CTX_DEFAULT_STREAM) ||
-      gcreate(&g_comp, d_comp, dev, CU_GREEN_CTX_DEFAULT_STREAM)) {
-    auto gdestroy = driver_fn<GreenDestroyFn>("cuGreenCtxDestroy");
+  CUstream up = nullptr, host = nullptr;
+  auto undo = [&]() {  // a partial setup leaves nothing behind
+    if (up) cudaStreamDestroy(reinterpret_cast<cudaStream_t>(up));
+    if (host) cudaStreamDestroy(reinterpret_cast<cudaStream_t>(host));
     if (gdestroy && g_up) gdestroy(g_up);
+    if (gdestroy && g_comp) gdestroy(g_comp);
     cudaGetLastError();
     return BCSS_ERR_STATE;
-  }
+  };
+  if (gcreate(&g_up, d_up, dev, CU_GREEN_CTX_DEFAULT_STREAM) ||
+      gcreate(&g_comp, d_comp, dev, CU_GREEN_CTX_DEFAULT_STREAM))
+    return undo();
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);
-  CUstream up = nullptr, host = nullptr;
-  if (gstream(&up, g_up, CU_STREAM_NON_BLOCKING, hi) || gstream(&host, g_comp, CU_STREAM_NON_BLOCKING, 0)) {
-    cudaGetLastError();
-    return BCSS_ERR_STATE;
-  }
+  if (gstream(&up, g_up, CU_STREAM_NON_BLOCKING, hi) || gstream(&host, g_comp, CU_STREAM_NON_BLOCKING, 0))
+    return undo();
   P->g_up = g_up;
   P->g_comp = g_comp;
   P->g_sym_stream = reinterpret_cast<cudaStream_t>(up);
