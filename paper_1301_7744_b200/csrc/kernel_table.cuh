@@ -65,6 +65,21 @@ constexpr int N_POLICY_SHAPES = 10;
 constexpr int N_GEN = 4;
 constexpr int BCSS_GEN_OF[N_GEN] = {3, 4, 2, 8};
 
+// Non-power-of-two b_a (multiples of 4): the same kernel with POW2 = false,
+// instantiated per row group RG (the largest of 28, 24, 20, 12, 4 dividing
+// b_a; BK a multiple of RG) on three tile shapes, 16 consumer warps each; every
+// policy shape index maps to one of them (BCSS_NP_SHAPES).
+#define BCSS_NP_BIG(RG, BK) WsLevelKernel<128, 128, BK, 4, 4, 3, RG, 4, false, false>
+#define BCSS_NP_MID(RG, BK) WsLevelKernel<64, 256, BK, 2, 8, 3, RG, 4, false, false>
+#define BCSS_NP_SMALL(RG, BK) WsLevelKernel<32, 256, BK, 1, 16, 3, RG, 4, false, false>
+constexpr int N_NP = 5;
+constexpr int kNpRg[N_NP] = {4, 12, 20, 24, 28};
+extern const KernelCfg kNP4[N_SHAPES];
+extern const KernelCfg kNP12[N_SHAPES];
+extern const KernelCfg kNP20[N_SHAPES];
+extern const KernelCfg kNP24[N_SHAPES];
+extern const KernelCfg kNP28[N_SHAPES];
+
 // b_a variants of the fast kernels (one translation unit each): 4, 8, 16, 32, 64
 constexpr int N_BA = 5;
 extern const KernelCfg kFast4[N_SHAPES];

@@ -27,6 +27,11 @@ const KernelCfg& kernel_cfg(int cfg) {
   if (cfg == CFG_GENERIC_PERM) return bcss::kGenericPerm;
   const KernelCfg* const fast[bcss::N_BA] = {bcss::kFast4, bcss::kFast8, bcss::kFast16, bcss::kFast32, bcss::kFast64};
   const KernelCfg* const gen[bcss::N_BA] = {bcss::kGen4, bcss::kGen8, bcss::kGen16, bcss::kGen32, bcss::kGen64};
+  const int np0 = 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN;  // non-power-of-two b_a
+  if (cfg >= np0 && cfg < np0 + bcss::N_NP * N_SHAPES) {
+    const KernelCfg* const np[bcss::N_NP] = {bcss::kNP4, bcss::kNP12, bcss::kNP20, bcss::kNP24, bcss::kNP28};
+    return np[(cfg - np0) % bcss::N_NP][(cfg - np0) / bcss::N_NP];
+  }
   const int ba = (cfg - 1) % bcss::N_BA;
   if (cfg > bcss::N_BA * N_SHAPES)  // general-redirection variants
     return gen[ba][(cfg - 1 - bcss::N_BA * N_SHAPES) / bcss::N_BA];
@@ -34,6 +39,7 @@ const KernelCfg& kernel_cfg(int cfg) {
 }
 // general-redirection configuration mirroring fast shape `shape` (one of BCSS_GEN_OF), else -1
 int gen_cfg(int64_t bA, int shape) {
+  if (!is_pow2(bA)) return -1;  // general redirection: power-of-two b_a only
   const int f = fast_cfg(bA, 0);
   if (f < 0) return -1;
   for (int g = 0; g < N_GEN; ++g)
@@ -49,7 +55,13 @@ int fast_cfg(int64_t bA, int shape) {
     case 16: i = 2; break;
     case 32: i = 3; break;
     case 64: i = 4; break;
-    default: return -1;
+    default: {
+      // non-power-of-two multiple of 4: the largest row group dividing it
+      if (bA < 12 || bA % 4 != 0 || is_pow2(bA)) return -1;
+      for (int j = bcss::N_NP - 1; j >= 0; --j)
+        if (bA % bcss::kNpRg[j] == 0) return 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + shape * bcss::N_NP + j;
+      return -1;
+    }
   }
   return 1 + shape * bcss::N_BA + i;
 }
@@ -308,7 +320,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       std::vector<std::pair<int, int>> pieces;
       const bool fast = fast_shape && (P.reuse || k < P.m - 1);
       // reuse=False top level: unsorted keys, general redirection permutations
-      const bool gen = fast_shape && !fast && !getenv("BCSS_NO_GEN_TOP");
+      const bool gen = fast_shape && !fast && is_pow2(P.bA) && !getenv("BCSS_NO_GEN_TOP");
       unsigned gen_mask = 0;
       for (int g = 0; g < bcss::N_GEN; ++g) gen_mask |= 1u << bcss::BCSS_GEN_OF[g];
       if (fast && level_shape >= 0) pieces = {{level_shape, whole.z}};
@@ -382,7 +394,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
     // the level ends half a tile earlier.  Not for chunk-gated / grouped levels
     // (their item ranges follow keys) - and only when every tile is full.
     if (level_shape >= 0 && !grouped && L.launches.size() == 1 && (k < P.m - 1 || P.pipeline_waves <= 1) &&
-        P.bC % 32 == 0 && L.rest % 256 == 0 && !getenv("BCSS_NO_TAIL_TRIM")) {
+        P.bC % 32 == 0 && L.rest % 256 == 0 && is_pow2(P.bA) && !getenv("BCSS_NO_TAIL_TRIM")) {
       static const int sms = [] {
         int dev = 0, v = 0;
         if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {

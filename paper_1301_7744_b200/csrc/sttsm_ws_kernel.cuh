@@ -63,7 +63,13 @@ __device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.a
 // they shrink to PROD_REGS registers and the consumers grow into the rest.
 // GEN = true: general redirection permutations (reuse=False top level, whose
 // unsorted keys map to A's canonical blocks by arbitrary mode permutations).
-template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, int BA, int NPROD = 4, bool GEN = false>
+// POW2 = false: b_a is not a power of two (a multiple of 4); BA is then the
+// row group RG (a multiple of 4 dividing b_a and BK) and b_a comes from the
+// launch arguments: stored-block offsets use b_a^p multiplications and
+// divisions instead of shifts, every row group is staged [e][col], and the
+// epilogue splits columns by division.
+template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, int BA, int NPROD = 4, bool GEN = false,
+          bool POW2 = true>
 struct WsLevelKernel {
   static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int NCW = WM * WN;               // consumer warps
@@ -79,7 +85,7 @@ struct WsLevelKernel {
   static constexpr int WTM = BM / WM, WTN = BN / WN;
   static constexpr int FM = WTM / 8, FN = WTN / 8;
   static constexpr int LBA = (BA == 2) ? 1 : (BA == 4) ? 2 : (BA == 8) ? 3 : (BA == 16) ? 4 : (BA == 32) ? 5 : 6;
-  static constexpr int RG = BA < BK ? BA : BK;  // rows per group (one ib)
+  static constexpr int RG = !POW2 ? BA : BA < BK ? BA : BK;  // rows per group (one ib)
   static constexpr int G = BK / RG;             // groups per stage
   static constexpr int LDA = BK + 4;
   static constexpr int LDR = BN + 4;            // row-major group stride ([e][col])
@@ -108,7 +114,8 @@ struct WsLevelKernel {
   static_assert(BM <= PT, "one producer thread per output row");
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
   static_assert((BM * BK / 2) % PT == 0 && (BK * BN / 2) % PT == 0 && GP % 32 == 0, "loader balance");
-  static_assert((1 << LBA) == BA && RG % 4 == 0, "BA must be a power of two in 4..64");
+  static_assert(POW2 ? ((1 << LBA) == BA && RG % 4 == 0) : (RG % 4 == 0 && BK % RG == 0 && !GEN),
+                "BA must be a power of two in 4..64 (or, !POW2, a row group dividing BK)");
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
 
   static __device__ __forceinline__ int swz(int col) { return ((col >> SW_SHIFT) & SW_MASK) << 2; }
@@ -134,7 +141,7 @@ struct WsLevelKernel {
   static constexpr int CPR = BN / 2;         // column pairs per row (column-contiguous blocks)
   static constexpr int ESTEP = PT >= CPR ? PT / CPR : 1;   // row stride of a thread
   static constexpr int NCOL = PT >= CPR ? 1 : CPR / PT;    // column pairs per thread
-  static_assert(PT % HP == 0 && BN % CSTEP == 0 && CSTEP % 4 == 0, "e-contiguous loader");
+  static_assert(!POW2 || (PT % HP == 0 && BN % CSTEP == 0 && CSTEP % 4 == 0), "e-contiguous loader");
   static_assert((PT >= CPR ? PT % CPR == 0 && RG % ESTEP == 0 : CPR % PT == 0), "column loader");
 
   static __device__ __forceinline__ void cp16(unsigned sdst, const double* src) {
@@ -153,7 +160,7 @@ struct WsLevelKernel {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int i0 = kstep * BK + g * RG;
-      nb[g] = __ldg(nrow + (i0 < a.n ? (i0 >> LBA) : 0));
+      nb[g] = __ldg(nrow + (i0 < a.n ? (POW2 ? (i0 >> LBA) : i0 / a.bA) : 0));
     }
   }
 
@@ -218,6 +225,50 @@ struct WsLevelKernel {
     }
   }
 
+  // !POW2: one row group staged [e][col].  Contracted digit at stored
+  // position 0 (e-contiguous in HBM, every level-0 block): element (e, col)
+  // at e + b_a * col' (col' = col, or digit-reversed on mirrored level 0),
+  // copied 8 bytes at a time; position p > 0: column pairs are contiguous
+  // (b_a^p is even), element (e, col) at lo + hi * b_a^(p+1) + e * b_a^p with
+  // lo = col mod b_a^p, hi = col div b_a^p.
+  static __device__ __forceinline__ void produce_group_np(const LevelArgs& a, const double* base, int e0, int pos,
+                                                        bool grp_ok, bool full_n, int n0, unsigned dst, int ptid) {
+    const int et = PT >= CPR ? ptid / CPR : 0;
+#pragma unroll
+    for (int j = 0; j < NCOL; ++j) {
+      const int c2 = 2 * ((PT >= CPR ? ptid % CPR : ptid) + j * PT);
+      const int cg = n0 + c2;
+      const bool ok = grp_ok && (full_n || cg < a.rest);
+      const bool ok1 = grp_ok && (full_n || cg + 1 < a.rest);
+      const unsigned d = dst + (unsigned)(et * LDR + c2) * 8u;
+      if (pos == 0) {
+        long long c0 = cg, c1 = cg + 1;
+        if (a.mirror_digits) {
+          c0 = digit_rev(cg, a.mirror_digits, a.lbc);
+          c1 = digit_rev(cg + 1, a.mirror_digits, a.lbc);
+        }
+        const double* s0 = base + e0 + et + (long long)a.bA * c0;
+        const double* s1 = base + e0 + et + (long long)a.bA * c1;
+#pragma unroll 4
+        for (int i = 0; i < RG / ESTEP; ++i) {
+          const unsigned di = d + (unsigned)(i * ESTEP * LDR) * 8u;
+          cp8z(di, ok ? s0 + i * ESTEP : a.X, ok);
+          cp8z(di + 8u, ok1 ? s1 + i * ESTEP : a.X, ok1);
+        }
+      } else {
+        const long long bp = a.pw[pos];
+        const long long hi = cg / bp, lo = cg - hi * bp;
+        const double* src = base + lo + hi * bp * a.bA + (long long)(e0 + et) * bp;
+        const long long sstep = (long long)ESTEP * bp;
+#pragma unroll 4
+        for (int i = 0; i < RG / ESTEP; ++i) {
+          const unsigned di = d + (unsigned)(i * ESTEP * LDR) * 8u;
+          cp16z(di, ok ? src + i * sstep : a.X, ok);
+        }
+      }
+    }
+  }
+
   static __device__ __forceinline__ void produce(const LevelArgs& a, const TileInfo& t, int kstep,
                                                  const int2 (&nb)[G], unsigned As_s, unsigned Bs_s, int* modes,
                                                  const int* srev, int ptid, uint64_t* fullbar) {
@@ -240,10 +291,15 @@ struct WsLevelKernel {
       const bool grp_ok = i0 < a.n;
       const int pos = code_p(nb[g].y);
       const double* base = tin_call + (long long)nb[g].x * a.blk_in;
-      const int e0 = i0 & (BA - 1);
+      const int e0 = POW2 ? (i0 & (BA - 1)) : i0 % a.bA;
       const unsigned dst = Bs_s + (unsigned)(g * GR_SIZE) * 8u;
       if constexpr (GEN) {
         produce_group_gen(a, nb[g].y, base, e0, grp_ok, full_n, n0, dst, modes + g, ptid);
+        continue;
+      }
+      if constexpr (!POW2) {
+        if (ptid == 0) modes[g] = 0;
+        produce_group_np(a, base, e0, pos, grp_ok, full_n, n0, dst, ptid);
         continue;
       }
       if (ptid == 0) modes[g] = pos == 0;
@@ -365,7 +421,9 @@ struct WsLevelKernel {
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      if constexpr (RG >= 16) {  // the mode is CTA-uniform per group: branch to a specialized body
+      if constexpr (!POW2) {  // every group is staged [e][col]
+        consume_group<NF, 0>(ap, Bs + g * GR_SIZE, colw, sw, g, false, acc);
+      } else if constexpr (RG >= 16) {  // the mode is CTA-uniform per group: branch to a specialized body
         if (md[g]) consume_group<NF, 1>(ap, Bs + g * GR_SIZE, colw, sw, g, true, acc);
         else consume_group<NF, 0>(ap, Bs + g * GR_SIZE, colw, sw, g, false, acc);
       } else {  // short groups (b_a <= 8): selects are cheaper than the branches (measured)
@@ -408,6 +466,30 @@ struct WsLevelKernel {
     if (a.k >= 0) return;
 #endif
     const long long tstride = (long long)a.bAk * a.bC;
+    if constexpr (!POW2) {
+#pragma unroll
+      for (int fm = 0; fm < FM; ++fm) {
+        if (roff[fm] == kNoRow) continue;
+        double* base = a.Tout + roff[fm];
+#pragma unroll
+        for (int fn = 0; fn < FN; ++fn) {
+          const int col = nt * BN + (cw % WN) * WTN + fn * 8 + 2 * (lane & 3);
+          if (col >= a.rest) continue;
+          if (a.bAk >= 2) {  // b_a^k even: col, col + 1 in one run
+            const long long q = col / a.bAk;
+            *reinterpret_cast<double2*>(base + (col - q * a.bAk) + tstride * q) =
+                make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+          } else if (a.mirror_digits) {
+            if (col + 1 < a.rest) *reinterpret_cast<double2*>(base + col) = make_double2(acc[fm][fn][0], acc[fm][fn][1]);
+            else base[col] = acc[fm][fn][0];
+          } else {
+            base[tstride * col] = acc[fm][fn][0];
+            if (col + 1 < a.rest) base[tstride * (col + 1)] = acc[fm][fn][1];
+          }
+        }
+      }
+      return;
+    }
 #ifndef BCSS_EPI_GENERAL
     // (only where the consumers have register headroom beyond the
     // accumulators and ptxas does not spill for it: not in the 104-register

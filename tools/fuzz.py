@@ -23,9 +23,9 @@ bad = 0
 done = 0
 while done < cases:
     m = int(rng.integers(2, 7))
-    ba = int(rng.choice([1, 2, 3, 4, 8, 16, 32, 64] if m <= 3 else [1, 2, 4, 8, 16]))
+    ba = int(rng.choice([1, 2, 3, 4, 8, 12, 16, 20, 24, 28, 32, 36, 44, 48, 64] if m <= 3 else [1, 2, 4, 8, 12, 16]))
     bc = int(rng.choice([1, 2, 3, 4, 5, 6, 8, 12, 16] if m <= 4 else [1, 2, 3, 4, 6, 8]))
-    nbar = int(rng.integers(1, {2: 9, 3: 7, 4: 5, 5: 4, 6: 3}[m] if ba < 64 else 4))
+    nbar = int(rng.integers(1, {2: 9, 3: 7, 4: 5, 5: 4, 6: 3}[m] if ba < 36 else 4))
     pbar = int(rng.integers(1, {2: 9, 3: 7, 4: 5, 5: 4, 6: 3}[m]))
     n, p = ba * nbar, bc * pbar
     if orc.bcss_flops(m, n, p, ba, bc) > 2e9:  # keep the numpy oracle fast
