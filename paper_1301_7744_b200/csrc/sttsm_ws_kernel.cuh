@@ -89,7 +89,17 @@ struct WsLevelKernel {
   static constexpr int G = BK / RG;             // groups per stage
   static constexpr int LDA = BK + 4;
   static constexpr int LDR = BN + 4;            // row-major group stride ([e][col])
-  static constexpr int GR_SIZE = RG * LDR;      // >= BN*RG (col-major footprint)
+  // [col][e] staging (e-contiguous blocks): column stride CS; power-of-two row
+  // groups use RG with an XOR swizzle, the others pad to CS = RG+4 or RG+8
+  // (CS/4 odd: the fragment loads' rows fall in distinct banks, no swizzle)
+  static constexpr int CS = POW2 ? RG : (((RG + 4) / 4) % 2 ? RG + 4 : RG + 8);
+  static constexpr int GR_ROW = RG * LDR;
+  static constexpr int GR_COL = BN * CS;
+  // !POW2: the [col][e] layout only where its larger groups keep the ring in
+  // shared memory (else those groups are gathered 8 bytes at a time, [e][col])
+  static constexpr bool NP_EC =
+      !POW2 && (size_t)STAGES * (BM * LDA + (BK / RG) * (GR_ROW > GR_COL ? GR_ROW : GR_COL)) * 8 + 8192 <= 232448;
+  static constexpr int GR_SIZE = NP_EC && GR_COL > GR_ROW ? GR_COL : GR_ROW;  // POW2: >= BN*RG
   static constexpr int SW_SHIFT = RG >= 16 ? 0 : 1;
   static constexpr int SW_MASK = RG >= 16 ? 3 : (RG == 8 ? 1 : 0);
   static constexpr int A_STAGE = BM * LDA, B_STAGE = G * GR_SIZE;
@@ -241,7 +251,9 @@ struct WsLevelKernel {
       const bool ok = grp_ok && (full_n || cg < a.rest);
       const bool ok1 = grp_ok && (full_n || cg + 1 < a.rest);
       const unsigned d = dst + (unsigned)(et * LDR + c2) * 8u;
-      if (pos == 0) {
+      if (pos == 0 && NP_EC) {
+        return;  // staged [col][e] by produce_group_np_ec
+      } else if (pos == 0) {
         long long c0 = cg, c1 = cg + 1;
         if (a.mirror_digits) {
           c0 = digit_rev(cg, a.mirror_digits, a.lbc);
@@ -256,9 +268,9 @@ struct WsLevelKernel {
           cp8z(di + 8u, ok1 ? s1 + i * ESTEP : a.X, ok1);
         }
       } else {
-        const long long bp = a.pw[pos];
-        const long long hi = cg / bp, lo = cg - hi * bp;
-        const double* src = base + lo + hi * bp * a.bA + (long long)(e0 + et) * bp;
+        const int bp = (int)a.pw[pos];  // b_a^p <= rest < 2^31: 32-bit division
+        const int hi = cg / bp, lo = cg - hi * bp;
+        const double* src = base + lo + (long long)hi * bp * a.bA + (long long)(e0 + et) * bp;
         const long long sstep = (long long)ESTEP * bp;
 #pragma unroll 4
         for (int i = 0; i < RG / ESTEP; ++i) {
@@ -266,6 +278,24 @@ struct WsLevelKernel {
           cp16z(di, ok ? src + i * sstep : a.X, ok);
         }
       }
+    }
+  }
+
+  // !POW2, contracted digit at stored position 0 (e-contiguous in HBM):
+  // 16-byte e pairs into the padded [col][e] layout (column stride CS)
+  static __device__ __forceinline__ void produce_group_np_ec(const LevelArgs& a, const double* base, int e0,
+                                                           bool grp_ok, bool full_n, int n0, unsigned dst, int ptid) {
+    constexpr int NP_PAIRS = BN * (RG / 2);
+    static_assert(NP_PAIRS % PT == 0, "e-pair loader balance");
+#pragma unroll 4
+    for (int j = 0; j < NP_PAIRS / PT; ++j) {
+      const int q = ptid + j * PT;
+      const int col = q / (RG / 2), e2 = 2 * (q - col * (RG / 2));
+      const int cg = n0 + col;
+      const bool ok = grp_ok && (full_n || cg < a.rest);
+      const long long cc = a.mirror_digits ? digit_rev(cg, a.mirror_digits, a.lbc) : (long long)cg;
+      const double* src = base + e0 + e2 + (long long)a.bA * cc;
+      cp16z(dst + (unsigned)(col * CS + e2) * 8u, ok ? src : a.X, ok);
     }
   }
 
@@ -298,8 +328,9 @@ struct WsLevelKernel {
         continue;
       }
       if constexpr (!POW2) {
-        if (ptid == 0) modes[g] = 0;
-        produce_group_np(a, base, e0, pos, grp_ok, full_n, n0, dst, ptid);
+        if (ptid == 0) modes[g] = NP_EC && pos == 0;
+        if (NP_EC && pos == 0) produce_group_np_ec(a, base, e0, grp_ok, full_n, n0, dst, ptid);
+        else produce_group_np(a, base, e0, pos, grp_ok, full_n, n0, dst, ptid);
         continue;
       }
       if (ptid == 0) modes[g] = pos == 0;
@@ -388,11 +419,11 @@ struct WsLevelKernel {
                                                        bool cm_rt, double (&acc)[FM][FN][2]) {
     const int lane = threadIdx.x & 31;
     const bool cm = MODE < 0 ? cm_rt : MODE == 1;
-    const double* bp = Bg + (cm ? colw * RG + (lane & 3) : (lane & 3) * LDR + colw);
-    const int SN = cm ? 8 * RG : 8;
+    const double* bp = Bg + (cm ? colw * CS + (lane & 3) : (lane & 3) * LDR + colw);
+    const int SN = cm ? 8 * CS : 8;
 #pragma unroll
     for (int kk = 0; kk < RG / 4; ++kk) {
-      const int ko = cm ? ((kk * 4) ^ sw) : kk * 4 * LDR;
+      const int ko = cm ? (POW2 ? ((kk * 4) ^ sw) : kk * 4) : kk * 4 * LDR;
       double af[NF], bf[FN];
 #pragma unroll
       for (int fm = 0; fm < NF; ++fm) af[fm] = ap[fm * 8 * WM * LDA + (g * RG + kk * 4)];
@@ -421,8 +452,9 @@ struct WsLevelKernel {
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      if constexpr (!POW2) {  // every group is staged [e][col]
-        consume_group<NF, 0>(ap, Bs + g * GR_SIZE, colw, sw, g, false, acc);
+      if constexpr (!POW2) {  // [col][e] (position-0 groups, where it fits) or [e][col]
+        if (NP_EC && md[g]) consume_group<NF, 1>(ap, Bs + g * GR_SIZE, colw, sw, g, true, acc);
+        else consume_group<NF, 0>(ap, Bs + g * GR_SIZE, colw, sw, g, false, acc);
       } else if constexpr (RG >= 16) {  // the mode is CTA-uniform per group: branch to a specialized body
         if (md[g]) consume_group<NF, 1>(ap, Bs + g * GR_SIZE, colw, sw, g, true, acc);
         else consume_group<NF, 0>(ap, Bs + g * GR_SIZE, colw, sw, g, false, acc);
