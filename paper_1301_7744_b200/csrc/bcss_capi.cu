@@ -93,6 +93,8 @@ int bcss_plan_create(int m, int64_t n, int64_t p, int64_t b_a, int64_t b_c, int 
   P->m = m; P->n = n; P->p = p; P->bA = b_a; P->bC = b_c;
   P->nbar = n / b_a; P->pbar = p / b_c; P->reuse = reuse != 0;
   if (const char* e = getenv("BCSS_SERIAL_LAUNCH")) P->concurrent = atoi(e) == 0;
+  if (const char* e = getenv("BCSS_SLICE_MB")) P->slice_bytes = (size_t)std::max(0.0, atof(e) * 1048576.0);
+  if (const char* e = getenv("BCSS_SHARE")) P->share_frac = std::min(1.0, std::max(0.0, atof(e)));
   *out_plan = P;
   return BCSS_OK;
 }

@@ -354,6 +354,9 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
         X.item_off.push_back(X.item_off.back() +
                              (flat ? 1LL : (long long)L.keys_out) * X.n_tiles * ((par.z + C.BM - 1) / C.BM));
         X.flops += (uint64_t)2 * par.z * P.n * L.keys_out * L.rest;
+        if (fast && pc.first >= 0 && pc.first < bcss::N_POLICY_SHAPES)  // modelled time per column (SM shares, run.cu)
+          for (int r = 0; r < par.z; r += C.BM)
+            X.cost += ShapePolicy::tile_cost(ShapePolicy::table(P.bA), pc.first, std::min(C.BM, par.z - r));
       }
     }
     const bool grouped = cascade_wave && k >= 1;
@@ -378,9 +381,24 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
               for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, 0, nt, mt});
             continue;
           }
-          for (int64_t key = k_lo; key < k_hi; ++key)
-            for (int nt = 0; nt < X.n_tiles; ++nt)
-              for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});
+          // Tail slices: the GEMM columns' high part is the tail index (b_c
+          // modes), which is also the slowest dimension of every T(k+1) block,
+          // so a range of n-tiles reads one contiguous slice of each block.  A
+          // parent whose T(k+1) exceeds the slice budget is walked slice by
+          // slice (all keys per slice), so the k+1 reads of a block by
+          // different keys meet in L2 instead of going back to HBM.
+          int slices = 1;
+          if (!grouped && k < P.m - 1 && P.slice_bytes > 0) {
+            const double in_bytes = (double)L.keys_in * (double)L.blk_in * sizeof(double);
+            slices = (int)std::min<double>((double)X.n_tiles, std::ceil(in_bytes / (double)P.slice_bytes));
+            slices = std::max(slices, 1);
+          }
+          for (int sg = 0; sg < slices; ++sg) {
+            const int nt_lo = (int)((int64_t)X.n_tiles * sg / slices), nt_hi = (int)((int64_t)X.n_tiles * (sg + 1) / slices);
+            for (int64_t key = k_lo; key < k_hi; ++key)
+              for (int nt = nt_lo; nt < nt_hi; ++nt)
+                for (int mt = 0; mt < mtiles; ++mt) X.items.push_back(int4{(int)pi, (int)key, nt, mt});
+          }
         }
         if (grouped && X.n_w0 >= (int)X.parents.size()) X.group_w0.push_back((long long)X.items.size());
       }

@@ -56,6 +56,7 @@ struct LaunchHost {
   int cfg = 0;
   int n_tiles = 0;
   uint64_t flops = 0;
+  double cost = 0;                 // modelled time (ShapePolicy::tile_cost units per column), 0 = unknown
   std::vector<int4> parents;       // {in_call, row0, rows, child_off}
   std::vector<long long> item_off; // prefix sums of work items, size parents+1
   std::vector<int4> items;         // per work item {parent, key, n-tile, m-tile}
@@ -131,6 +132,8 @@ struct bcss_plan {
   int64_t last_launches = 0;
   bool timing = false;
   bool concurrent = true;           // concurrent launches per level (BCSS_SERIAL_LAUNCH=1 disables)
+  size_t slice_bytes = 0;           // > 0: parents whose T(k+1) is larger are walked in tail slices of about this size (plan.cu); BCSS_SLICE_MB
+  double share_frac = 0;            // > 0: a level's tile shapes run side by side on SM shares (run.cu); BCSS_SHARE
   int pipeline_waves = 0;           // run_host: overlap H2D / compute / D2H over this many waves
   bool top_first = false;           // first wave computes T(m-1) for all units
   // Mirrored C-block order (pipelined plans): the plan contracts X' (row blocks

@@ -342,11 +342,62 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
           a0 = a1;
         }
       } else {
+        // SM shares: the tile shapes of one level run side by side for the
+        // whole level, each on a share of the SMs proportional to its modelled
+        // time, so the memory-bound small-row shapes (8/16-row parents) draw
+        // on HBM while the tall shapes keep the DMMA pipes busy, instead of
+        // one after the other.  The first share_frac of every launch's items
+        // runs on its share; the rest follows on the same stream as a
+        // full-width grid of short CTAs that fills SMs as the shares finish.
+        std::vector<int> share(nl, 0);
+        bool shared = conc && nl > 1 && P->share_frac > 0;
+        if (shared) {
+          double total = 0;
+          int live = 0;
+          for (const LaunchHost& X : L.launches) {
+            if (X.item_off.back() == 0) continue;
+            if (X.cost <= 0 || is_generic(X.cfg)) shared = false;
+            total += X.cost;
+            ++live;
+          }
+          shared = shared && live > 1 && live <= sms && total > 0;
+          if (shared) {
+            // largest-remainder apportionment with at least one SM per launch
+            std::vector<std::pair<double, int>> rem;
+            int used = 0;
+            for (int li = 0; li < nl; ++li) {
+              const LaunchHost& X = L.launches[li];
+              if (X.item_off.back() == 0) continue;
+              const double q = X.cost / total * sms;
+              share[li] = std::max(1, (int)q);
+              used += share[li];
+              rem.push_back({q - (int)q, li});
+            }
+            std::sort(rem.begin(), rem.end(), [](auto& x, auto& y) { return x.first > y.first; });
+            for (size_t i = 0; used < sms && !rem.empty(); i = (i + 1) % rem.size()) { ++share[rem[i].second]; ++used; }
+            for (size_t i = 0; used > sms; i = (i + 1) % rem.size())
+              if (share[rem[rem.size() - 1 - i].second] > 1) { --share[rem[rem.size() - 1 - i].second]; --used; }
+          }
+        }
         for (int li = 0; li < nl; ++li) {
           const LaunchHost& X = L.launches[li];
           cudaStream_t ls = (li == 0 || !conc) ? s : P->side[li - 1];
-          if (X.item_off.back() == 0) continue;
-          if ((st = launch_one(P, W, L, X, A, X_, C, 0, X.item_off.back(), ls, sms))) return st;
+          const long long total = X.item_off.back();
+          if (total == 0) continue;
+          if (shared) {
+            long long head = (long long)((double)total * P->share_frac);
+            head -= head % share[li];  // whole rounds of the share
+            if (head > 0) {
+              if ((st = launch_one(P, W, L, X, A, X_, C, 0, head, ls, share[li]))) return st;
+              ++launches;
+            }
+            if (head < total) {
+              if ((st = launch_one(P, W, L, X, A, X_, C, head, total, ls, sms))) return st;
+              ++launches;
+            }
+            continue;
+          }
+          if ((st = launch_one(P, W, L, X, A, X_, C, 0, total, ls, sms))) return st;
           ++launches;
         }
       }
