@@ -114,7 +114,9 @@ int bcss_plan_destroy(bcss_plan* P) {
   if (P->hA) cudaFree(P->hA);
   if (P->hX) cudaFree(P->hX);
   if (P->dXm) cudaFree(P->dXm);
+  if (P->dXp) cudaFree(P->dXp);
   if (P->dXt) cudaFree(P->dXt);
+  if (P->dXtp) cudaFree(P->dXtp);
   if (P->hA1) cudaFree(P->hA1);
   if (P->hX1) cudaFree(P->hX1);
   if (P->hC1) cudaFree(P->hC1);

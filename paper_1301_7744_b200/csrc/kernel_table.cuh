@@ -69,9 +69,10 @@ constexpr int BCSS_GEN_OF[N_GEN] = {3, 4, 2, 8};
 // instantiated per row group RG (the largest of 28, 24, 20, 12, 4 dividing
 // b_a; BK a multiple of RG) on three tile shapes, 16 consumer warps each; every
 // policy shape index maps to one of them (BCSS_NP_SHAPES).
-#define BCSS_NP_BIG(RG, BK) WsLevelKernel<128, 128, BK, 4, 4, 3, RG, 4, false, false>
-#define BCSS_NP_MID(RG, BK) WsLevelKernel<64, 256, BK, 2, 8, 3, RG, 4, false, false>
-#define BCSS_NP_SMALL(RG, BK) WsLevelKernel<32, 256, BK, 1, 16, 3, RG, 4, false, false>
+// (PAD: b_a padded up to a multiple of RG, see WsLevelKernel; one more table per RG)
+#define BCSS_NP_BIG(RG, BK, PAD) WsLevelKernel<128, 128, BK, 4, 4, 3, RG, 4, false, false, PAD>
+#define BCSS_NP_MID(RG, BK, PAD) WsLevelKernel<64, 256, BK, 2, 8, 3, RG, 4, false, false, PAD>
+#define BCSS_NP_SMALL(RG, BK, PAD) WsLevelKernel<32, 256, BK, 1, 16, 3, RG, 4, false, false, PAD>
 constexpr int N_NP = 5;
 constexpr int kNpRg[N_NP] = {4, 12, 20, 24, 28};
 extern const KernelCfg kNP4[N_SHAPES];
@@ -79,6 +80,11 @@ extern const KernelCfg kNP12[N_SHAPES];
 extern const KernelCfg kNP20[N_SHAPES];
 extern const KernelCfg kNP24[N_SHAPES];
 extern const KernelCfg kNP28[N_SHAPES];
+extern const KernelCfg kNPP4[N_SHAPES];
+extern const KernelCfg kNPP12[N_SHAPES];
+extern const KernelCfg kNPP20[N_SHAPES];
+extern const KernelCfg kNPP24[N_SHAPES];
+extern const KernelCfg kNPP28[N_SHAPES];
 
 // b_a variants of the fast kernels (one translation unit each): 4, 8, 16, 32, 64
 constexpr int N_BA = 5;

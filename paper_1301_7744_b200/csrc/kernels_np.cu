@@ -1,10 +1,20 @@
 // Fast level kernels for non-power-of-two b_a (POW2 = false), one row group
-// per translation unit (compile with -DBCSS_NP_RG=4|12|20|24|28).  The table
-// has one entry per policy shape index, each one of three tile shapes.
+// per translation unit (compile with -DBCSS_NP_RG=4|12|20|24|28, and
+// -DBCSS_NP_PAD=1 for the padded-row-group variants).  The table has one
+// entry per policy shape index, each one of three tile shapes.
 #include "kernel_table.cuh"
 
 #ifndef BCSS_NP_RG
 #error "define BCSS_NP_RG"
+#endif
+
+#ifndef BCSS_NP_PAD
+#define BCSS_NP_PAD 0
+#endif
+#if BCSS_NP_PAD
+#define BCSS_NP_TABLE kNPP
+#else
+#define BCSS_NP_TABLE kNP
 #endif
 
 #define BCSS_CAT2(a, b) a##b
@@ -20,17 +30,18 @@ constexpr int BK_MID = RG == 4 ? 16 : RG == 12 ? 24 : RG;
 constexpr int BK_SMALL = RG == 4 ? 32 : RG == 12 ? 24 : RG;
 // 32-row tiles need BK a multiple of 8 (loader balance); else the 64-row one
 constexpr bool SMALL_OK = BK_SMALL % 8 == 0;
-using Big = BCSS_NP_BIG(RG, BK_BIG);
-using Mid = BCSS_NP_MID(RG, BK_MID);
+constexpr bool PADDED = BCSS_NP_PAD != 0;
+using Big = BCSS_NP_BIG(RG, BK_BIG, PADDED);
+using Mid = BCSS_NP_MID(RG, BK_MID, PADDED);
 template <bool OK>
-struct SmallSel { using type = BCSS_NP_SMALL(RG, BK_SMALL); };
+struct SmallSel { using type = BCSS_NP_SMALL(RG, BK_SMALL, PADDED); };
 template <>
 struct SmallSel<false> { using type = Mid; };
 using Small = SmallSel<SMALL_OK>::type;
 }  // namespace
 
 // policy shape index -> tile shape (kernel_table.cuh BCSS_FAST_SHAPES order)
-const KernelCfg BCSS_CAT(kNP, BCSS_NP_RG)[N_SHAPES] = {
+const KernelCfg BCSS_CAT(BCSS_NP_TABLE, BCSS_NP_RG)[N_SHAPES] = {
     make_cfg<Big>("np128x128"),   // 0 ws128x128c8
     make_cfg<Mid>("np64x256"),    // 1 ws64x256c8
     make_cfg<Small>("np32x256"),  // 2 ws32x256c8

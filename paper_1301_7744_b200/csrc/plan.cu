@@ -32,10 +32,50 @@ const KernelCfg& kernel_cfg(int cfg) {
     const KernelCfg* const np[bcss::N_NP] = {bcss::kNP4, bcss::kNP12, bcss::kNP20, bcss::kNP24, bcss::kNP28};
     return np[(cfg - np0) % bcss::N_NP][(cfg - np0) / bcss::N_NP];
   }
+  const int npp0 = np0 + bcss::N_NP * N_SHAPES;  // ... padded up to a multiple of the row group
+  if (cfg >= npp0 && cfg < npp0 + bcss::N_NP * N_SHAPES) {
+    const KernelCfg* const npp[bcss::N_NP] = {bcss::kNPP4, bcss::kNPP12, bcss::kNPP20, bcss::kNPP24, bcss::kNPP28};
+    return npp[(cfg - npp0) % bcss::N_NP][(cfg - npp0) / bcss::N_NP];
+  }
   const int ba = (cfg - 1) % bcss::N_BA;
   if (cfg > bcss::N_BA * N_SHAPES)  // general-redirection variants
     return gen[ba][(cfg - 1 - bcss::N_BA * N_SHAPES) / bcss::N_BA];
   return fast[ba][(cfg - 1) / bcss::N_BA];
+}
+// Non-power-of-two b_a (even >= 6, odd >= 15) on the fast kernels (POW2 = false): index of the
+// row group RG (bcss::kNpRg) and the padded block width b_a' >= b_a, a
+// multiple of RG, that the contraction index runs over.  b_a' = b_a when a
+// row group divides b_a (the largest one wins); else the padding with the
+// least wasted DMMA work (rows e >= b_a are zero-filled), where 4-row groups
+// count double (one neighbour entry and one barrier round per 4 rows:
+// measured about half the rate of the 12..28-row groups).  -1: a power of
+// two, or a b_a the generic kernel serves better.
+int np_row_group(int64_t bA, int64_t* padded) {
+  if (bA < 6 || is_pow2(bA)) return -1;
+  // odd b_a moves 8 bytes per copy: below 15 the generic kernel is faster
+  // (measured, m = 3: b_a = 13: 12.2 vs 12.9 TF, 7: 5.4 vs 11.9, 5: 2.0 vs 10.0)
+  if ((bA & 1) && bA < 15) return -1;
+  int best = -1;
+  double best_score = 0;
+  int64_t best_pad = 0;
+  for (int j = 0; j < bcss::N_NP; ++j) {
+    const int64_t rg = bcss::kNpRg[j];
+    const int64_t pad = (bA + rg - 1) / rg * rg;
+    const double score = (double)pad / (double)bA * (rg == 4 ? 2.0 : 1.0);
+    if (best < 0 || score < best_score - 1e-9 || (score < best_score + 1e-9 && rg > bcss::kNpRg[best])) {
+      best = j;
+      best_score = score;
+      best_pad = pad;
+    }
+  }
+  if (padded) *padded = best_pad;
+  return best;
+}
+// contraction rows per block on the fast kernels: b_a, or its padded width
+int64_t padded_ba(int64_t bA) {
+  int64_t pad = bA;
+  if (np_row_group(bA, &pad) < 0) return bA;
+  return pad;
 }
 // general-redirection configuration mirroring fast shape `shape` (one of BCSS_GEN_OF), else -1
 int gen_cfg(int64_t bA, int shape) {
@@ -56,11 +96,11 @@ int fast_cfg(int64_t bA, int shape) {
     case 32: i = 3; break;
     case 64: i = 4; break;
     default: {
-      // non-power-of-two multiple of 4: the largest row group dividing it
-      if (bA < 12 || bA % 4 != 0 || is_pow2(bA)) return -1;
-      for (int j = bcss::N_NP - 1; j >= 0; --j)
-        if (bA % bcss::kNpRg[j] == 0) return 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + shape * bcss::N_NP + j;
-      return -1;
+      int64_t pad = bA;
+      const int j = np_row_group(bA, &pad);
+      if (j < 0) return -1;
+      return 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + (pad != bA ? bcss::N_NP * N_SHAPES : 0) +
+             shape * bcss::N_NP + j;
     }
   }
   return 1 + shape * bcss::N_BA + i;
@@ -76,7 +116,7 @@ struct ShapePolicy {
   ShapePolicy() {
     if (const char* f = getenv("BCSS_FORCE_SHAPE")) force = atoi(f);
   }
-  static int table(int64_t bA) { return bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3; }
+  static int table(int64_t bA) { return !is_pow2(bA) ? 4 : bA <= 4 ? 0 : bA == 8 ? 1 : bA == 16 ? 2 : 3; }
   // time (arbitrary units) of one tile of shape s holding v valid rows
   static double tile_cost(int bi, int s, int v) {
     const int bm = shape_bm(s);

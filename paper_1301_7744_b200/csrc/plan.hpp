@@ -43,11 +43,13 @@ inline int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; r
 using bcss::KernelCfg;
 using bcss::N_SHAPES;
 using bcss::N_GEN;
-constexpr int N_CFGS = 2 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + bcss::N_NP * N_SHAPES;
+constexpr int N_CFGS = 2 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + 2 * bcss::N_NP * N_SHAPES;
 enum { CFG_GENERIC = 0, CFG_GENERIC_PERM = N_CFGS - 1 };
 inline bool is_generic(int cfg) { return cfg == CFG_GENERIC || cfg == CFG_GENERIC_PERM; }
 const KernelCfg& kernel_cfg(int cfg);
 int fast_cfg(int64_t bA, int shape);
+int np_row_group(int64_t bA, int64_t* padded);
+int64_t padded_ba(int64_t bA);
 int gen_cfg(int64_t bA, int shape);
 
 // ---- plan ----------------------------------------------------------------------
@@ -154,6 +156,8 @@ struct bcss_plan {
   bool cascade_nofit = false;       // the disjoint first-wave regions exceeded the workspace limit
   std::vector<int64_t> group_a;     // first-index boundaries of the key groups
   int defer_group = 0;              // cascade: top-level rows of later waves in groups >= this run after wave 0
+  double* dXp = nullptr;            // X with every b_a column block zero-padded to b_a' columns (device, p x n')
+  size_t dXp_bytes = 0;
   double* dXm = nullptr;            // X' (device, p x n)
   size_t dXm_bytes = 0;
   // Gathered X rows for one level (gather_level): row block i of X_g is row
@@ -168,6 +172,8 @@ struct bcss_plan {
   int gather_level = -1;
   size_t off_gather_rows = 0;       // into the device table buffer
   double* dXt = nullptr;            // X_g (device, |gather_rows|·b_C x n)
+  double* dXtp = nullptr;           // X_g with padded column blocks (see dXp)
+  size_t dXtp_bytes = 0;
   size_t dXt_bytes = 0;
   int start_level = 0;              // 0 = from A; else compute below caller-provided T(start_level)
   std::vector<int32_t> start_suffixes;  // their calls (m - start_level entries each)

@@ -34,7 +34,12 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   char* tbl = static_cast<char*>(P->d_tables);
   bcss::LevelArgs a;
   memset(&a, 0, sizeof(a));
-  a.X = (L.k == P->gather_level && !P->gather_rows.empty()) ? P->dXt : X_;
+  // fast kernels on a b_a that no row group divides contract over blocks
+  // padded to b_a' rows: they read the zero-padded copy of X (p x n')
+  const int64_t bAp = is_generic(X.cfg) ? P->bA : padded_ba(P->bA);
+  const bool padded = bAp != P->bA;
+  const bool gathered = L.k == P->gather_level && !P->gather_rows.empty();
+  a.X = gathered ? (padded ? P->dXtp : P->dXt) : (padded ? P->dXp : X_);
   const bool from_input = (P->start_level == 0 && L.k == P->m - 1) || (P->start_level > 0 && L.k == P->start_level - 1);
   a.Tin = from_input ? A : region_for(*P, W, L.k + 1);
   a.Tout = (L.k == P->stop_level) ? C : region_for(*P, W, L.k);
@@ -46,8 +51,9 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   a.keys_in = L.keys_in; a.keys_out = L.keys_out;
   a.blk_in = L.blk_in; a.blk_out = L.blk_out;
   a.n_parents = (int)X.parents.size();
-  a.n = (int)P->n; a.ldx = (int)P->n; a.p_rows = (int)P->p;
+  a.n = (int)(P->nbar * bAp); a.ldx = a.n; a.p_rows = (int)P->p;
   a.nbar = (int)P->nbar; a.bA = (int)P->bA; a.bC = (int)P->bC;
+  a.bAp = (int)bAp;
   a.lbA = is_pow2(P->bA) ? ilog2(P->bA) : -1;
   a.k = L.k;
   a.rest = (int)L.rest; a.bAk = (int)L.bAk;
@@ -78,6 +84,33 @@ __global__ void reverse_row_blocks(const double* __restrict__ src, double* __res
     const long long pbar = p / bc, jb = r / bc;
     dst[i] = src[((pbar - 1 - jb) * bc + (r - jb * bc)) * n + c];
   }
+}
+
+// X with every b_a column block padded to b_a' columns of zeros behind it
+// (fast kernels on a b_a that no row group divides): dst is rows x nbar*b_a'
+__global__ void pad_column_blocks(const double* __restrict__ src, double* __restrict__ dst, long long rows,
+                                  long long nbar, long long ba, long long bap) {
+  const long long np = nbar * bap, total = rows * np;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / np, c = i - r * np;
+    const long long ib = c / bap, e = c - ib * bap;
+    dst[i] = e < ba ? src[r * nbar * ba + ib * ba + e] : 0.0;
+  }
+}
+
+int pad_x(bcss_plan* P, const double* src, long long rows, double** buf, size_t* cap, cudaStream_t s) {
+  const int64_t bAp = padded_ba(P->bA);
+  const size_t xb = (size_t)(rows * P->nbar * bAp) * sizeof(double);
+  if (*cap < xb) {
+    if (*buf) cudaFree(*buf);
+    *buf = nullptr;
+    *cap = 0;
+    CUDA_TRY(cudaMalloc(buf, xb));
+    *cap = xb;
+  }
+  pad_column_blocks<<<296, 256, 0, s>>>(src, *buf, rows, P->nbar, P->bA, bAp);
+  CUDA_TRY(cudaGetLastError());
+  return BCSS_OK;
 }
 
 // gathered X rows (plan.hpp gather_rows): row block i of dst is row block rows[i] of src
@@ -161,6 +194,11 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     CUDA_TRY(cudaGetLastError());
     X_ = P->dXm;
   }
+  const bool pad = padded_ba(P->bA) != P->bA;  // (generic launches, if any, keep reading the plain X)
+  if (pad) {
+    if (pipe && !P->mirror) CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[0], 0));  // X was uploaded ahead of A chunk 0
+    if ((st = pad_x(P, X_, P->p, &P->dXp, &P->dXp_bytes, s))) return st;
+  }
   if (!P->gather_rows.empty()) {  // gathered X rows of one level (shard / child-subset plans)
     const size_t xb = P->gather_rows.size() * (size_t)(P->bC * P->n) * sizeof(double);
     if (P->dXt_bytes < xb) {
@@ -174,6 +212,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     const int* rows = reinterpret_cast<const int*>(static_cast<char*>(P->d_tables) + P->off_gather_rows);
     gather_row_blocks<<<296, 256, 0, s>>>(X_, P->dXt, rows, (long long)P->gather_rows.size(), P->n, P->bC);
     CUDA_TRY(cudaGetLastError());
+    if (pad && (st = pad_x(P, P->dXt, (long long)P->gather_rows.size() * P->bC, &P->dXtp, &P->dXtp_bytes, s))) return st;
   }
   if ((st = ensure_workspace(*P)) == BCSS_ERR_NOMEM && !P->d_ws && !P->keep_temps && P->start_level == 0 &&
       P->stop_level == 0 && P->ws_bytes > 0) {

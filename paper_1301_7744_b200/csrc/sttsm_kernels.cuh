@@ -40,6 +40,8 @@ struct LevelArgs {
   int n_parents;
   int n, ldx, p_rows;
   int nbar, bA, bC, lbA;
+  int bAp;                  // fast kernels: rows per block of the contraction index (b_a, or b_a padded
+                            // up to a multiple of the row group: n and ldx then count padded columns of X)
   int k;
   int rest, bAk;
   int n_tiles;

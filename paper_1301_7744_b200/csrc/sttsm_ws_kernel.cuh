@@ -68,9 +68,14 @@ __device__ __forceinline__ void regs_inc() { asm volatile("setmaxnreg.inc.sync.a
 // launch arguments: stored-block offsets use b_a^p multiplications and
 // divisions instead of shifts, every row group is staged [e][col], and the
 // epilogue splits columns by division.
+// PAD (with POW2 = false): b_a is not a multiple of the row group; the
+// contraction index runs over blocks padded to b_a' = a.bAp rows (X is
+// padded with zero columns, run.cu), rows e >= b_a of a group are zero-filled,
+// and an odd b_a (odd strides, 8-byte alignment only) moves 8 bytes at a time.
 template <int BM_, int BN_, int BK_, int WM, int WN, int STAGES, int BA, int NPROD = 4, bool GEN = false,
-          bool POW2 = true>
+          bool POW2 = true, bool PAD = false>
 struct WsLevelKernel {
+  static_assert(!PAD || !POW2, "padded row groups are a non-power-of-two variant");
   static constexpr int BM = BM_, BN = BN_, BK = BK_;
   static constexpr int NCW = WM * WN;               // consumer warps
   static_assert(NPROD % 4 == 0 && NCW % 4 == 0, "roles must be whole warpgroups");
@@ -170,7 +175,7 @@ struct WsLevelKernel {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
       const int i0 = kstep * BK + g * RG;
-      nb[g] = __ldg(nrow + (i0 < a.n ? (POW2 ? (i0 >> LBA) : i0 / a.bA) : 0));
+      nb[g] = __ldg(nrow + (i0 < a.n ? (POW2 ? (i0 >> LBA) : i0 / a.bAp) : 0));
     }
   }
 
@@ -244,6 +249,8 @@ struct WsLevelKernel {
   static __device__ __forceinline__ void produce_group_np(const LevelArgs& a, const double* base, int e0, int pos,
                                                         bool grp_ok, bool full_n, int n0, unsigned dst, int ptid) {
     const int et = PT >= CPR ? ptid / CPR : 0;
+    const int ev = PAD ? a.bA - e0 - et : RG;  // row et + i*ESTEP of the group is real while i*ESTEP < ev
+    const bool odd = PAD && (a.bA & 1);
 #pragma unroll
     for (int j = 0; j < NCOL; ++j) {
       const int c2 = 2 * ((PT >= CPR ? ptid % CPR : ptid) + j * PT);
@@ -264,18 +271,32 @@ struct WsLevelKernel {
 #pragma unroll 4
         for (int i = 0; i < RG / ESTEP; ++i) {
           const unsigned di = d + (unsigned)(i * ESTEP * LDR) * 8u;
-          cp8z(di, ok ? s0 + i * ESTEP : a.X, ok);
-          cp8z(di + 8u, ok1 ? s1 + i * ESTEP : a.X, ok1);
+          const bool r = !PAD || i * ESTEP < ev;
+          cp8z(di, ok && r ? s0 + i * ESTEP : a.X, ok && r);
+          cp8z(di + 8u, ok1 && r ? s1 + i * ESTEP : a.X, ok1 && r);
         }
       } else {
         const int bp = (int)a.pw[pos];  // b_a^p <= rest < 2^31: 32-bit division
         const int hi = cg / bp, lo = cg - hi * bp;
         const double* src = base + lo + (long long)hi * bp * a.bA + (long long)(e0 + et) * bp;
         const long long sstep = (long long)ESTEP * bp;
+        if (!odd) {
 #pragma unroll 4
-        for (int i = 0; i < RG / ESTEP; ++i) {
-          const unsigned di = d + (unsigned)(i * ESTEP * LDR) * 8u;
-          cp16z(di, ok ? src + i * sstep : a.X, ok);
+          for (int i = 0; i < RG / ESTEP; ++i) {
+            const unsigned di = d + (unsigned)(i * ESTEP * LDR) * 8u;
+            const bool r = ok && (!PAD || i * ESTEP < ev);
+            cp16z(di, r ? src + i * sstep : a.X, r);
+          }
+        } else {  // odd b_a^p: columns cg, cg+1 may sit in different runs, and nothing is 16-byte aligned
+          const int hi1 = (cg + 1) / bp, lo1 = cg + 1 - hi1 * bp;
+          const double* src1 = base + lo1 + (long long)hi1 * bp * a.bA + (long long)(e0 + et) * bp;
+#pragma unroll 4
+          for (int i = 0; i < RG / ESTEP; ++i) {
+            const unsigned di = d + (unsigned)(i * ESTEP * LDR) * 8u;
+            const bool r = i * ESTEP < ev;
+            cp8z(di, ok && r ? src + i * sstep : a.X, ok && r);
+            cp8z(di + 8u, ok1 && r ? src1 + i * sstep : a.X, ok1 && r);
+          }
         }
       }
     }
@@ -287,6 +308,7 @@ struct WsLevelKernel {
                                                            bool grp_ok, bool full_n, int n0, unsigned dst, int ptid) {
     constexpr int NP_PAIRS = BN * (RG / 2);
     static_assert(NP_PAIRS % PT == 0, "e-pair loader balance");
+    const bool odd = PAD && (a.bA & 1);
 #pragma unroll 4
     for (int j = 0; j < NP_PAIRS / PT; ++j) {
       const int q = ptid + j * PT;
@@ -295,7 +317,20 @@ struct WsLevelKernel {
       const bool ok = grp_ok && (full_n || cg < a.rest);
       const long long cc = a.mirror_digits ? digit_rev(cg, a.mirror_digits, a.lbc) : (long long)cg;
       const double* src = base + e0 + e2 + (long long)a.bA * cc;
-      cp16z(dst + (unsigned)(col * CS + e2) * 8u, ok ? src : a.X, ok);
+      const unsigned d = dst + (unsigned)(col * CS + e2) * 8u;
+      if (!PAD) {
+        cp16z(d, ok ? src : a.X, ok);
+      } else {
+        const int er = a.bA - (e0 + e2);  // real rows left from this pair on (even for an even b_a)
+        if (!odd) {
+          const bool r = ok && er >= 2;
+          cp16z(d, r ? src : a.X, r);
+        } else {
+          const bool r0 = ok && er >= 1, r1 = ok && er >= 2;
+          cp8z(d, r0 ? src : a.X, r0);
+          cp8z(d + 8u, r1 ? src + 1 : a.X, r1);
+        }
+      }
     }
   }
 
@@ -321,7 +356,7 @@ struct WsLevelKernel {
       const bool grp_ok = i0 < a.n;
       const int pos = code_p(nb[g].y);
       const double* base = tin_call + (long long)nb[g].x * a.blk_in;
-      const int e0 = POW2 ? (i0 & (BA - 1)) : i0 % a.bA;
+      const int e0 = POW2 ? (i0 & (BA - 1)) : i0 % a.bAp;
       const unsigned dst = Bs_s + (unsigned)(g * GR_SIZE) * 8u;
       if constexpr (GEN) {
         produce_group_gen(a, nb[g].y, base, e0, grp_ok, full_n, n0, dst, modes + g, ptid);
@@ -499,6 +534,28 @@ struct WsLevelKernel {
 #endif
     const long long tstride = (long long)a.bAk * a.bC;
     if constexpr (!POW2) {
+      if (PAD && a.bAk >= 2 && (a.bAk & 1)) {
+        // odd b_a: col and col + 1 may sit in different runs of b_a^k columns,
+        // and rows are only 8-byte aligned (a loop of its own, so the common
+        // case keeps its code)
+#pragma unroll
+        for (int fm = 0; fm < FM; ++fm) {
+          if (roff[fm] == kNoRow) continue;
+          double* base = a.Tout + roff[fm];
+#pragma unroll
+          for (int fn = 0; fn < FN; ++fn) {
+            const int col = nt * BN + (cw % WN) * WTN + fn * 8 + 2 * (lane & 3);
+            if (col >= a.rest) continue;
+            const int q = col / a.bAk;
+            base[(col - q * a.bAk) + tstride * q] = acc[fm][fn][0];
+            if (col + 1 < a.rest) {
+              const int q1 = (col + 1) / a.bAk;
+              base[(col + 1 - q1 * a.bAk) + tstride * q1] = acc[fm][fn][1];
+            }
+          }
+        }
+        return;
+      }
 #pragma unroll
       for (int fm = 0; fm < FM; ++fm) {
         if (roff[fm] == kNoRow) continue;
@@ -602,6 +659,54 @@ struct WsLevelKernel {
     }
   }
 
+  static __device__ __forceinline__ void producer_main(const LevelArgs& a, double* As, double* Bs, long long* rowoff,
+                                                       int4* tiles, uint64_t* full, uint64_t* empty, int* modes,
+                                                       int* srev, long long first, long long total_steps, int ksteps) {
+    const int ptid = threadIdx.x - NCW * 32;
+    if (a.mirror_digits) {  // producers only: named barrier 1 over the PT producer threads
+      if (ptid < BN / CSTEP) srev[ptid] = (int)digit_rev(ptid * CSTEP, a.mirror_digits, a.lbc);
+      asm volatile("bar.sync 1, %0;\n" ::"n"(PT) : "memory");
+    }
+    TileInfo t = decode_item(a, first, BM);
+    long long my_roff = ptid < BM ? row_offset(a, t, ptid) : kNoRow;  // fetched a tile ahead of use
+    int2 nb[G];
+    load_nb(a, t, 0, nb);
+    const unsigned As_s = (unsigned)__cvta_generic_to_shared(As);
+    const unsigned Bs_s = (unsigned)__cvta_generic_to_shared(Bs);
+    int k = 0, slot = 0;
+    unsigned phase = 0;
+    for (long long step = 0; step < total_steps; ++step) {
+      // next stage's position and neighbour entries, loaded before this stage's copies
+      TileInfo tn = t;
+      int kn = k + 1;
+      const bool more = step + 1 < total_steps;
+      if (kn == ksteps) {
+        kn = 0;
+        if (more) tn = decode_item(a, t.item + gridDim.x, BM);
+      }
+      int2 nbn[G];
+      if (more) load_nb(a, tn, kn, nbn);
+      if (step >= STAGES) mbar_wait(empty + slot, phase ^ 1);
+      produce(a, t, k, nb, As_s + (unsigned)(slot * A_STAGE) * 8u, Bs_s + (unsigned)(slot * B_STAGE) * 8u,
+              modes + slot * GPAD, srev, ptid, full + slot);
+      mbar_arrive_cp_async(full + slot);
+      const bool last = (k == ksteps - 1);
+      if (last && ptid < BM) rowoff[slot * BM + ptid] = my_roff;
+      if (ptid == 0) {
+        const int vrows = t.rows - t.mt * BM;
+        tiles[slot] = make_int4(t.nt, ((vrows < BM ? vrows : BM) + 7) >> 3, 0, 0);
+      }
+      mbar_arrive(full + slot);  // release this thread's modes / rowoff / tiles writes
+      if (++slot == STAGES) { slot = 0; phase ^= 1; }
+      if (last && more && ptid < BM) my_roff = row_offset(a, tn, ptid);
+      t = tn;
+      k = kn;
+#pragma unroll
+      for (int g = 0; g < G; ++g) nb[g] = nbn[g];
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+  }
+
   static __device__ void run(const LevelArgs& a) {
     extern __shared__ __align__(16) double smem[];
     double* As = smem;
@@ -630,49 +735,7 @@ struct WsLevelKernel {
     if (warp >= NCW) {
       // ---------------- producer warps ----------------
       regs_dec<PROD_REGS>();
-      const int ptid = threadIdx.x - NCW * 32;
-      if (a.mirror_digits) {  // producers only: named barrier 1 over the PT producer threads
-        if (ptid < BN / CSTEP) srev[ptid] = (int)digit_rev(ptid * CSTEP, a.mirror_digits, a.lbc);
-        asm volatile("bar.sync 1, %0;\n" ::"n"(PT) : "memory");
-      }
-      TileInfo t = decode_item(a, first, BM);
-      long long my_roff = ptid < BM ? row_offset(a, t, ptid) : kNoRow;  // fetched a tile ahead of use
-      int2 nb[G];
-      load_nb(a, t, 0, nb);
-      const unsigned As_s = (unsigned)__cvta_generic_to_shared(As);
-      const unsigned Bs_s = (unsigned)__cvta_generic_to_shared(Bs);
-      int k = 0, slot = 0;
-      unsigned phase = 0;
-      for (long long step = 0; step < total_steps; ++step) {
-        // next stage's position and neighbour entries, loaded before this stage's copies
-        TileInfo tn = t;
-        int kn = k + 1;
-        const bool more = step + 1 < total_steps;
-        if (kn == ksteps) {
-          kn = 0;
-          if (more) tn = decode_item(a, t.item + gridDim.x, BM);
-        }
-        int2 nbn[G];
-        if (more) load_nb(a, tn, kn, nbn);
-        if (step >= STAGES) mbar_wait(empty + slot, phase ^ 1);
-        produce(a, t, k, nb, As_s + (unsigned)(slot * A_STAGE) * 8u, Bs_s + (unsigned)(slot * B_STAGE) * 8u,
-                modes + slot * GPAD, srev, ptid, full + slot);
-        mbar_arrive_cp_async(full + slot);
-        const bool last = (k == ksteps - 1);
-        if (last && ptid < BM) rowoff[slot * BM + ptid] = my_roff;
-        if (ptid == 0) {
-          const int vrows = t.rows - t.mt * BM;
-          tiles[slot] = make_int4(t.nt, ((vrows < BM ? vrows : BM) + 7) >> 3, 0, 0);
-        }
-        mbar_arrive(full + slot);  // release this thread's modes / rowoff / tiles writes
-        if (++slot == STAGES) { slot = 0; phase ^= 1; }
-        if (last && more && ptid < BM) my_roff = row_offset(a, tn, ptid);
-        t = tn;
-        k = kn;
-#pragma unroll
-        for (int g = 0; g < G; ++g) nb[g] = nbn[g];
-      }
-      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      producer_main(a, As, Bs, rowoff, tiles, full, empty, modes, srev, first, total_steps, ksteps);
       return;
     }
     // ---------------- consumer warps ----------------

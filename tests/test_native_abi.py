@@ -128,11 +128,15 @@ def test_int32_table_limits_raise_instead_of_truncating(args):
     ((3, 96, 96, 32, 6), True), ((4, 64, 60, 16, 12), True),        # b_c not a power of two
     ((4, 32, 30, 8, 3), True), ((3, 64, 45, 32, 5), True),          # odd b_c
     ((3, 12, 12, 3, 2), False), ((3, 16, 16, 2, 2), False), ((2, 8, 8, 1, 1), False),
+    # b_a no row group divides: padded row groups (even >= 6, odd >= 15); small odd b_a stays generic
+    ((3, 60, 30, 10, 6), True), ((3, 90, 32, 30, 8), True), ((3, 45, 15, 15, 5), True), ((4, 24, 12, 6, 4), True),
+    ((3, 88, 32, 44, 8), True), ((3, 35, 14, 7, 7), False), ((3, 39, 13, 13, 13), False), ((3, 25, 10, 5, 5), False),
 ])
 def test_fast_kernel_coverage(cfg, fast):
     """Every b_a in {4, 8, 16, 32, 64} runs on the warp-specialized DMMA
     kernels for any b_c (b_a = 64 and non-power-of-two b_c fell
-    to the generic kernel); other b_a use the generic kernel."""
+    to the generic kernel); multiples of 4 and, through padded row groups,
+    even b_a >= 6 and odd b_a >= 15 too; other b_a use the generic kernel."""
     st = bs.SttsmPlan(*cfg).stats()
     if fast:
         assert st["generic_launches"] == 0 and st["fast_launches"] > 0

@@ -23,7 +23,7 @@ bad = 0
 done = 0
 while done < cases:
     m = int(rng.integers(2, 7))
-    ba = int(rng.choice([1, 2, 3, 4, 8, 12, 16, 20, 24, 28, 32, 36, 44, 48, 64] if m <= 3 else [1, 2, 4, 8, 12, 16]))
+    ba = int(rng.choice([1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15, 16, 18, 20, 21, 22, 24, 25, 27, 28, 30, 32, 33, 36, 44, 48, 64] if m <= 3 else [1, 2, 4, 5, 6, 7, 8, 9, 10, 12, 14, 16]))
     bc = int(rng.choice([1, 2, 3, 4, 5, 6, 8, 12, 16] if m <= 4 else [1, 2, 3, 4, 6, 8]))
     nbar = int(rng.integers(1, {2: 9, 3: 7, 4: 5, 5: 4, 6: 3}[m] if ba < 36 else 4))
     pbar = int(rng.integers(1, {2: 9, 3: 7, 4: 5, 5: 4, 6: 3}[m]))
