@@ -29,7 +29,7 @@ UNITS = [("bcss_capi", CSRC / "bcss_capi.cu", []),
          ("sym_upload", CSRC / "sym_upload.cu", [])] + [
     (f"kernels_fast_ba{ba}", CSRC / "kernels_fast.cu", [f"-DBCSS_BA={ba}"]) for ba in (4, 8, 16, 32, 64)] + [
     (f"kernels_np_rg{rg}", CSRC / "kernels_np.cu", [f"-DBCSS_NP_RG={rg}"]) for rg in (4, 12, 20, 24, 28)] + [
-    (f"kernels_npp_rg{rg}", CSRC / "kernels_np.cu", [f"-DBCSS_NP_RG={rg}", "-DBCSS_NP_PAD=1"]) for rg in (4, 12, 20, 24, 28)]
+    (f"kernels_npp_rg{rg}", CSRC / "kernels_np.cu", [f"-DBCSS_NP_RG={rg}", "-DBCSS_NP_PAD=1"]) for rg in (4, 8, 12, 16, 20, 24, 28)]
 HEADERS = [CSRC / "plan.hpp", CSRC / "sttsm_kernels.cuh", CSRC / "sttsm_ws_kernel.cuh", CSRC / "kernel_table.cuh", CSRC / "combinatorics.hpp", CSRC / "shape_costs.hpp",
            ROOT / "include" / "bcss_sttsm.h"]
 

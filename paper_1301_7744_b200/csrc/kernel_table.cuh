@@ -80,8 +80,13 @@ extern const KernelCfg kNP12[N_SHAPES];
 extern const KernelCfg kNP20[N_SHAPES];
 extern const KernelCfg kNP24[N_SHAPES];
 extern const KernelCfg kNP28[N_SHAPES];
+// padded variants (PAD = true): also 8- and 16-row groups, for b_a just below them (6, 14, 15, ...)
+constexpr int N_NPP = 7;
+constexpr int kNppRg[N_NPP] = {4, 8, 12, 16, 20, 24, 28};
 extern const KernelCfg kNPP4[N_SHAPES];
+extern const KernelCfg kNPP8[N_SHAPES];
 extern const KernelCfg kNPP12[N_SHAPES];
+extern const KernelCfg kNPP16[N_SHAPES];
 extern const KernelCfg kNPP20[N_SHAPES];
 extern const KernelCfg kNPP24[N_SHAPES];
 extern const KernelCfg kNPP28[N_SHAPES];

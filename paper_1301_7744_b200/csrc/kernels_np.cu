@@ -1,5 +1,5 @@
 // Fast level kernels for non-power-of-two b_a (POW2 = false), one row group
-// per translation unit (compile with -DBCSS_NP_RG=4|12|20|24|28, and
+// per translation unit (compile with -DBCSS_NP_RG=4|12|20|24|28 (|8|16 padded), and
 // -DBCSS_NP_PAD=1 for the padded-row-group variants).  The table has one
 // entry per policy shape index, each one of three tile shapes.
 #include "kernel_table.cuh"
@@ -24,10 +24,11 @@ namespace bcss {
 namespace {
 constexpr int RG = BCSS_NP_RG;
 // slice depths: a multiple of RG that keeps the loaders balanced and the ring
-// within shared memory (RG 4: 32 / 16 / 32; else RG, or 2 RG for RG 12)
-constexpr int BK_BIG = RG == 4 ? 32 : RG == 12 ? 24 : RG;
-constexpr int BK_MID = RG == 4 ? 16 : RG == 12 ? 24 : RG;
-constexpr int BK_SMALL = RG == 4 ? 32 : RG == 12 ? 24 : RG;
+// within shared memory (RG 4, 8, 16: 32 / 16 / 32; else RG, or 2 RG for RG 12)
+constexpr bool SUB32 = RG == 4 || RG == 8 || RG == 16;  // (8, 16: padded variants only)
+constexpr int BK_BIG = SUB32 ? 32 : RG == 12 ? 24 : RG;
+constexpr int BK_MID = SUB32 ? 16 : RG == 12 ? 24 : RG;
+constexpr int BK_SMALL = SUB32 ? 32 : RG == 12 ? 24 : RG;
 // 32-row tiles need BK a multiple of 8 (loader balance); else the 64-row one
 constexpr bool SMALL_OK = BK_SMALL % 8 == 0;
 constexpr bool PADDED = BCSS_NP_PAD != 0;

@@ -33,9 +33,10 @@ const KernelCfg& kernel_cfg(int cfg) {
     return np[(cfg - np0) % bcss::N_NP][(cfg - np0) / bcss::N_NP];
   }
   const int npp0 = np0 + bcss::N_NP * N_SHAPES;  // ... padded up to a multiple of the row group
-  if (cfg >= npp0 && cfg < npp0 + bcss::N_NP * N_SHAPES) {
-    const KernelCfg* const npp[bcss::N_NP] = {bcss::kNPP4, bcss::kNPP12, bcss::kNPP20, bcss::kNPP24, bcss::kNPP28};
-    return npp[(cfg - npp0) % bcss::N_NP][(cfg - npp0) / bcss::N_NP];
+  if (cfg >= npp0 && cfg < npp0 + bcss::N_NPP * N_SHAPES) {
+    const KernelCfg* const npp[bcss::N_NPP] = {bcss::kNPP4,  bcss::kNPP8,  bcss::kNPP12, bcss::kNPP16,
+                                               bcss::kNPP20, bcss::kNPP24, bcss::kNPP28};
+    return npp[(cfg - npp0) % bcss::N_NPP][(cfg - npp0) / bcss::N_NPP];
   }
   const int ba = (cfg - 1) % bcss::N_BA;
   if (cfg > bcss::N_BA * N_SHAPES)  // general-redirection variants
@@ -50,25 +51,35 @@ const KernelCfg& kernel_cfg(int cfg) {
 // count double (one neighbour entry and one barrier round per 4 rows:
 // measured about half the rate of the 12..28-row groups).  -1: a power of
 // two, or a b_a the generic kernel serves better.
+constexpr double kRg8Penalty = 1.15;  // 8-row groups: two neighbour entries per 16-deep slice
 int np_row_group(int64_t bA, int64_t* padded) {
   if (bA < 6 || is_pow2(bA)) return -1;
   // odd b_a moves 8 bytes per copy: below 15 the generic kernel is faster
   // (measured, m = 3: b_a = 13: 12.2 vs 12.9 TF, 7: 5.4 vs 11.9, 5: 2.0 vs 10.0)
   if ((bA & 1) && bA < 15) return -1;
+  // a 12..28-row group that divides b_a: the unpadded kernels (index into kNpRg)
+  for (int j = bcss::N_NP - 1; j >= 1; --j)
+    if (bA % bcss::kNpRg[j] == 0) {
+      if (padded) *padded = bA;
+      return j;
+    }
+  // else pad (index into kNppRg); a multiple of 4 keeps its 4-row group only
+  // if no padding beats it
   int best = -1;
   double best_score = 0;
   int64_t best_pad = 0;
-  for (int j = 0; j < bcss::N_NP; ++j) {
-    const int64_t rg = bcss::kNpRg[j];
+  for (int j = 0; j < bcss::N_NPP; ++j) {
+    const int64_t rg = bcss::kNppRg[j];
     const int64_t pad = (bA + rg - 1) / rg * rg;
-    const double score = (double)pad / (double)bA * (rg == 4 ? 2.0 : 1.0);
-    if (best < 0 || score < best_score - 1e-9 || (score < best_score + 1e-9 && rg > bcss::kNpRg[best])) {
+    const double score = (double)pad / (double)bA * (rg == 4 ? 2.0 : rg == 8 ? kRg8Penalty : 1.0);
+    if (best < 0 || score < best_score - 1e-9 || (score < best_score + 1e-9 && rg > bcss::kNppRg[best])) {
       best = j;
       best_score = score;
       best_pad = pad;
     }
   }
   if (padded) *padded = best_pad;
+  if (best_pad == bA) return 0;  // (a multiple of 4 that 4-row groups serve best: kNpRg[0] = 4, unpadded)
   return best;
 }
 // contraction rows per block on the fast kernels: b_a, or its padded width
@@ -99,8 +110,9 @@ int fast_cfg(int64_t bA, int shape) {
       int64_t pad = bA;
       const int j = np_row_group(bA, &pad);
       if (j < 0) return -1;
-      return 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + (pad != bA ? bcss::N_NP * N_SHAPES : 0) +
-             shape * bcss::N_NP + j;
+      const int np0 = 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN;
+      if (pad == bA) return np0 + shape * bcss::N_NP + j;               // j indexes kNpRg
+      return np0 + bcss::N_NP * N_SHAPES + shape * bcss::N_NPP + j;     // j indexes kNppRg
     }
   }
   return 1 + shape * bcss::N_BA + i;

@@ -43,7 +43,7 @@ inline int64_t ipow(int64_t b, int e) { int64_t r = 1; while (e-- > 0) r *= b; r
 using bcss::KernelCfg;
 using bcss::N_SHAPES;
 using bcss::N_GEN;
-constexpr int N_CFGS = 2 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + 2 * bcss::N_NP * N_SHAPES;
+constexpr int N_CFGS = 2 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + (bcss::N_NP + bcss::N_NPP) * N_SHAPES;
 enum { CFG_GENERIC = 0, CFG_GENERIC_PERM = N_CFGS - 1 };
 inline bool is_generic(int cfg) { return cfg == CFG_GENERIC || cfg == CFG_GENERIC_PERM; }
 const KernelCfg& kernel_cfg(int cfg);
