@@ -52,7 +52,7 @@ const KernelCfg& kernel_cfg(int cfg) {
 // measured about half the rate of the 12..28-row groups).  -1: a power of
 // two, or a b_a the generic kernel serves better.
 constexpr double kRg8Penalty = 1.15;  // 8-row groups: two neighbour entries per 16-deep slice
-int np_row_group(int64_t bA, int64_t* padded) {
+int np_row_group(int64_t bA, int m, int64_t* padded) {
   if (bA < 6 || is_pow2(bA)) return -1;
   // odd b_a moves 8 bytes per copy: below 15 the generic kernel is faster
   // (measured, m = 3: b_a = 13: 12.2 vs 12.9 TF, 7: 5.4 vs 11.9, 5: 2.0 vs 10.0)
@@ -64,7 +64,11 @@ int np_row_group(int64_t bA, int64_t* padded) {
       return j;
     }
   // else pad (index into kNppRg); a multiple of 4 keeps its 4-row group only
-  // if no padding beats it
+  // if no padding beats it.  Not where the top level has fewer than 64 GEMM
+  // columns per key (b_a^(m-1): b_a = 6 at m = 3, any b_a at m = 2): the
+  // key-major tiles are mostly empty there and the generic kernel's flat
+  // (key, column) tiles win (measured, m = 3, b_a = 6: 6.5 vs 11.3 TF)
+  if (bA % 4 != 0 && std::pow((double)bA, m - 1) < 64.0) return -1;
   int best = -1;
   double best_score = 0;
   int64_t best_pad = 0;
@@ -83,22 +87,22 @@ int np_row_group(int64_t bA, int64_t* padded) {
   return best;
 }
 // contraction rows per block on the fast kernels: b_a, or its padded width
-int64_t padded_ba(int64_t bA) {
+int64_t padded_ba(int64_t bA, int m) {
   int64_t pad = bA;
-  if (np_row_group(bA, &pad) < 0) return bA;
+  if (np_row_group(bA, m, &pad) < 0) return bA;
   return pad;
 }
 // general-redirection configuration mirroring fast shape `shape` (one of BCSS_GEN_OF), else -1
-int gen_cfg(int64_t bA, int shape) {
+int gen_cfg(int64_t bA, int m, int shape) {
   if (!is_pow2(bA)) return -1;  // general redirection: power-of-two b_a only
-  const int f = fast_cfg(bA, 0);
+  const int f = fast_cfg(bA, m, 0);
   if (f < 0) return -1;
   for (int g = 0; g < N_GEN; ++g)
     if (bcss::BCSS_GEN_OF[g] == shape) return 1 + bcss::N_BA * N_SHAPES + g * bcss::N_BA + (f - 1);
   return -1;
 }
 // fast configuration of tile shape `shape` for power-of-two b_a in {4, 8, 16, 32, 64}, else -1
-int fast_cfg(int64_t bA, int shape) {
+int fast_cfg(int64_t bA, int m, int shape) {
   int i;
   switch (bA) {
     case 4: i = 0; break;
@@ -108,7 +112,7 @@ int fast_cfg(int64_t bA, int shape) {
     case 64: i = 4; break;
     default: {
       int64_t pad = bA;
-      const int j = np_row_group(bA, &pad);
+      const int j = np_row_group(bA, m, &pad);
       if (j < 0) return -1;
       const int np0 = 1 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN;
       if (pad == bA) return np0 + shape * bcss::N_NP + j;               // j indexes kNpRg
@@ -252,7 +256,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
   // (any b_c: rows are (jb, c) pairs addressed by division, the tail modes
   // pass through the column index whole; the mirrored C order alone needs a
   // power-of-two b_c)
-  const bool fast_shape = fast_cfg(P.bA, 0) >= 0;
+  const bool fast_shape = fast_cfg(P.bA, P.m, 0) >= 0;
   static const ShapePolicy policy;
   W.levels.clear();
   std::vector<int32_t> prev_suffix;  // suffixes of level k+1 calls
@@ -383,7 +387,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       for (const auto& pc : pieces) {
         // generic kernel: the insertion-form addressing unless the level
         // redirects through general permutations (reuse=False top level)
-        const int cfg = fast ? fast_cfg(P.bA, pc.first) : gen ? gen_cfg(P.bA, pc.first)
+        const int cfg = fast ? fast_cfg(P.bA, P.m, pc.first) : gen ? gen_cfg(P.bA, P.m, pc.first)
                         : (P.reuse || k < P.m - 1) ? CFG_GENERIC : CFG_GENERIC_PERM;
         int4 par = whole;
         par.y = whole.y + r0;
@@ -478,7 +482,7 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
       constexpr int kHalfShape = 10;  // ws32x128c16s5
       if (total > sms && r > 0 && r <= sms / 2) {
         LaunchHost T;
-        T.cfg = fast_cfg(P.bA, kHalfShape);
+        T.cfg = fast_cfg(P.bA, P.m, kHalfShape);
         T.n_tiles = (int)(L.rest / kernel_cfg(T.cfg).BN);
         T.parents = X.parents;
         for (long long i = total - r; i < total; ++i) {
@@ -535,7 +539,7 @@ int build_plan(bcss_plan& P) {
     std::vector<int> units = P.units;
     // mirrored C order for pipelined full runs on the fast kernels
     P.mirror = P.pipeline_waves > 1 && !P.keep_temps && !P.units_set && P.start_level == 0 &&
-               P.stop_level == 0 && P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, 0) >= 0 &&
+               P.stop_level == 0 && P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, P.m, 0) >= 0 &&
                !getenv("BCSS_NO_MIRROR");
     const bool cascade_ok = P.mirror && !getenv("BCSS_NO_CASCADE") && !P.cascade_nofit;
     P.cascade = false;  // decided by the pipeline model below

@@ -47,10 +47,10 @@ constexpr int N_CFGS = 2 + bcss::N_BA * N_SHAPES + bcss::N_BA * N_GEN + (bcss::N
 enum { CFG_GENERIC = 0, CFG_GENERIC_PERM = N_CFGS - 1 };
 inline bool is_generic(int cfg) { return cfg == CFG_GENERIC || cfg == CFG_GENERIC_PERM; }
 const KernelCfg& kernel_cfg(int cfg);
-int fast_cfg(int64_t bA, int shape);
-int np_row_group(int64_t bA, int64_t* padded);
-int64_t padded_ba(int64_t bA);
-int gen_cfg(int64_t bA, int shape);
+int fast_cfg(int64_t bA, int m, int shape);
+int np_row_group(int64_t bA, int m, int64_t* padded);
+int64_t padded_ba(int64_t bA, int m);
+int gen_cfg(int64_t bA, int m, int shape);
 
 // ---- plan ----------------------------------------------------------------------
 // One kernel launch: the parents of a level that share a tile configuration.

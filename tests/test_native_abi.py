@@ -131,6 +131,7 @@ def test_int32_table_limits_raise_instead_of_truncating(args):
     # b_a no row group divides: padded row groups (even >= 6, odd >= 15); small odd b_a stays generic
     ((3, 60, 30, 10, 6), True), ((3, 90, 32, 30, 8), True), ((3, 45, 15, 15, 5), True), ((4, 24, 12, 6, 4), True),
     ((3, 88, 32, 44, 8), True), ((3, 35, 14, 7, 7), False), ((3, 39, 13, 13, 13), False), ((3, 25, 10, 5, 5), False),
+    ((3, 24, 12, 6, 4), False), ((2, 44, 16, 22, 8), False),  # fewer than 64 columns per key at the top level
 ])
 def test_fast_kernel_coverage(cfg, fast):
     """Every b_a in {4, 8, 16, 32, 64} runs on the warp-specialized DMMA

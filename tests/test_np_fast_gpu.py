@@ -37,7 +37,9 @@ def test_np_fast_kernels_match_oracle(cfg):
     want = orc.sttsm_bcss_packed(a, x, m, n, ba, bc)
     plan = bs.SttsmPlan(m, n, p, ba, bc)
     st = plan.stats()
-    if ba % 2 == 0 or ba >= 15:  # (small odd b_a stays on the generic kernel: faster there)
+    # (small odd b_a, and padded b_a with fewer than 64 top-level columns per
+    # key, stay on the generic kernel: faster there)
+    if ba % 4 == 0 or ((ba % 2 == 0 or ba >= 15) and ba ** (m - 1) >= 64):
         assert st["generic_launches"] == 0 and st["fast_launches"] > 0
     c = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64, device="cuda")
     plan.run(torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), c)
