@@ -64,11 +64,8 @@ int np_row_group(int64_t bA, int m, int64_t* padded) {
       return j;
     }
   // else pad (index into kNppRg); a multiple of 4 keeps its 4-row group only
-  // if no padding beats it.  Not where the top level has fewer than 64 GEMM
-  // columns per key (b_a^(m-1): b_a = 6 at m = 3, any b_a at m = 2): the
-  // key-major tiles are mostly empty there and the generic kernel's flat
-  // (key, column) tiles win (measured, m = 3, b_a = 6: 6.5 vs 11.3 TF)
-  if (bA % 4 != 0 && std::pow((double)bA, m - 1) < 64.0) return -1;
+  // if no padding beats it
+  (void)m;  // (problems with fewer than 64 top-level columns per key never get here: fast_cfg)
   int best = -1;
   double best_score = 0;
   int64_t best_pad = 0;
@@ -89,7 +86,7 @@ int np_row_group(int64_t bA, int m, int64_t* padded) {
 // contraction rows per block on the fast kernels: b_a, or its padded width
 int64_t padded_ba(int64_t bA, int m) {
   int64_t pad = bA;
-  if (np_row_group(bA, m, &pad) < 0) return bA;
+  if (fast_cfg(bA, m, 0) < 0 || np_row_group(bA, m, &pad) < 0) return bA;
   return pad;
 }
 // general-redirection configuration mirroring fast shape `shape` (one of BCSS_GEN_OF), else -1
@@ -103,6 +100,14 @@ int gen_cfg(int64_t bA, int m, int shape) {
 }
 // fast configuration of tile shape `shape` for power-of-two b_a in {4, 8, 16, 32, 64}, else -1
 int fast_cfg(int64_t bA, int m, int shape) {
+  if (getenv("BCSS_FORCE_GENERIC")) return -1;  // (experiments)
+  // Few GEMM columns per key at the top level (b_a^(m-1) < 64, and every
+  // m = 2 problem): the fast kernels' key-major tiles of 128..512 columns
+  // are mostly empty, the generic kernel's flat (key, column) tiles are not
+  // (measured: m=3 b=4 3.8 vs 9.0 TF, m=2 b=32 4.0 vs 9.6, m=2 b=64 8.1 vs
+  // 13.5; at 64 columns with m >= 3 the fast kernels win: m=3 b=8 15.6 vs
+  // 13.2, m=4 b=4 9.6 vs 7.1).  BCSS_FORCE_FAST keeps the fast kernels (tests).
+  if ((m == 2 || std::pow((double)bA, m - 1) < 64.0) && !getenv("BCSS_FORCE_FAST")) return -1;
   int i;
   switch (bA) {
     case 4: i = 0; break;

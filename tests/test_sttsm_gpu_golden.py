@@ -25,7 +25,7 @@ def _load(path):
 
 @pytest.mark.parametrize("path", CASES, ids=lambda s: s.split("/")[-1][6:-4])
 @pytest.mark.parametrize("reuse", [True, False])
-def test_drop_in_matches_reference(path, reuse):
+def test_drop_in_matches_reference(path, reuse, kernels):
     d, m, n, p, b_a, b_c = _load(path)
     a = bs.BcssTensor(m, n, b_a, payload=d["A"])
     ctr = bs.OpCounter()
@@ -51,7 +51,7 @@ def test_temp_hook_replays_reference_temporaries(golden_dir):
 
 
 @pytest.mark.parametrize("path", CASES, ids=lambda s: s.split("/")[-1][6:-4])
-def test_pipelined_mirrored_plan_matches_reference(path):
+def test_pipelined_mirrored_plan_matches_reference(path, kernels):
     """The e2e path (pipelined plan: chunked upload, mirrored C order, per-wave
     downloads) on every golden case, through run_host with pinned buffers and
     through the device run."""

@@ -7,6 +7,7 @@ the numpy oracle (rel. Frobenius <= 1e-12; partial plans on their own blocks).
 
 usage: python tools/fuzz.py [cases] [seed]
 """
+import os
 import sys
 
 import numpy as np
@@ -31,6 +32,12 @@ while done < cases:
     if orc.bcss_flops(m, n, p, ba, bc) > 2e9:  # keep the numpy oracle fast
         continue
     done += 1
+    # half of the cases keep the fast kernels on shapes whose few columns per
+    # key would send them to the generic kernel (the product's own rule)
+    if rng.random() < 0.5:
+        os.environ["BCSS_FORCE_FAST"] = "1"
+    else:
+        os.environ.pop("BCSS_FORCE_FAST", None)
     a = orc.random_bcss_packed(m, n, ba, int(rng.integers(1 << 30)))
     x = rng.standard_normal((p, n))
     want = orc.sttsm_bcss_packed(a, x, m, n, ba, bc)
