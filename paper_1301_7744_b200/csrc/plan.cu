@@ -542,6 +542,9 @@ int build_plan(bcss_plan& P) {
   if (P.built) return BCSS_OK;
   try {
     std::vector<int> units = P.units;
+    // contraction rows per block on the fast kernels (fixed with the plan's
+    // kernel choice: the runs must not re-derive it from the environment)
+    P.bAp = padded_ba(P.bA, P.m);
     // mirrored C order for pipelined full runs on the fast kernels
     P.mirror = P.pipeline_waves > 1 && !P.keep_temps && !P.units_set && P.start_level == 0 &&
                P.stop_level == 0 && P.reuse && is_pow2(P.bC) && fast_cfg(P.bA, P.m, 0) >= 0 &&

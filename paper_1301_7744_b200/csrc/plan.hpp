@@ -100,6 +100,7 @@ using bcss_host::WaveHost;
 struct bcss_plan {
   int m = 0;
   int64_t n = 0, p = 0, bA = 0, bC = 0, nbar = 0, pbar = 0;
+  int64_t bAp = 0;                  // b_a, or its padded width on the fast kernels (set by build_plan)
   bool reuse = true;
   std::vector<int> units;
   bool units_set = false;

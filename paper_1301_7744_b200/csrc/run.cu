@@ -36,7 +36,7 @@ int launch_one(bcss_plan* P, const WaveHost& W, const LevelHost& L, const Launch
   memset(&a, 0, sizeof(a));
   // fast kernels on a b_a that no row group divides contract over blocks
   // padded to b_a' rows: they read the zero-padded copy of X (p x n')
-  const int64_t bAp = is_generic(X.cfg) ? P->bA : padded_ba(P->bA, P->m);
+  const int64_t bAp = is_generic(X.cfg) ? P->bA : P->bAp;
   const bool padded = bAp != P->bA;
   const bool gathered = L.k == P->gather_level && !P->gather_rows.empty();
   a.X = gathered ? (padded ? P->dXtp : P->dXt) : (padded ? P->dXp : X_);
@@ -99,7 +99,7 @@ __global__ void pad_column_blocks(const double* __restrict__ src, double* __rest
 }
 
 int pad_x(bcss_plan* P, const double* src, long long rows, double** buf, size_t* cap, cudaStream_t s) {
-  const int64_t bAp = padded_ba(P->bA, P->m);
+  const int64_t bAp = P->bAp;
   const size_t xb = (size_t)(rows * P->nbar * bAp) * sizeof(double);
   if (*cap < xb) {
     if (*buf) cudaFree(*buf);
@@ -194,7 +194,7 @@ int run_impl(bcss_plan* P, const double* A, const double* X_, double* C, cudaStr
     CUDA_TRY(cudaGetLastError());
     X_ = P->dXm;
   }
-  const bool pad = padded_ba(P->bA, P->m) != P->bA;  // (generic launches, if any, keep reading the plain X)
+  const bool pad = P->bAp != P->bA;  // (generic launches, if any, keep reading the plain X)
   if (pad) {
     if (pipe && !P->mirror) CUDA_TRY(cudaStreamWaitEvent(s, chunk_ev[0], 0));  // X was uploaded ahead of A chunk 0
     if ((st = pad_x(P, X_, P->p, &P->dXp, &P->dXp_bytes, s))) return st;
