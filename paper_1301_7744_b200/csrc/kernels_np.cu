@@ -32,7 +32,15 @@ constexpr int BK_SMALL = SUB32 ? 32 : RG == 12 ? 24 : RG;
 // 32-row tiles need BK a multiple of 8 (loader balance); else the 64-row one
 constexpr bool SMALL_OK = BK_SMALL % 8 == 0;
 constexpr bool PADDED = BCSS_NP_PAD != 0;
+#ifdef BCSS_NP_BIG_ALT
+template <bool ALT>
+struct BigSel { using type = BCSS_NP_BIG96(RG, BK_BIG, PADDED); };
+template <>
+struct BigSel<false> { using type = BCSS_NP_BIG(RG, BK_BIG, PADDED); };
+using Big = BigSel<(BK_BIG <= 28 && (96 * BK_BIG / 2) % 128 == 0)>::type;
+#else
 using Big = BCSS_NP_BIG(RG, BK_BIG, PADDED);
+#endif
 using Mid = BCSS_NP_MID(RG, BK_MID, PADDED);
 template <bool OK>
 struct SmallSel { using type = BCSS_NP_SMALL(RG, BK_SMALL, PADDED); };
