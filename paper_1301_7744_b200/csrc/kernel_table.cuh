@@ -71,7 +71,7 @@ constexpr int BCSS_GEN_OF[N_GEN] = {3, 4, 2, 8};
 // policy shape index maps to one of them (BCSS_NP_SHAPES).
 // (PAD: b_a padded up to a multiple of RG, see WsLevelKernel; one more table per RG)
 #define BCSS_NP_BIG(RG, BK, PAD) WsLevelKernel<128, 128, BK, 4, 4, 3, RG, 4, false, false, PAD>
-// (experiment -DBCSS_NP_BIG_ALT: 96x128 tiles, 12 consumer warps, 4 stages where the ring fits)
+// 96x128 tiles, 12 consumer warps, 4 stages (row groups 12 and 24: kernels_np.cu)
 #define BCSS_NP_BIG96(RG, BK, PAD) WsLevelKernel<96, 128, BK, 3, 4, 4, RG, 4, false, false, PAD>
 #define BCSS_NP_MID(RG, BK, PAD) WsLevelKernel<64, 256, BK, 2, 8, 3, RG, 4, false, false, PAD>
 #define BCSS_NP_SMALL(RG, BK, PAD) WsLevelKernel<32, 256, BK, 1, 16, 3, RG, 4, false, false, PAD>

@@ -32,15 +32,16 @@ constexpr int BK_SMALL = SUB32 ? 32 : RG == 12 ? 24 : RG;
 // 32-row tiles need BK a multiple of 8 (loader balance); else the 64-row one
 constexpr bool SMALL_OK = BK_SMALL % 8 == 0;
 constexpr bool PADDED = BCSS_NP_PAD != 0;
-#ifdef BCSS_NP_BIG_ALT
-template <bool ALT>
-struct BigSel { using type = BCSS_NP_BIG96(RG, BK_BIG, PADDED); };
-template <>
-struct BigSel<false> { using type = BCSS_NP_BIG(RG, BK_BIG, PADDED); };
-using Big = BigSel<(BK_BIG <= 28 && (96 * BK_BIG / 2) % 128 == 0)>::type;
-#else
 using Big = BCSS_NP_BIG(RG, BK_BIG, PADDED);
-#endif
+// 96x128 tiles with 12 consumer warps and a 4-deep ring, where the ring fits
+// and the loaders balance (BK = 24: row groups 12 and 24), for the policy's
+// 96-row shape; unpadded kernels only (measured: b_a = 24 top level 27.7 ->
+// 29.4 TF at m = 3, 24.5 -> 32.4 TF at m = 4; the padded variants lose 2 %)
+template <bool OK>
+struct Big96Sel { using type = BCSS_NP_BIG96(RG, BK_BIG, PADDED); };
+template <>
+struct Big96Sel<false> { using type = Big; };
+using Big96 = Big96Sel<(!PADDED && BK_BIG <= 28 && (96 * BK_BIG / 2) % 128 == 0)>::type;
 using Mid = BCSS_NP_MID(RG, BK_MID, PADDED);
 template <bool OK>
 struct SmallSel { using type = BCSS_NP_SMALL(RG, BK_SMALL, PADDED); };
@@ -59,7 +60,7 @@ const KernelCfg BCSS_CAT(BCSS_NP_TABLE, BCSS_NP_RG)[N_SHAPES] = {
     make_cfg<Small>("np32x256"),  // 5 ws32x256c16
     make_cfg<Small>("np32x256"),  // 6 ws16x512c16k16
     make_cfg<Mid>("np64x256"),    // 7 ws64x256c16k16s5
-    make_cfg<Big>("np128x128"),   // 8 ws96x128c12
+    make_cfg<Big96>(Big96::BM == 96 ? "np96x128" : "np128x128"),  // 8 ws96x128c12
     make_cfg<Mid>("np64x256"),    // 9 ws48x256c12k16
     make_cfg<Small>("np32x256"),  // 10 ws32x128c16s5
 };

@@ -43,44 +43,55 @@ const KernelCfg& kernel_cfg(int cfg) {
     return gen[ba][(cfg - 1 - bcss::N_BA * N_SHAPES) / bcss::N_BA];
   return fast[ba][(cfg - 1) / bcss::N_BA];
 }
-// Non-power-of-two b_a (even >= 6, odd >= 15) on the fast kernels (POW2 = false): index of the
-// row group RG (bcss::kNpRg) and the padded block width b_a' >= b_a, a
-// multiple of RG, that the contraction index runs over.  b_a' = b_a when a
-// row group divides b_a (the largest one wins); else the padding with the
-// least wasted DMMA work (rows e >= b_a are zero-filled), where 4-row groups
-// count double (one neighbour entry and one barrier round per 4 rows:
-// measured about half the rate of the 12..28-row groups).  -1: a power of
+// Non-power-of-two b_a (even >= 6, odd >= 15) on the fast kernels (POW2 =
+// false): np_row_group returns the index of the row group RG and the block
+// width b_a' the contraction index runs over - b_a itself when RG divides it
+// (unpadded kernels, index into bcss::kNpRg), else b_a padded up to a multiple
+// of RG (rows e >= b_a zero-filled; index into bcss::kNppRg).  -1: a power of
 // two, or a b_a the generic kernel serves better.
-constexpr double kRg8Penalty = 1.15;  // 8-row groups: two neighbour entries per 16-deep slice
+// relative rate of the POW2 = false kernels by row group (measured full-size
+// shapes, profiles/r02/padded_row_groups.txt and np_shapes.txt: RG 20 / 24 run
+// at 28-31 TF, 28 at 26, 16 at ~24, 12 at 18-19, 8 at ~20, 4 at ~13)
+static double np_rate(int64_t rg) {
+  switch (rg) {
+    case 4: return 0.45;
+    case 8: return 0.70;
+    case 12: return 0.65;
+    case 16: return 0.82;
+    case 28: return 0.80;  // (its [col][e] ring does not fit: level 0 gathers 8 bytes at a time)
+    default: return 1.0;
+  }
+}
 int np_row_group(int64_t bA, int m, int64_t* padded) {
+  (void)m;  // (problems with fewer than 64 top-level columns per key never get here: fast_cfg)
   if (bA < 6 || is_pow2(bA)) return -1;
   // odd b_a moves 8 bytes per copy: below 15 the generic kernel is faster
   // (measured, m = 3: b_a = 13: 12.2 vs 12.9 TF, 7: 5.4 vs 11.9, 5: 2.0 vs 10.0)
   if ((bA & 1) && bA < 15) return -1;
-  // a 12..28-row group that divides b_a: the unpadded kernels (index into kNpRg)
-  for (int j = bcss::N_NP - 1; j >= 1; --j)
-    if (bA % bcss::kNpRg[j] == 0) {
-      if (padded) *padded = bA;
-      return j;
-    }
-  // else pad (index into kNppRg); a multiple of 4 keeps its 4-row group only
-  // if no padding beats it
-  (void)m;  // (problems with fewer than 64 top-level columns per key never get here: fast_cfg)
+  // candidates: a row group that divides b_a (unpadded kernels, index into
+  // kNpRg), or b_a padded up to a multiple of a row group (index into
+  // kNppRg); the least wasted DMMA work per unit rate wins, ties to the
+  // larger row group (so 36 runs as 40 = 2 x 20 rather than 3 x 12, 44 as
+  // 48 = 2 x 24 rather than 11 x 4)
   int best = -1;
   double best_score = 0;
-  int64_t best_pad = 0;
-  for (int j = 0; j < bcss::N_NPP; ++j) {
-    const int64_t rg = bcss::kNppRg[j];
-    const int64_t pad = (bA + rg - 1) / rg * rg;
-    const double score = (double)pad / (double)bA * (rg == 4 ? 2.0 : rg == 8 ? kRg8Penalty : 1.0);
-    if (best < 0 || score < best_score - 1e-9 || (score < best_score + 1e-9 && rg > bcss::kNppRg[best])) {
+  int64_t best_pad = 0, best_rg = 0;
+  auto consider = [&](int j, int64_t rg, int64_t pad, double bonus) {
+    const double score = (double)pad / (double)bA / np_rate(rg) * bonus;
+    if (best < 0 || score < best_score - 1e-9 || (score < best_score + 1e-9 && rg > best_rg)) {
       best = j;
       best_score = score;
       best_pad = pad;
+      best_rg = rg;
     }
+  };
+  for (int j = 0; j < bcss::N_NP; ++j)
+    if (bA % bcss::kNpRg[j] == 0) consider(j, bcss::kNpRg[j], bA, 0.95);  // (near ties go to the unpadded kernels)
+  for (int j = 0; j < bcss::N_NPP; ++j) {
+    const int64_t rg = bcss::kNppRg[j];
+    if (bA % rg != 0) consider(j, rg, (bA + rg - 1) / rg * rg, 1.0);
   }
   if (padded) *padded = best_pad;
-  if (best_pad == bA) return 0;  // (a multiple of 4 that 4-row groups serve best: kNpRg[0] = 4, unpadded)
   return best;
 }
 // contraction rows per block on the fast kernels: b_a, or its padded width
@@ -521,6 +532,11 @@ void build_wave_levels(bcss_plan& P, WaveHost& W, bool cascade_wave) {
         fprintf(stderr, "[bcss plan] level %d %-18s parents %zu items %lld gflop %.2f rows:", L.k,
                 kernel_cfg(X.cfg).name, X.parents.size(), (long long)X.item_off.back(), X.flops / 1e9);
         for (auto& kv : rows_hist) fprintf(stderr, " %dx%d", kv.first, kv.second);
+        if (!is_generic(X.cfg) && !is_pow2(P.bA)) {  // non-power-of-two b_a: its row group and padded width
+          int64_t pad = P.bA;
+          const int j = np_row_group(P.bA, P.m, &pad);
+          if (j >= 0) fprintf(stderr, " (row group %d, b_a' %lld)", pad == P.bA ? bcss::kNpRg[j] : bcss::kNppRg[j], (long long)pad);
+        }
         fprintf(stderr, "\n");
       }
     }
