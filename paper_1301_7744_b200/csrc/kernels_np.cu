@@ -33,15 +33,17 @@ constexpr int BK_SMALL = SUB32 ? 32 : RG == 12 ? 24 : RG;
 constexpr bool SMALL_OK = BK_SMALL % 8 == 0;
 constexpr bool PADDED = BCSS_NP_PAD != 0;
 using Big = BCSS_NP_BIG(RG, BK_BIG, PADDED);
-// 96x128 tiles with 12 consumer warps and a 4-deep ring, where the ring fits
-// and the loaders balance (BK = 24: row groups 12 and 24), for the policy's
-// 96-row shape; unpadded kernels only (measured: b_a = 24 top level 27.7 ->
-// 29.4 TF at m = 3, 24.5 -> 32.4 TF at m = 4; the padded variants lose 2 %)
+// 96x128 tiles with 12 consumer warps and a 4-deep ring for the policy's
+// 96-row shape: row groups 12, 20 and 24 (BK <= 24; the X loader's last round
+// is partial for BK = 20), unpadded kernels only (measured: b_a = 24 top level
+// 27.7 -> 29.4 TF at m = 3, 24.5 -> 32.4 TF at m = 4; b_a = 20 29.6 -> 30.5 TF
+// at m = 4, 23.3 -> 24.9 at m = 3; row group 28 loses 4 %, the padded
+// variants 2 %)
 template <bool OK>
 struct Big96Sel { using type = BCSS_NP_BIG96(RG, BK_BIG, PADDED); };
 template <>
 struct Big96Sel<false> { using type = Big; };
-using Big96 = Big96Sel<(!PADDED && BK_BIG <= 28 && (96 * BK_BIG / 2) % 128 == 0)>::type;
+using Big96 = Big96Sel<(!PADDED && BK_BIG <= 24)>::type;
 using Mid = BCSS_NP_MID(RG, BK_MID, PADDED);
 template <bool OK>
 struct SmallSel { using type = BCSS_NP_SMALL(RG, BK_SMALL, PADDED); };

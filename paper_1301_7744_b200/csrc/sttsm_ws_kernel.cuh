@@ -108,7 +108,8 @@ struct WsLevelKernel {
   static constexpr int SW_SHIFT = RG >= 16 ? 0 : 1;
   static constexpr int SW_MASK = RG >= 16 ? 3 : (RG == 8 ? 1 : 0);
   static constexpr int A_STAGE = BM * LDA, B_STAGE = G * GR_SIZE;
-  static constexpr int NA = (BM * BK / 2) / PT;  // X pairs per producer thread per stage
+  static constexpr int NA = (BM * BK / 2 + PT - 1) / PT;  // X pairs per producer thread per stage
+  static constexpr bool NA_EXACT = (BM * BK / 2) % PT == 0;  // (else the last round is partial)
   static constexpr int GP = RG * BN / 2;         // B pairs per group
   // column runs of at least 2^BULK_MIN_LG doubles go through bulk copies
   // (measured after the producer's addressing was hoisted: >= 512 B runs pay
@@ -128,7 +129,7 @@ struct WsLevelKernel {
                                        (BN / CSTEP_) * sizeof(int);  // mirrored level 0: digit_rev(i * CSTEP)
   static_assert(BM <= PT, "one producer thread per output row");
   static_assert(WTM % 8 == 0 && WTN % 8 == 0, "tile shape");
-  static_assert((BM * BK / 2) % PT == 0 && (BK * BN / 2) % PT == 0 && GP % 32 == 0, "loader balance");
+  static_assert((BK * BN / 2) % PT == 0 && GP % 32 == 0, "loader balance");
   static_assert(POW2 ? ((1 << LBA) == BA && RG % 4 == 0) : (RG % 4 == 0 && BK % RG == 0 && !GEN),
                 "BA must be a power of two in 4..64 (or, !POW2, a row group dividing BK)");
   static_assert(SMEM_BYTES <= 232448, "shared memory per CTA");
@@ -341,6 +342,7 @@ struct WsLevelKernel {
 #pragma unroll
     for (int u = 0; u < NA; ++u) {
       const int idx = ptid + u * PT;
+      if (!NA_EXACT && idx >= BM * BK / 2) break;
       const int r = idx / (BK / 2), c = (idx % (BK / 2)) * 2;
       const int rr = t.mt * BM + r;
       const bool ok = (rr < t.rows) && (k0 + c < a.n);
